@@ -1,0 +1,157 @@
+/*
+ * fermiforge B200 C ABI -- the drop-in boundary of the finite-temperature
+ * density-matrix builder (MLSP2 recursion) on sm_100a.
+ *
+ * Plain C: pointers, sizes, doubles.  No C++ or CUDA types in any signature
+ * (streams are passed as `void*` = cudaStream_t).  Implemented by
+ * paper_2605_08523_b200/lib/libfermiforge_b200.so (hand-written sm_100a CUDA,
+ * no CPU fallback: every compute entry point returns FFG_ERR_CUDA when no
+ * sm_100 device is present).
+ *
+ * Each entry point replaces a reference interface.  The reference specifies the
+ * matrix path in SPEC.md (module matrix_engine / workflow) on top of the
+ * proj/core types; citations are file:line relative to the reference root:
+ *
+ *   ffg_spectral_bounds        SPEC.md:319-327  spectral_bounds(H) -> SpectralBounds
+ *   ffg_in_region_of_validity  SPEC.md:349-357  in_region_of_validity(beta', mu', beta0, mu0)
+ *   ffg_apply_model            SPEC.md:359-367  apply_model(H0, m, mode)
+ *   ffg_mixed_square           SPEC.md:369-377  mixed_square(X)
+ *   ffg_density_statistics     SPEC.md:389-397  density_statistics(D)
+ *   ffg_density_matrix         SPEC.md:458-462  compute_density_matrix(H, beta, mu, lib, mode)
+ *                              (model already selected; the B200 north-star entry
+ *                              "H, mu, kT, coefficients -> D, Tr D")
+ *   ffg_density_matrices       batched compute_density_matrix (no reference
+ *                              counterpart)
+ *   ffg_density_matrices_dev   the same on device-resident buffers, asynchronous
+ *                              on a caller stream
+ *
+ * Coefficients are the reference's Mlsp2Coefficients rows
+ * (proj/core/include/fermiforge/scalar_models.hpp:80-88: a, b, c, d per layer)
+ * with ModelCoefficients::trained_at = (beta0, mu0) (scalar_models.hpp:173-183).
+ * The model is evaluated exactly as evaluate_model (scalar_models.cpp:330-333,
+ * 243-252): X0 = (1 - mu0) I - (beta/beta0)(H - mu I); per layer
+ * A += d X; X = a X^2 + b X + c I; D = A + X.
+ *
+ * Errors: every function returns an ffg_status; ffg_last_error() gives a
+ * thread-local message naming the violated condition, mirroring the reference
+ * exceptions (ValidationError scalar_models.hpp:21-24, out-of-region SPEC.md:343,
+ * DivergedEvaluationError trainer.hpp:20-25, HalfRangeError half_precision.hpp:13-16,
+ * std::invalid_argument on dimension mismatch symmetric_matrix.cpp:31).
+ *
+ * Threading: every entry point is re-entrant; device workspaces are cached
+ * per (device, stream) under a mutex.  All reductions are fixed-order, so
+ * results are bit-reproducible for a given device, n and batch.
+ */
+#ifndef FERMIFORGE_FFG_H
+#define FERMIFORGE_FFG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFG_ABI_VERSION 1
+
+typedef enum ffg_status {
+    FFG_OK = 0,
+    FFG_ERR_VALIDATION = 1,    /* ValidationError: bad coefficients / kT / mode / sizes   */
+    FFG_ERR_OUT_OF_REGION = 2, /* rescale_to_model: (beta', mu') outside Eq. 41            */
+    FFG_ERR_DIVERGED = 3,      /* non-finite entry mid-recursion (layer in provenance)     */
+    FFG_ERR_HALF_RANGE = 4,    /* binary16 split overflow (HalfRangeError)                 */
+    FFG_ERR_UNSUPPORTED = 5,   /* DOUBLE / SINGLE modes stay on the CPU reference          */
+    FFG_ERR_DIMENSION = 6,     /* std::invalid_argument: dimension mismatch                */
+    FFG_ERR_CUDA = 7,          /* no sm_100 device, launch or allocation failure           */
+    FFG_ERR_NCCL = 8
+} ffg_status;
+
+/* PrecisionMode plus the two north-star low-precision modes. */
+typedef enum ffg_mode {
+    FFG_MODE_DOUBLE = 0,          /* not on the GPU path -> FFG_ERR_UNSUPPORTED             */
+    FFG_MODE_SINGLE = 1,          /* not on the GPU path -> FFG_ERR_UNSUPPORTED             */
+    FFG_MODE_MIXED_EMULATED = 2,  /* FP32-emulated: binary16 hi/lo split (x 2^14 pre-scale),
+                                     hi*hi + hi*lo + lo*hi with FP32 accumulation (Eq. 48) */
+    FFG_MODE_BF16 = 3,            /* one bf16 product per square, FP32 accumulation          */
+    FFG_MODE_FP16 = 4             /* one binary16 product per square (x 2^14), FP32 accum.   */
+} ffg_mode;
+
+/* An MLSP2 ModelCoefficients, borrowed for the duration of a call. */
+typedef struct ffg_model {
+    const double* abcd; /* n_layers rows of {a, b, c, d}                          */
+    int32_t n_layers;   /* >= 1                                                   */
+    double beta0;       /* trained_at.beta  (> 0, finite)                         */
+    double mu0;         /* trained_at.mu    (in (0, 1))                           */
+} ffg_model;
+
+/* Provenance record. */
+typedef struct ffg_provenance {
+    double eps_min, eps_max;  /* widened Gershgorin bounds of H                         */
+    double beta_prime;        /* SPEC normalize_problem: beta' = (eps_max - eps_min) beta */
+    double mu_prime;          /* SPEC (flipped) mu' = (eps_max - mu) / (eps_max - eps_min) */
+    double x_min, x_max;      /* bounds mapped into the model's un-flipped frame:
+                                 x = mu0 + (beta/beta0)(eps - mu); valid iff in [0,1]    */
+    int32_t mode;
+    int32_t n_layers;
+    int64_t half_products;    /* tensor-core products per density matrix: 3L / L / L   */
+    int32_t diverged_layer;   /* first X_k (k = 0..L) non-finite, -1 if none              */
+    int32_t half_range_layer; /* first X_k whose binary16 split overflowed, -1 if none    */
+    int32_t status;           /* ffg_status of this matrix                                */
+    int32_t n;
+    double device_ms;         /* device time: rescale + L layers + statistics            */
+} ffg_provenance;
+
+int ffg_abi_version(void);
+const char* ffg_last_error(void);
+/* 1 when an sm_100 device is usable, else 0 (ffg_last_error says why). */
+int ffg_device_available(void);
+
+/* SPEC.md:349-357, Eq. 41: (mu0/mu')beta0 >= beta' and ((1-mu0)/(1-mu'))beta0 >= beta',
+ * with mu' in the reference model's UN-flipped frame (mu' = (mu - eps_min)/W).
+ * Returns 1 valid / 0 not valid.  Pure host function. */
+int ffg_in_region_of_validity(double beta_prime, double mu_prime, double beta0, double mu0);
+
+/* Gershgorin bounds of a host matrix, computed on the device (K1). */
+int ffg_spectral_bounds(const double* H, int64_t n, double* eps_min, double* eps_max);
+
+/* D = p(H0) for H0 already in the model frame (SPEC apply_model).  D_out n*n. */
+int ffg_apply_model(const double* H0, int64_t n, const ffg_model* model, int32_t mode,
+                    double* D_out, ffg_provenance* prov);
+
+/* Y = mixed_square(X) on the tensor cores (one FP32-emulated square, fp32 in/out). */
+int ffg_mixed_square(const float* X, int64_t n, float* Y_out);
+
+/* (Tr D, sum_ij D_ij^2) of a host matrix (fixed-order device reduction). */
+int ffg_density_statistics(const double* D, int64_t n, double* stats_out);
+
+/* North-star entry: H (n*n row-major fp64, exactly symmetric), mu, kT -> D, stats.
+ * D_out may be NULL (statistics only).  stats_out = {Tr D, Tr D^2}, may be NULL. */
+int ffg_density_matrix(const double* H, int64_t n, double mu, double kT, const ffg_model* model,
+                       int32_t mode, double* D_out, double* stats_out, ffg_provenance* prov);
+
+/* Batched: `batch` independent H (host pointers), per-matrix mu / kT.
+ * D_out may be NULL or hold NULL entries; stats_out batch*2; prov batch entries or NULL.
+ * Returns FFG_OK when every matrix succeeded, else the first failing status. */
+int ffg_density_matrices(int32_t batch, const double* const* H, int64_t n, const double* mu,
+                         const double* kT, const ffg_model* model, int32_t mode,
+                         double* const* D_out, double* stats_out, ffg_provenance* prov);
+
+/* Device-resident batch, asynchronous on `stream` (cudaStream_t, NULL = default):
+ * H_dev [batch][n][n] fp64; mu / kT host arrays (copied at call time);
+ * D_dev [batch][n][n] fp64 or NULL; stats_dev [batch][2]; status_dev [batch] int32
+ * (ffg_status per matrix); bounds_dev [batch][4] (eps_min, eps_max, x_min, x_max)
+ * or NULL.  Returns after enqueueing; host-side validation errors are synchronous. */
+int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, const double* mu,
+                             const double* kT, const ffg_model* model, int32_t mode,
+                             double* D_dev, double* stats_dev, int32_t* status_dev,
+                             double* bounds_dev, void* stream);
+
+/* Number of kernels ffg_density_matrices_dev launches for one call (for accounting). */
+int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, int32_t mode);
+
+/* Release cached device workspaces of the calling process. */
+void ffg_release_workspaces(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FERMIFORGE_FFG_H */

@@ -1,0 +1,740 @@
+// Host side of the fermiforge B200 C ABI (include/fermiforge/ffg.h).
+//
+// Validation mirrors the reference (ModelCoefficients::validate
+// scalar_models.cpp:133-171, FermiParams::validate :27-34); then the device
+// pipeline  reset -> K1 rescale_gershgorin -> L x K2 mlsp2_layer -> K3 finalize
+// is enqueued on one stream.  No CPU fallback: without an sm_100 device every
+// compute entry point fails with FFG_ERR_CUDA.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fermiforge/ffg.h"
+#include "kernels.cuh"
+
+using namespace ffg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess)                                                                 \
+            return set_err(FFG_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+                           __LINE__);                                                          \
+    } while (0)
+
+// --------------------------------------------------------------------- validation
+int validate_model(const ffg_model* m) {
+    if (!m || !m->abcd) return set_err(FFG_ERR_VALIDATION, "ModelCoefficients: model is null");
+    if (!(m->beta0 > 0.0) || !std::isfinite(m->beta0))
+        return set_err(FFG_ERR_VALIDATION, "FermiParams: beta must be positive and finite");
+    if (!std::isfinite(m->mu0)) return set_err(FFG_ERR_VALIDATION, "FermiParams: mu must be finite");
+    if (!(m->mu0 > 0.0 && m->mu0 < 1.0))
+        return set_err(FFG_ERR_VALIDATION, "ModelCoefficients: mu0 must lie in (0,1)");
+    if (m->n_layers < 1)
+        return set_err(FFG_ERR_VALIDATION, "ModelCoefficients: MLSP2 needs at least one layer");
+    for (int i = 0; i < 4 * m->n_layers; ++i)
+        if (!std::isfinite(m->abcd[i]))
+            return set_err(FFG_ERR_VALIDATION, "ModelCoefficients: MLSP2 coefficients must be finite");
+    return FFG_OK;
+}
+
+int mode_to_internal(int32_t mode, int* out) {
+    switch (mode) {
+        case FFG_MODE_MIXED_EMULATED: *out = kModeF32E; return FFG_OK;
+        case FFG_MODE_FP16: *out = kModeF16; return FFG_OK;
+        case FFG_MODE_BF16: *out = kModeBF16; return FFG_OK;
+        case FFG_MODE_DOUBLE:
+        case FFG_MODE_SINGLE:
+            return set_err(FFG_ERR_UNSUPPORTED,
+                           "PrecisionMode %d (DOUBLE/SINGLE) is not a tensor-core mode; "
+                           "use MIXED_EMULATED, BF16 or FP16", mode);
+        default: return set_err(FFG_ERR_VALIDATION, "unknown PrecisionMode %d", mode);
+    }
+}
+
+int validate_n(int64_t n) {
+    if (n < 1) return set_err(FFG_ERR_DIMENSION, "matrix dimension must be >= 1 (got %lld)", (long long)n);
+    if (n > 65536) return set_err(FFG_ERR_DIMENSION, "matrix dimension %lld exceeds 65536", (long long)n);
+    return FFG_OK;
+}
+
+int check_device(int* dev_out) {
+    int dev = 0, count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return set_err(FFG_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    CK(cudaGetDevice(&dev));
+    int major = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10)
+        return set_err(FFG_ERR_CUDA, "device %d is sm_%d0; this library is built for sm_100a only", dev, major);
+    *dev_out = dev;
+    return FFG_OK;
+}
+
+// --------------------------------------------------------------------- tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 16-bit operand matrix [rows][np] viewed by TMA as 128-row x 64-col boxes, 128B swizzle.
+int make_operand_map(CUtensorMap* tm, void* base, int64_t rows, int64_t np) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return set_err(FFG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)np, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)np * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(FFG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return FFG_OK;
+}
+
+// --------------------------------------------------------------------- workspace
+struct Workspace {
+    int device = -1;
+    size_t cap_elems = 0;  // B * np * np
+    int cap_B = 0;
+    size_t cap_T = 0;      // B * T
+    size_t cap_h = 0;      // staging elements (B * n * n)
+    float* X = nullptr;
+    float* A = nullptr;
+    uint16_t* op[4] = {nullptr, nullptr, nullptr, nullptr};  // hi0, lo0, hi1, lo1
+    double* Hs = nullptr;
+    double* Ds = nullptr;
+    double* params = nullptr;       // [4][cap_B]: alpha, gamma, scale, mu
+    double* params_host = nullptr;  // pinned mirror
+    unsigned long long* bounds = nullptr;
+    int* flags = nullptr;
+    double2* partials = nullptr;
+    double* stats = nullptr;
+    double* bounds_out = nullptr;
+    int* status = nullptr;
+    void* host_small = nullptr;     // pinned readback: stats, bounds, status, flags
+    size_t host_small_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // tensor-map cache
+    int tm_B = -1, tm_np = -1;
+    CUtensorMap tm[4];
+    std::mutex mu;
+};
+
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
+
+Workspace* get_ws(int dev, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto key = std::make_pair(dev, st);
+    auto it = g_ws.find(key);
+    if (it != g_ws.end()) return it->second;
+    Workspace* w = new Workspace();
+    w->device = dev;
+    g_ws[key] = w;
+    return w;
+}
+
+void free_ws(Workspace* w) {
+    cudaFree(w->X);
+    cudaFree(w->A);
+    for (auto& p : w->op) cudaFree(p);
+    cudaFree(w->Hs);
+    cudaFree(w->Ds);
+    cudaFree(w->params);
+    cudaFreeHost(w->params_host);
+    cudaFree(w->bounds);
+    cudaFree(w->flags);
+    cudaFree(w->partials);
+    cudaFree(w->stats);
+    cudaFree(w->bounds_out);
+    cudaFree(w->status);
+    cudaFreeHost(w->host_small);
+    if (w->ev0) cudaEventDestroy(w->ev0);
+    if (w->ev1) cudaEventDestroy(w->ev1);
+}
+
+template <typename T>
+int grow(T** p, size_t& cap_field_unused, size_t n) {
+    (void)cap_field_unused;
+    cudaFree(*p);
+    *p = nullptr;
+    CK(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T)));
+    return FFG_OK;
+}
+
+int ensure(Workspace& w, int B, int64_t np, int64_t T, bool operands) {
+    size_t dummy = 0;
+    if (!w.ev0) {
+        CK(cudaEventCreate(&w.ev0));
+        CK(cudaEventCreate(&w.ev1));
+    }
+    const size_t elems = (size_t)B * np * np;
+    if (operands && elems > w.cap_elems) {
+        int rc;
+        if ((rc = grow(&w.X, dummy, elems))) return rc;
+        if ((rc = grow(&w.A, dummy, elems))) return rc;
+        for (auto& p : w.op)
+            if ((rc = grow(&p, dummy, elems))) return rc;
+        w.cap_elems = elems;
+        w.tm_B = -1;
+    }
+    if (B > w.cap_B) {
+        int rc;
+        if ((rc = grow(&w.params, dummy, (size_t)4 * B))) return rc;
+        cudaFreeHost(w.params_host);
+        CK(cudaMallocHost(&w.params_host, sizeof(double) * 4 * B));
+        if ((rc = grow(&w.bounds, dummy, (size_t)2 * B))) return rc;
+        if ((rc = grow(&w.flags, dummy, (size_t)2 * B))) return rc;
+        if ((rc = grow(&w.stats, dummy, (size_t)2 * B))) return rc;
+        if ((rc = grow(&w.bounds_out, dummy, (size_t)4 * B))) return rc;
+        if ((rc = grow(&w.status, dummy, (size_t)B))) return rc;
+        cudaFreeHost(w.host_small);
+        w.host_small_bytes = (size_t)B * (2 * 8 + 4 * 8 + 4 + 8);
+        CK(cudaMallocHost(&w.host_small, w.host_small_bytes));
+        w.cap_B = B;
+    }
+    if ((size_t)B * T > w.cap_T) {
+        int rc;
+        if ((rc = grow(&w.partials, dummy, (size_t)B * T))) return rc;
+        w.cap_T = (size_t)B * T;
+    }
+    return FFG_OK;
+}
+
+int ensure_staging(Workspace& w, size_t elems) {
+    size_t dummy = 0;
+    if (elems > w.cap_h) {
+        int rc;
+        if ((rc = grow(&w.Hs, dummy, elems))) return rc;
+        if ((rc = grow(&w.Ds, dummy, elems))) return rc;
+        w.cap_h = elems;
+    }
+    return FFG_OK;
+}
+
+// --------------------------------------------------------------------- small kernels
+__global__ void reset_kernel(unsigned long long* bounds, int* flags, int B) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < B) {
+        bounds[2 * m + 0] = ~0ull;
+        bounds[2 * m + 1] = 0ull;
+        flags[2 * m + 0] = INT_MAX;
+        flags[2 * m + 1] = INT_MAX;
+    }
+}
+
+// Per-row (diag, sum of squares) partials of a full fp64 matrix, one warp per row.
+__global__ void row_stats_kernel(const double* D, int n, double2* partials) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * 8 + warp;
+    if (i >= n) return;
+    double sq = 0.0, dg = 0.0;
+    for (int j = lane; j < n; j += 32) {
+        const double v = D[(size_t)i * n + j];
+        sq += v * v;
+        if (j == i) dg = v;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        dg += __shfl_xor_sync(0xffffffffu, dg, o);
+    }
+    if (lane == 0) partials[i] = make_double2(dg, sq);
+}
+
+template <int MODE>
+int launch_layer(const CUtensorMap& hi, const CUtensorMap& lo, const LayerParams& p, int grid,
+                 cudaStream_t st) {
+    static bool configured = false;
+    constexpr int smem = layer_smem_bytes<MODE>();
+    if (!configured) {
+        CK(cudaFuncSetAttribute(mlsp2_layer_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured = true;
+    }
+    mlsp2_layer_kernel<MODE><<<grid, 192, smem, st>>>(hi, lo, p);
+    CK(cudaGetLastError());
+    return FFG_OK;
+}
+
+struct Job {
+    int B = 0;
+    int64_t n = 0;
+    const double* H_dev = nullptr;      // [B][n][n]
+    const double* alpha = nullptr;      // host [B]
+    const double* gamma = nullptr;      // host [B]
+    const double* scale = nullptr;      // host [B] or null (no validity check)
+    const double* mu = nullptr;         // host [B] or null
+    const ffg_model* model = nullptr;
+    int mode = kModeF32E;
+    double* D_dev = nullptr;            // [B][n][n] or null
+    double* stats_dev = nullptr;        // [B][2] or null (-> workspace)
+    int* status_dev = nullptr;          // [B] or null (-> workspace)
+    double* bounds_dev = nullptr;       // [B][4] or null (-> workspace)
+};
+
+// Enqueue the full pipeline for one batch on `st`.  Host-synchronous only for
+// the tiny per-matrix parameter upload (pinned, async).
+int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
+    const int B = j.B;
+    const int64_t n = j.n;
+    const int64_t np = (n + kBM - 1) / kBM * kBM;
+    const int nb = (int)(np / kBM);
+    const int64_t T = (int64_t)nb * (nb + 1) / 2;
+    int rc;
+    if ((rc = ensure(w, B, np, T, true))) return rc;
+    if (w.tm_B != B || w.tm_np != (int)np) {
+        for (int k = 0; k < 4; ++k)
+            if ((rc = make_operand_map(&w.tm[k], w.op[k], (int64_t)B * np, np))) return rc;
+        w.tm_B = B;
+        w.tm_np = (int)np;
+    }
+    // per-matrix parameters
+    double* ph = w.params_host;
+    for (int m = 0; m < B; ++m) {
+        ph[0 * B + m] = j.alpha[m];
+        ph[1 * B + m] = j.gamma[m];
+        ph[2 * B + m] = j.scale ? j.scale[m] : 0.0;
+        ph[3 * B + m] = j.mu ? j.mu[m] : 0.0;
+    }
+    CK(cudaMemcpyAsync(w.params, ph, sizeof(double) * 4 * B, cudaMemcpyHostToDevice, st));
+    reset_kernel<<<(B + 127) / 128, 128, 0, st>>>(w.bounds, w.flags, B);
+    CK(cudaGetLastError());
+
+    const ffg_model& md = *j.model;
+    RescaleParams rp{};
+    rp.H = j.H_dev;
+    rp.alpha = w.params;
+    rp.gamma = w.params + B;
+    rp.d0 = md.abcd[3];
+    rp.X = w.X;
+    rp.A = w.A;
+    rp.hi = w.op[0];
+    rp.lo = w.op[1];
+    rp.bounds = w.bounds;
+    rp.flags = w.flags;
+    rp.n = (int)n;
+    rp.np = (int)np;
+    rp.mode = j.mode;
+    rp.write_operands = 1;
+    rescale_gershgorin_kernel<<<dim3((unsigned)(np / 8), (unsigned)B), 256, 0, st>>>(rp);
+    CK(cudaGetLastError());
+
+    for (int l = 0; l < md.n_layers; ++l) {
+        const int par = l & 1;
+        LayerParams lp{};
+        lp.X = w.X;
+        lp.A = w.A;
+        lp.hi_dst = w.op[2 * (par ^ 1) + 0];
+        lp.lo_dst = w.op[2 * (par ^ 1) + 1];
+        lp.D = j.D_dev;
+        lp.partials = w.partials;
+        lp.flags = w.flags;
+        lp.a = md.abcd[4 * l + 0];
+        lp.b = md.abcd[4 * l + 1];
+        lp.c = md.abcd[4 * l + 2];
+        lp.last = (l == md.n_layers - 1);
+        lp.d_next = lp.last ? 0.0 : md.abcd[4 * (l + 1) + 3];
+        lp.n = (int)n;
+        lp.np = (int)np;
+        lp.nb = nb;
+        lp.T = (int)T;
+        lp.layer = l;
+        const CUtensorMap& thi = w.tm[2 * par + 0];
+        const CUtensorMap& tlo = w.tm[2 * par + 1];
+        const int grid = (int)(B * T);
+        switch (j.mode) {
+            case kModeF32E: rc = launch_layer<kModeF32E>(thi, tlo, lp, grid, st); break;
+            case kModeF16: rc = launch_layer<kModeF16>(thi, tlo, lp, grid, st); break;
+            default: rc = launch_layer<kModeBF16>(thi, tlo, lp, grid, st); break;
+        }
+        if (rc) return rc;
+    }
+    FinalizeParams fp{};
+    fp.partials = w.partials;
+    fp.bounds = w.bounds;
+    fp.flags = w.flags;
+    fp.scale = j.scale ? w.params + 2 * B : nullptr;
+    fp.mu = w.params + 3 * B;
+    fp.mu0 = md.mu0;
+    fp.T = (int)T;
+    fp.B = B;
+    fp.stats = j.stats_dev ? j.stats_dev : w.stats;
+    fp.bounds_out = j.bounds_dev ? j.bounds_dev : w.bounds_out;
+    fp.status = j.status_dev ? j.status_dev : w.status;
+    finalize_stats_kernel<<<B, 256, 0, st>>>(fp);
+    CK(cudaGetLastError());
+    return FFG_OK;
+}
+
+cudaStream_t lib_stream() {
+    static cudaStream_t s = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] { cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); });
+    return s;
+}
+
+void fill_prov(ffg_provenance* pv, const double* bnd, const double* kT, double mu, int status,
+               const int* flags, const ffg_model* md, int mode_api, int n, double ms) {
+    pv->eps_min = bnd[0];
+    pv->eps_max = bnd[1];
+    pv->x_min = bnd[2];
+    pv->x_max = bnd[3];
+    const double W = bnd[1] - bnd[0];
+    pv->beta_prime = kT ? W / *kT : 0.0;
+    pv->mu_prime = W > 0 ? (bnd[1] - mu) / W : 0.0;
+    pv->mode = mode_api;
+    pv->n_layers = md->n_layers;
+    pv->half_products = (int64_t)md->n_layers * (mode_api == FFG_MODE_MIXED_EMULATED ? 3 : 1);
+    pv->diverged_layer = flags[0] == INT_MAX ? -1 : flags[0];
+    pv->half_range_layer = flags[1] == INT_MAX ? -1 : flags[1];
+    pv->status = status;
+    pv->n = n;
+    pv->device_ms = ms;
+}
+
+const char* status_text(int st) {
+    switch (st) {
+        case FFG_ERR_OUT_OF_REGION: return "out of region of validity";
+        case FFG_ERR_DIVERGED: return "non-finite entry mid-recursion";
+        case FFG_ERR_HALF_RANGE: return "binary16 split overflow";
+        default: return "error";
+    }
+}
+
+// Host-buffer driver shared by density_matrix(ces) / apply_model / mixed_square.
+int run_host(int B, const double* const* H, int64_t n, const double* alpha, const double* gamma,
+             const double* scale, const double* mu, const double* kT, const ffg_model* md,
+             int mode_api, double* const* D_out, double* stats_out, ffg_provenance* prov) {
+    int rc, dev, mode;
+    if ((rc = validate_model(md))) return rc;
+    if ((rc = mode_to_internal(mode_api, &mode))) return rc;
+    if ((rc = validate_n(n))) return rc;
+    if (B < 1) return set_err(FFG_ERR_DIMENSION, "batch must be >= 1");
+    for (int m = 0; m < B; ++m)
+        if (!H[m]) return set_err(FFG_ERR_VALIDATION, "H[%d] is null", m);
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    const size_t nn = (size_t)n * n;
+    if ((rc = ensure_staging(w, (size_t)B * nn))) return rc;
+    const int64_t np = (n + kBM - 1) / kBM * kBM;
+    const int64_t T = (np / kBM) * (np / kBM + 1) / 2;
+    if ((rc = ensure(w, B, np, T, true))) return rc;
+    for (int m = 0; m < B; ++m)
+        CK(cudaMemcpyAsync(w.Hs + m * nn, H[m], nn * sizeof(double), cudaMemcpyHostToDevice, st));
+    bool want_D = false;
+    if (D_out)
+        for (int m = 0; m < B; ++m) want_D |= D_out[m] != nullptr;
+    Job j;
+    j.B = B;
+    j.n = n;
+    j.H_dev = w.Hs;
+    j.alpha = alpha;
+    j.gamma = gamma;
+    j.scale = scale;
+    j.mu = mu;
+    j.model = md;
+    j.mode = mode;
+    j.D_dev = want_D ? w.Ds : nullptr;
+    CK(cudaEventRecord(w.ev0, st));
+    if ((rc = enqueue(w, j, st))) return rc;
+    CK(cudaEventRecord(w.ev1, st));
+    if (want_D)
+        for (int m = 0; m < B; ++m)
+            if (D_out[m])
+                CK(cudaMemcpyAsync(D_out[m], w.Ds + m * nn, nn * sizeof(double),
+                                   cudaMemcpyDeviceToHost, st));
+    uint8_t* hs = static_cast<uint8_t*>(w.host_small);
+    double* h_stats = reinterpret_cast<double*>(hs);
+    double* h_bounds = h_stats + 2 * B;
+    int* h_status = reinterpret_cast<int*>(h_bounds + 4 * B);
+    int* h_flags = h_status + B;
+    CK(cudaMemcpyAsync(h_stats, w.stats, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_bounds, w.bounds_out, sizeof(double) * 4 * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_status, w.status, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_flags, w.flags, sizeof(int) * 2 * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+    int first = FFG_OK, first_m = -1;
+    for (int m = 0; m < B; ++m) {
+        if (stats_out) {
+            stats_out[2 * m + 0] = h_stats[2 * m + 0];
+            stats_out[2 * m + 1] = h_stats[2 * m + 1];
+        }
+        if (prov)
+            fill_prov(&prov[m], h_bounds + 4 * m, kT ? kT + m : nullptr, mu ? mu[m] : 0.0,
+                      h_status[m], h_flags + 2 * m, md, mode_api, (int)n, ms);
+        if (h_status[m] != FFG_OK && first == FFG_OK) {
+            first = h_status[m];
+            first_m = m;
+        }
+    }
+    if (first != FFG_OK) {
+        const double* b = h_bounds + 4 * first_m;
+        if (first == FFG_ERR_OUT_OF_REGION)
+            return set_err(first, "matrix %d: out of region of validity: %s (x_min=%.17g, x_max=%.17g; "
+                           "eps=[%.17g, %.17g])", first_m,
+                           !(b[2] >= 0.0) ? "mu0 + (beta/beta0)(eps_min - mu) >= 0 violated"
+                                          : "mu0 + (beta/beta0)(eps_max - mu) <= 1 violated",
+                           b[2], b[3], b[0], b[1]);
+        const int* f = h_flags + 2 * first_m;
+        return set_err(first, "matrix %d: %s at layer %d", first_m, status_text(first),
+                       first == FFG_ERR_DIVERGED ? f[0] : f[1]);
+    }
+    return FFG_OK;
+}
+
+int check_mu_kT(int B, const double* mu, const double* kT) {
+    if (!mu || !kT) return set_err(FFG_ERR_VALIDATION, "mu / kT arrays are null");
+    for (int m = 0; m < B; ++m) {
+        if (!(kT[m] > 0.0) || !std::isfinite(kT[m]))
+            return set_err(FFG_ERR_VALIDATION, "kT[%d] must be positive and finite", m);
+        if (!std::isfinite(mu[m])) return set_err(FFG_ERR_VALIDATION, "mu[%d] must be finite", m);
+    }
+    return FFG_OK;
+}
+
+void rescale_coeffs(int B, const double* mu, const double* kT, const ffg_model* md,
+                    std::vector<double>& alpha, std::vector<double>& gamma,
+                    std::vector<double>& scale) {
+    alpha.resize(B);
+    gamma.resize(B);
+    scale.resize(B);
+    for (int m = 0; m < B; ++m) {
+        const double s = (1.0 / kT[m]) / md->beta0;
+        scale[m] = s;
+        alpha[m] = -s;
+        gamma[m] = (1.0 - md->mu0) + s * mu[m];
+    }
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int ffg_abi_version(void) { return FFG_ABI_VERSION; }
+const char* ffg_last_error(void) { return g_err.c_str(); }
+
+int ffg_device_available(void) {
+    int dev;
+    return check_device(&dev) == FFG_OK ? 1 : 0;
+}
+
+int ffg_in_region_of_validity(double beta_prime, double mu_prime, double beta0, double mu0) {
+    if (!(mu_prime > 0.0 && mu_prime < 1.0)) return 0;
+    return (mu0 / mu_prime) * beta0 >= beta_prime &&
+                   ((1.0 - mu0) / (1.0 - mu_prime)) * beta0 >= beta_prime
+               ? 1
+               : 0;
+}
+
+int ffg_spectral_bounds(const double* H, int64_t n, double* eps_min, double* eps_max) {
+    int rc, dev;
+    if ((rc = validate_n(n))) return rc;
+    if (!H || !eps_min || !eps_max) return set_err(FFG_ERR_VALIDATION, "null argument");
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    const size_t nn = (size_t)n * n;
+    if ((rc = ensure_staging(w, nn))) return rc;
+    if ((rc = ensure(w, 1, 128, 1, false))) return rc;
+    CK(cudaMemcpyAsync(w.Hs, H, nn * 8, cudaMemcpyHostToDevice, st));
+    reset_kernel<<<1, 32, 0, st>>>(w.bounds, w.flags, 1);
+    RescaleParams rp{};
+    double* ag = w.params_host;
+    ag[0] = 1.0;
+    ag[1] = 0.0;
+    CK(cudaMemcpyAsync(w.params, ag, 16, cudaMemcpyHostToDevice, st));
+    rp.H = w.Hs;
+    rp.alpha = w.params;
+    rp.gamma = w.params + 1;
+    rp.bounds = w.bounds;
+    rp.flags = w.flags;
+    rp.n = (int)n;
+    rp.np = (int)((n + 7) / 8 * 8);
+    rp.write_operands = 0;
+    rescale_gershgorin_kernel<<<dim3((unsigned)(rp.np / 8), 1), 256, 0, st>>>(rp);
+    CK(cudaGetLastError());
+    unsigned long long k[2];
+    CK(cudaMemcpyAsync(k, w.bounds, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double lo = key_to_double(k[0]), hi = key_to_double(k[1]);
+    const double wd = 1e-12 * (hi - lo);
+    *eps_min = lo - wd;
+    *eps_max = hi + wd;
+    return FFG_OK;
+}
+
+int ffg_apply_model(const double* H0, int64_t n, const ffg_model* model, int32_t mode,
+                    double* D_out, ffg_provenance* prov) {
+    const double alpha = -1.0, gamma = 1.0;  // X0 = I - H0 (scalar_models.cpp:333)
+    double* Dp[1] = {D_out};
+    return run_host(1, &H0, n, &alpha, &gamma, nullptr, nullptr, nullptr, model, mode, Dp,
+                    nullptr, prov);
+}
+
+int ffg_mixed_square(const float* X, int64_t n, float* Y_out) {
+    int rc;
+    if ((rc = validate_n(n))) return rc;
+    if (!X || !Y_out) return set_err(FFG_ERR_VALIDATION, "null argument");
+    const size_t nn = (size_t)n * n;
+    std::vector<double> Xd(nn), Yd(nn);
+    for (size_t e = 0; e < nn; ++e) Xd[e] = X[e];
+    const double abcd[4] = {1.0, 0.0, 0.0, 0.0};
+    ffg_model m{abcd, 1, 1.0, 0.5};
+    const double alpha = 1.0, gamma = 0.0;
+    const double* Hp[1] = {Xd.data()};
+    double* Dp[1] = {Yd.data()};
+    rc = run_host(1, Hp, n, &alpha, &gamma, nullptr, nullptr, nullptr, &m,
+                  FFG_MODE_MIXED_EMULATED, Dp, nullptr, nullptr);
+    if (rc) return rc;
+    for (size_t e = 0; e < nn; ++e) Y_out[e] = (float)Yd[e];
+    return FFG_OK;
+}
+
+int ffg_density_statistics(const double* D, int64_t n, double* stats_out) {
+    int rc, dev;
+    if ((rc = validate_n(n))) return rc;
+    if (!D || !stats_out) return set_err(FFG_ERR_VALIDATION, "null argument");
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    const size_t nn = (size_t)n * n;
+    if ((rc = ensure_staging(w, nn))) return rc;
+    if ((rc = ensure(w, 1, 128, n, false))) return rc;
+    CK(cudaMemcpyAsync(w.Hs, D, nn * 8, cudaMemcpyHostToDevice, st));
+    row_stats_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(w.Hs, (int)n, w.partials);
+    reset_kernel<<<1, 32, 0, st>>>(w.bounds, w.flags, 1);
+    FinalizeParams fp{};
+    fp.partials = w.partials;
+    fp.bounds = w.bounds;
+    fp.flags = w.flags;
+    fp.scale = nullptr;
+    fp.mu = nullptr;
+    fp.T = (int)n;
+    fp.B = 1;
+    fp.stats = w.stats;
+    fp.bounds_out = w.bounds_out;
+    fp.status = w.status;
+    finalize_stats_kernel<<<1, 256, 0, st>>>(fp);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(stats_out, w.stats, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return FFG_OK;
+}
+
+int ffg_density_matrix(const double* H, int64_t n, double mu, double kT, const ffg_model* model,
+                       int32_t mode, double* D_out, double* stats_out, ffg_provenance* prov) {
+    double* Dp[1] = {D_out};
+    return ffg_density_matrices(1, &H, n, &mu, &kT, model, mode, Dp, stats_out, prov);
+}
+
+int ffg_density_matrices(int32_t batch, const double* const* H, int64_t n, const double* mu,
+                         const double* kT, const ffg_model* model, int32_t mode,
+                         double* const* D_out, double* stats_out, ffg_provenance* prov) {
+    int rc;
+    if (batch < 1) return set_err(FFG_ERR_DIMENSION, "batch must be >= 1");
+    if (!H) return set_err(FFG_ERR_VALIDATION, "H is null");
+    if ((rc = validate_model(model))) return rc;
+    if ((rc = check_mu_kT(batch, mu, kT))) return rc;
+    std::vector<double> alpha, gamma, scale;
+    rescale_coeffs(batch, mu, kT, model, alpha, gamma, scale);
+    return run_host(batch, H, n, alpha.data(), gamma.data(), scale.data(), mu, kT, model, mode,
+                    D_out, stats_out, prov);
+}
+
+int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, const double* mu,
+                             const double* kT, const ffg_model* model, int32_t mode,
+                             double* D_dev, double* stats_dev, int32_t* status_dev,
+                             double* bounds_dev, void* stream) {
+    int rc, dev, imode;
+    if (batch < 1) return set_err(FFG_ERR_DIMENSION, "batch must be >= 1");
+    if (!H_dev) return set_err(FFG_ERR_VALIDATION, "H_dev is null");
+    if ((rc = validate_model(model))) return rc;
+    if ((rc = mode_to_internal(mode, &imode))) return rc;
+    if ((rc = validate_n(n))) return rc;
+    if ((rc = check_mu_kT(batch, mu, kT))) return rc;
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    std::vector<double> alpha, gamma, scale;
+    rescale_coeffs(batch, mu, kT, model, alpha, gamma, scale);
+    Job j;
+    j.B = batch;
+    j.n = n;
+    j.H_dev = H_dev;
+    j.alpha = alpha.data();
+    j.gamma = gamma.data();
+    j.scale = scale.data();
+    j.mu = mu;
+    j.model = model;
+    j.mode = imode;
+    j.D_dev = D_dev;
+    j.stats_dev = stats_dev;
+    j.status_dev = status_dev;
+    j.bounds_dev = bounds_dev;
+    return enqueue(w, j, st);
+}
+
+int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, int32_t mode) {
+    (void)batch;
+    (void)n;
+    (void)mode;
+    if (!model) return 0;
+    return 3 + (int64_t)model->n_layers;  // reset + K1 + L x K2 + K3
+}
+
+void ffg_release_workspaces(void) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto& kv : g_ws) {
+        free_ws(kv.second);
+        delete kv.second;
+    }
+    g_ws.clear();
+}
+
+}  // extern "C"

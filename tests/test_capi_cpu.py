@@ -1,0 +1,90 @@
+"""CPU tests of the C-ABI boundary: the library loads, exports every symbol the
+header declares, validates inputs like the reference, and refuses to compute
+without an sm_100 device (no CPU fallback)."""
+import ctypes
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2605_08523_b200 import engine as E
+
+HEADER = "include/fermiforge/ffg.h"
+
+
+def declared_symbols():
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    txt = open(os.path.join(root, HEADER)).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(ffg_\w+)\(", txt, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    out = subprocess.run(["nm", "-D", "--defined-only", E.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (ffg_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert set(E.SYMBOLS) <= exported
+    L = E.lib()
+    for s in syms:
+        assert hasattr(L, s)
+
+
+def test_binary_contains_tcgen05_and_tma():
+    sass = subprocess.run(["cuobjdump", "-sass", E.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass, "no tcgen05.mma in the product library"
+    assert "UTMALDG" in sass, "no TMA loads in the product library"
+    assert "LDTM" in sass, "no tcgen05.ld in the product library"
+    assert "HMMA" not in re.sub(r"UTCHMMA", "", sass), "legacy mma.sync found"
+
+
+def test_validation_mirrors_reference():
+    m = E.load_model("M1500")
+    H = np.eye(8)
+    with pytest.raises(E.ValidationError, match="kT"):
+        E.compute_density_matrix(H, 0.0, 0.0, m)
+    with pytest.raises(E.ValidationError, match="mu0 must lie in"):
+        E.compute_density_matrix(H, 0.0, 0.01, E.Mlsp2Model(m.abcd, 1500.0, 1.0))
+    with pytest.raises(E.ValidationError, match="beta must be positive"):
+        E.compute_density_matrix(H, 0.0, 0.01, E.Mlsp2Model(m.abcd, -1.0, 0.3))
+    bad = m.abcd.copy()
+    bad[3, 1] = np.nan
+    with pytest.raises(E.ValidationError, match="finite"):
+        E.compute_density_matrix(H, 0.0, 0.01, E.Mlsp2Model(bad, 1500.0, 1 / 3))
+    with pytest.raises(E.DimensionError):
+        E.compute_density_matrix(np.zeros((3, 4)), 0.0, 0.01, m)
+    with pytest.raises(E.DimensionError):
+        E.compute_density_matrices([np.eye(4), np.eye(5)], 0.0, 0.01, m)
+
+
+def test_modes():
+    m = E.load_model("M1500")
+    if E.device_available():
+        pytest.skip("device present")
+    for mode in (E.PrecisionMode.DOUBLE, E.PrecisionMode.SINGLE):
+        with pytest.raises(E.UnsupportedModeError):
+            E.lib()  # noqa
+            m_c = m._c()
+            rc = E.lib().ffg_density_matrix(E._dp(np.eye(4)), 4, 0.0, 0.01, ctypes.byref(m_c), int(mode),
+                                            None, None, None)
+            E._check(rc)
+
+
+def test_no_cpu_fallback_without_device():
+    if E.device_available():
+        pytest.skip("device present")
+    m = E.load_model("M1500")
+    with pytest.raises(E.CudaError):
+        E.compute_density_matrix(np.eye(8) * 0.1, 0.0, 0.01, m)
+    with pytest.raises(E.CudaError):
+        E.mixed_square(np.eye(8, dtype=np.float32))
+
+
+def test_kernel_launch_accounting():
+    m = E.load_model("M1500")
+    assert E.kernel_launches(1, 1024, m) == 3 + 30
+    assert E.algorithmic_flops(4096, 30, E.PrecisionMode.MIXED_EMULATED) == pytest.approx(6.19e12, rel=1e-3)
+    assert E.algorithmic_flops(1024, 30, E.PrecisionMode.BF16) == pytest.approx(3.22e10, rel=1e-2)

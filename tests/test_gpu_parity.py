@@ -1,0 +1,248 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tolerances, vs the fp64 recursion on identical inputs:
+  MIXED_EMULATED (FP32-emulated): max|dD| <= 5e-6, ||dD||_F/||D||_F <= 1e-5, |dTr|/Tr <= 1e-6
+  BF16:                           max|dD| <= 1e-1,                          |dTr|/Tr <= 1e-2
+  FP16:                           max|dD| <= 1e-2,                          |dTr|/Tr <= 1e-3
+Integer-exact cases (exact-half inputs of mixed_square, Gershgorin bounds of the
+tight-binding family) are bit-exact.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2605_08523_b200 import engine as E
+from paper_2605_08523_b200.hamiltonians import tight_binding, goe, batch_params
+
+pytestmark = pytest.mark.gpu
+
+TOL = {
+    E.PrecisionMode.MIXED_EMULATED: dict(max=5e-6, fro=1e-5, tr=1e-6),
+    E.PrecisionMode.BF16: dict(max=1e-1, fro=None, tr=1e-2),
+    E.PrecisionMode.FP16: dict(max=1e-2, fro=None, tr=1e-3),
+}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_device():
+    if not E.device_available():
+        pytest.fail("no sm_100 device: " + E.lib().ffg_last_error().decode())
+
+
+@pytest.fixture(scope="module")
+def model():
+    return E.load_model("M1500")
+
+
+def errors(D, Dref):
+    dD = D - Dref
+    return (float(np.abs(dD).max()), float(np.linalg.norm(dD) / np.linalg.norm(Dref)),
+            float(abs(np.trace(D) - np.trace(Dref)) / abs(np.trace(Dref))))
+
+
+def check(D, Dref, mode, fro_tol=None, max_tol=None, tr_tol=None):
+    mx, fro, tr = errors(D, Dref)
+    t = TOL[mode]
+    assert mx <= (max_tol or t["max"]), (mx, fro, tr)
+    if t["fro"] is not None or fro_tol is not None:
+        assert fro <= (fro_tol or t["fro"]), (mx, fro, tr)
+    assert tr <= (tr_tol or t["tr"]), (mx, fro, tr)
+    return mx, fro, tr
+
+
+# ----------------------------------------------------------------- mixed_square (K2 alone)
+@pytest.mark.parametrize("n", [256, 200, 64, 1])
+def test_mixed_square_exact_half_inputs_bit_exact(n):
+    # entries that are exact binary16 values -> X1 = 0 and, with
+    # multiples of 2^-8 in [0,1), every partial sum is exact in fp32.
+    rng = np.random.default_rng(n)
+    K = rng.integers(0, 256, size=(n, n))
+    X = (np.triu(K) + np.triu(K, 1).T).astype(np.float64) / 256.0
+    Y = E.mixed_square(X.astype(np.float32))
+    assert np.array_equal(Y.astype(np.float64), X @ X)
+
+
+def test_mixed_square_identity():
+    Y = E.mixed_square(np.eye(300, dtype=np.float32))
+    assert np.array_equal(Y, np.eye(300, dtype=np.float32))
+
+
+def test_mixed_square_random_spectrum_unit_interval():
+    # random symmetric X with spectrum in [0,1], N=256: rel 2-norm <= 1e-5
+    rng = np.random.default_rng(5)
+    Q, _ = np.linalg.qr(rng.standard_normal((256, 256)))
+    X = (Q * rng.uniform(0, 1, 256)) @ Q.T
+    X = np.triu(X) + np.triu(X, 1).T
+    Y = E.mixed_square(X.astype(np.float32)).astype(np.float64)
+    X32 = X.astype(np.float32).astype(np.float64)
+    ref = X32 @ X32
+    assert np.linalg.norm(Y - ref, 2) / np.linalg.norm(ref, 2) <= 1e-5
+    # and it agrees with the C emulation of Eq. 48 to fp32 accumulation error
+    emu = np.empty((256, 256), dtype=np.float32)
+    Xf = np.ascontiguousarray(X, dtype=np.float32)
+    import ctypes
+    O.lib().ffo_mixed_square_emul(Xf.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), 256,
+                                  16384.0, emu.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+    assert np.abs(Y - emu).max() <= 1e-5 * np.abs(emu).max()
+
+
+# ----------------------------------------------------------------- bounds / statistics
+@pytest.mark.parametrize("n,seed", [(256, 1234), (1024, 1234), (100, 3)])
+def test_spectral_bounds_match_oracle(n, seed):
+    H = tight_binding(n, seed=seed)
+    b = E.spectral_bounds(H)
+    lo, hi = O.gershgorin(H)
+    # TB rows: integer hoppings + one diagonal -> sums are exact, bounds bit-exact
+    assert (b.eps_min, b.eps_max) == (lo, hi)
+    H = goe(96, seed=1)
+    b = E.spectral_bounds(H)
+    lo, hi = O.gershgorin(H)
+    assert abs(b.eps_min - lo) <= 1e-13 * abs(lo) and abs(b.eps_max - hi) <= 1e-13 * abs(hi)
+
+
+def test_density_statistics_vs_reference_pairwise():
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((333, 333))
+    D = (A + A.T) / 2
+    s = E.density_statistics(D)
+    tr, sq = O.density_statistics(D)
+    assert abs(s.trace - tr) <= 1e-12 * max(1.0, abs(tr))
+    assert abs(s.trace_square - sq) <= 1e-13 * sq
+    s = E.density_statistics(np.eye(4))
+    assert (s.trace, s.trace_square) == (4.0, 4.0)
+    s = E.density_statistics(np.diag([0.5, 0.5]))
+    assert (s.trace, s.trace_square) == (1.0, 0.5)
+
+
+# ----------------------------------------------------------------- golden fixtures
+@pytest.mark.parametrize("tag", ["tb16", "tb64", "tb64_m40", "goe64"])
+def test_golden_matrix_fixtures(tag):
+    f = np.load(f"{O.GOLDEN}/matrix_{tag}.npz")
+    model = E.load_model(str(f["model"]))
+    D, st, pv = E.compute_density_matrix(f["H"], float(f["mu"]), float(f["kT"]), model,
+                                         E.PrecisionMode.MIXED_EMULATED)
+    assert pv.status == 0 and pv.diverged_layer == -1
+    assert (pv.eps_min, pv.eps_max) == tuple(f["bounds"]) or tag == "goe64"
+    assert np.array_equal(D, D.T)
+    if tag == "goe64":  # loose Gershgorin bounds: ~3e-5 FP32 floor; reported, not gated
+        check(D, f["D_recursion"], E.PrecisionMode.MIXED_EMULATED, fro_tol=5e-4, max_tol=5e-4, tr_tol=1e-4)
+    else:
+        check(D, f["D_recursion"], E.PrecisionMode.MIXED_EMULATED)
+        check(D, f["D_spectral"], E.PrecisionMode.MIXED_EMULATED)
+    assert abs(st.trace - np.trace(D)) <= 1e-12 * abs(st.trace)
+
+
+# ----------------------------------------------------------------- configs 1-3
+@pytest.mark.parametrize("mode", list(TOL))
+def test_config1_n256_all_modes(model, mode):
+    H = tight_binding(256, seed=1234)
+    Dref = O.density_matrix_f64(H, 0.0, 0.01, model.abcd, model.beta0, model.mu0)
+    D, st, pv = E.compute_density_matrix(H, 0.0, 0.01, model, mode)
+    check(D, Dref, mode)
+    assert pv.half_products == model.layer_count * (3 if mode == E.PrecisionMode.MIXED_EMULATED else 1)
+
+
+def test_config2_n1024_fp32_emulated(model):
+    H = tight_binding(1024, seed=1234)
+    Dref = O.density_matrix_f64(H, 0.0, 0.01, model.abcd, model.beta0, model.mu0)
+    D, st, pv = E.compute_density_matrix(H, 0.0, 0.01, model)
+    check(D, Dref, E.PrecisionMode.MIXED_EMULATED)
+    tr_ref, sq_ref = O.density_statistics(Dref)
+    assert abs(st.trace - tr_ref) / tr_ref <= 1e-6
+    assert abs(st.trace_square - sq_ref) / sq_ref <= 1e-5
+
+
+@pytest.mark.parametrize("mode", [E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16])
+def test_config3_n4096_properties(model, mode):
+    # full-size: size-independent properties (exact symmetry, trace vs exact Fermi
+    # occupation, 0 <= Tr D^2 <= Tr D, determinism)
+    H = tight_binding(4096, seed=1234)
+    D, st, pv = E.compute_density_matrix(H, 0.0, 0.01, model, mode)
+    assert np.array_equal(D, D.T)
+    lam = np.linalg.eigvalsh(H)
+    occ = np.sum(1.0 / (1.0 + np.exp(np.clip((lam - 0.0) / 0.01, -700, 700))))
+    tol = 2e-6 if mode == E.PrecisionMode.MIXED_EMULATED else 1e-2
+    assert abs(st.trace - occ) / occ <= tol, (st.trace, occ)
+    assert 0.0 <= st.trace_square <= st.trace * (1 + 1e-6)
+    D2, st2, _ = E.compute_density_matrix(H, 0.0, 0.01, model, mode)
+    assert np.array_equal(D, D2) and st == st2
+
+
+# ----------------------------------------------------------------- batched (config 4)
+def test_config4_batched_sample(model):
+    B, n = 24, 512
+    mu, kT = batch_params(512)
+    mu, kT = mu[:B], kT[:B]
+    Hs = [tight_binding(n, seed=10000 + k) for k in range(B)]
+    Ds, stats, provs = E.compute_density_matrices(Hs, mu, kT, model)
+    for k in (0, 5, 11, 23):
+        Dref = O.density_matrix_f64(Hs[k], mu[k], kT[k], model.abcd, model.beta0, model.mu0)
+        check(Ds[k], Dref, E.PrecisionMode.MIXED_EMULATED)
+    # each batch member equals the single-matrix call bit-for-bit
+    D1, s1, _ = E.compute_density_matrix(Hs[5], mu[5], kT[5], model)
+    assert np.array_equal(D1, Ds[5]) and s1 == stats[5]
+
+
+def test_device_variant_matches_host(model):
+    import torch
+
+    B, n = 4, 256
+    mu, kT = batch_params(B)
+    Hs = [tight_binding(n, seed=10000 + k) for k in range(B)]
+    Ds, stats, _ = E.compute_density_matrices(Hs, mu, kT, model)
+    H_dev = torch.from_numpy(np.stack(Hs)).cuda()
+    D_dev = torch.empty_like(H_dev)
+    st, status, bnd = E.compute_density_matrices_device(H_dev, mu, kT, model, D_dev=D_dev)
+    torch.cuda.synchronize()
+    assert status.cpu().tolist() == [0] * B
+    assert np.array_equal(D_dev.cpu().numpy(), np.stack(Ds))
+    assert np.array_equal(st.cpu().numpy(), np.array([[s.trace, s.trace_square] for s in stats]))
+
+
+# ----------------------------------------------------------------- SPEC known answers / edges
+def test_spec_two_level_example(model):
+    # SPEC.md:464 (frame trap pinned): H=diag(0,1), beta=50, mu=0.5 -> D ~ diag(f(0), f(1))
+    D, st, pv = E.compute_density_matrix(np.diag([0.0, 1.0]), 0.5, beta=50.0, model=model)
+    f0, f1 = 1 / (1 + np.exp(-25.0)), 1 / (1 + np.exp(25.0))
+    assert abs(D[0, 0] - f0) <= 1e-6 and abs(D[1, 1] - f1) <= 1e-6
+    assert D[0, 1] == 0.0 and D[1, 0] == 0.0
+
+
+def test_spec_n1_at_mu(model):
+    # N=1, H=[mu] -> D=[0.5] +- model error
+    D, st, pv = E.compute_density_matrix(np.array([[0.3]]), 0.3, 0.01, model)
+    assert abs(D[0, 0] - 0.5) <= 2e-6
+
+
+def test_apply_model_diagonal(model):
+    # H0 = diag(lambda) -> D = diag(evaluate_model(m, lambda))
+    lam = np.linspace(0.02, 0.98, 77)
+    D = E.apply_model(np.diag(lam), model)
+    ref = O.evaluate_model_np(model.abcd, lam)
+    assert np.abs(np.diag(D) - ref).max() <= 5e-6
+    assert np.count_nonzero(D - np.diag(np.diag(D))) == 0
+
+
+@pytest.mark.parametrize("n", [2, 3, 127, 129, 130, 300])
+def test_ragged_sizes(model, n):
+    H = tight_binding(n, seed=n) if n >= 4 else np.diag(np.linspace(-1, 1, n))
+    Dref = O.density_matrix_f64(H, 0.0, 0.01, model.abcd, model.beta0, model.mu0)
+    D, st, pv = E.compute_density_matrix(H, 0.0, 0.01, model)
+    check(D, Dref, E.PrecisionMode.MIXED_EMULATED)
+
+
+def test_out_of_region_raises(model):
+    H = tight_binding(256, seed=1)
+    with pytest.raises(E.OutOfRegionError, match="violated"):
+        E.compute_density_matrix(H, 0.0, 0.001, model)  # beta' ~ 9000 > 1000
+
+
+def test_validation_errors(model):
+    H = tight_binding(64)
+    with pytest.raises(E.ValidationError):
+        E.compute_density_matrix(H, 0.0, -1.0, model)
+    with pytest.raises(E.UnsupportedModeError):
+        E.compute_density_matrix(H, 0.0, 0.01, model, E.PrecisionMode.DOUBLE)
+    bad = E.Mlsp2Model(model.abcd, model.beta0, 1.5)
+    with pytest.raises(E.ValidationError, match="mu0"):
+        E.compute_density_matrix(H, 0.0, 0.01, bad)
