@@ -280,18 +280,38 @@ __global__ void row_stats_kernel(const double* D, int n, double2* partials) {
     if (lane == 0) partials[i] = make_double2(dg, sq);
 }
 
-template <int MODE>
-int launch_layer(const CUtensorMap& hi, const CUtensorMap& lo, const LayerParams& p, int grid,
-                 cudaStream_t st) {
+int drain_granularity() {
+    static int dr = [] {
+        const char* e = getenv("FFG_DRAIN_K16");
+        const int v = e ? atoi(e) : 1;
+        return (v == 2 || v == 4) ? v : 1;
+    }();
+    return dr;
+}
+
+template <int MODE, int DR>
+int launch_layer_dr(const CUtensorMap& hi, const CUtensorMap& lo, const LayerParams& p, int grid,
+                    cudaStream_t st) {
     static bool configured = false;
     constexpr int smem = layer_smem_bytes<MODE>();
     if (!configured) {
-        CK(cudaFuncSetAttribute(mlsp2_layer_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(cudaFuncSetAttribute(mlsp2_layer_kernel<MODE, DR>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         configured = true;
     }
-    mlsp2_layer_kernel<MODE><<<grid, 192, smem, st>>>(hi, lo, p);
+    mlsp2_layer_kernel<MODE, DR><<<grid, kLayerThreads, smem, st>>>(hi, lo, p);
     CK(cudaGetLastError());
     return FFG_OK;
+}
+
+template <int MODE>
+int launch_layer(const CUtensorMap& hi, const CUtensorMap& lo, const LayerParams& p, int grid,
+                 cudaStream_t st) {
+    switch (drain_granularity()) {
+        case 4: return launch_layer_dr<MODE, 4>(hi, lo, p, grid, st);
+        case 2: return launch_layer_dr<MODE, 2>(hi, lo, p, grid, st);
+        default: return launch_layer_dr<MODE, 1>(hi, lo, p, grid, st);
+    }
 }
 
 struct Job {

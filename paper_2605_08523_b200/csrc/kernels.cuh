@@ -39,6 +39,9 @@ constexpr int kUK = 16;             // K per UMMA instruction (kind::f16)
 constexpr int kOpBytes = kBM * kBK * 2;  // one 128x64 16-bit operand tile = 16 KB
 constexpr float kHalfScale = 16384.0f;   // global 2^14 pre-scale before the binary16 split
 constexpr float kHalfMax = 65504.0f;
+constexpr int kEpiWarps = 8;            // accumulator-drain / epilogue warps
+constexpr int kEpiCols = kBN / (kEpiWarps / 4);  // tile columns per epilogue warp
+constexpr int kLayerThreads = 64 + kEpiWarps * 32;
 
 template <int MODE>
 struct ModeTraits;
@@ -237,24 +240,40 @@ __device__ __forceinline__ void decode_upper_tile(int t, int nb, int& I, int& J)
     J = I_ + t;
 }
 
-// Warp roles: 0 = TMA producer, 1 = TMEM allocator + UMMA issuer, 2..5 = epilogue
-// (warp w reads TMEM lanes 32*(w%4) .. +31).  One 128x128 upper-triangular output
-// tile per CTA; grid = B * T.
-template <int MODE>
-__global__ void __launch_bounds__(192, 1)
+// Warp roles: 0 = TMA producer, 1 = TMEM allocator + UMMA issuer, 2..9 = accumulator /
+// epilogue warps (warp w reads TMEM lanes 32*(w%4) .. +31 and column half (w-2)/4).
+// One 128x128 upper-triangular output tile per CTA; grid = B * T.
+//
+// Accumulation precision.  tcgen05 FP32 accumulation truncates (round-toward-zero)
+// at every MMA.  Summing hi*lo terms into the large hi*hi accumulator, or letting
+// the hi*hi accumulator run over the whole K extent, biases Tr D by ~3e-6 (measured
+// and reproduced by emulation).  So:
+//   * hi*lo + lo*hi go to their own TMEM accumulator (2^-11 smaller: its truncation
+//     is negligible);
+//   * hi*hi goes to a ping-pong pair of TMEM accumulators, restarted every K-block;
+//     the epilogue warps drain each finished K-block into an fp32 register sum
+//     with round-to-nearest while the tensor core fills the other buffer.
+// TMEM columns: [0,128) hh0, [128,256) hh1, [256,384) hl.
+template <int MODE, int DR>
+__global__ void __launch_bounds__(kLayerThreads, 1)
     mlsp2_layer_kernel(const __grid_constant__ CUtensorMap tm_hi,
                        const __grid_constant__ CUtensorMap tm_lo,
                        const __grid_constant__ LayerParams p) {
     using Tr = ModeTraits<MODE>;
     constexpr int S = Tr::kStages;
     constexpr int SB = stage_bytes<MODE>();
+    constexpr uint32_t kHL = 384;  // TMEM column of the cross-term accumulator
+    constexpr int NHB = 3;         // hi*hi accumulator buffers, each filled by DR K16-MMAs
+    static_assert(DR == 1 || DR == 2 || DR == 4, "drain granularity");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
     uint64_t* empty = full + S;
-    uint64_t* tmem_full = empty + S;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* hh_full = empty + S;       // [NHB]
+    uint64_t* hh_empty = hh_full + NHB;  // [NHB]
+    uint64_t* hl_full = hh_empty + NHB;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hl_full + 1);
     double* red = reinterpret_cast<double*>(smem + S * SB + 512);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -270,12 +289,16 @@ __global__ void __launch_bounds__(192, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int b = 0; b < NHB; ++b) {
+            mbar_init(&hh_full[b], 1);
+            mbar_init(&hh_empty[b], kEpiWarps);  // one arrive per epilogue warp
+        }
+        mbar_init(hl_full, 1);
         fence_barrier_init();
         tma_prefetch_desc(&tm_hi);
         if (Tr::kHasLo) tma_prefetch_desc(&tm_lo);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 128);
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -307,6 +330,7 @@ __global__ void __launch_bounds__(192, 1)
         // ------------------------------------------------ UMMA issuer (one thread)
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc_f16(Tr::kFmt, kBM, kBN);
+            int g = 0;  // index of the current hi*hi fill (DR K16 steps each)
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % S;
                 const uint32_t ph = (kb / S) & 1;
@@ -321,54 +345,100 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int kk = 0; kk < kBK / kUK; ++kk) {
                     const uint32_t koff = kk * kUK * 2;  // bytes along K inside the atom
-                    const uint32_t acc0 = (kb | kk) != 0;
-                    umma_f16(tmem, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff),
-                             idesc, acc0);
+                    const int hb = g % NHB;
+                    if (kk % DR == 0) {
+                        mbar_wait(&hh_empty[hb], ((g / NHB) & 1) ^ 1);  // drained by the epilogue
+                        tc_fence_after();
+                    }
+                    umma_f16(tmem + hb * 128, umma_desc_sw128(a_hi + koff),
+                             umma_desc_sw128(b_hi + koff), idesc, (kk % DR) != 0);
+                    if (kk % DR == DR - 1) {
+                        umma_commit(&hh_full[hb]);  // this fill's hi*hi partial is ready
+                        ++g;
+                    }
                     if (Tr::kProducts == 3) {
-                        umma_f16(tmem, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff),
-                                 idesc, 1u);
-                        umma_f16(tmem, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff),
-                                 idesc, 1u);
+                        umma_f16(tmem + kHL, umma_desc_sw128(a_hi + koff),
+                                 umma_desc_sw128(b_lo + koff), idesc, (kb | kk) != 0);
+                        umma_f16(tmem + kHL, umma_desc_sw128(a_lo + koff),
+                                 umma_desc_sw128(b_hi + koff), idesc, 1u);
                     }
                 }
                 umma_commit(&empty[s]);  // frees the smem stage once these MMAs retire
             }
-            umma_commit(tmem_full);
+            umma_commit(hl_full);
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------ epilogue (4 warps, 128 rows)
+        // ------------------------------------------------ accumulator drain + epilogue
         const int q = warp & 3;
+        const int hc = (warp - 2) >> 2;  // column half owned by this warp
         const int r = q * 32 + lane;
         const int gi = I * kBM + r;
         const int np = p.np, n = p.n;
+        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + hc * kEpiCols;
         const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
         const size_t mat = (size_t)m * np * np;
+
+        float yacc[kEpiCols];
+#pragma unroll
+        for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
+#pragma unroll 1
+        for (int g = 0; g < nk * (kBK / kUK) / DR; ++g) {
+            const int hb = g % NHB;
+            mbar_wait(&hh_full[hb], (g / NHB) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int ch = 0; ch < kEpiCols / 32; ++ch) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(trow + hb * 128 + ch * 32, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    float2 acc = make_float2(yacc[ch * 32 + e], yacc[ch * 32 + e + 1]);
+                    acc = add_f32x2(acc, make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+                    yacc[ch * 32 + e] = acc.x;
+                    yacc[ch * 32 + e + 1] = acc.y;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hh_empty[hb]);
+        }
+        if (Tr::kProducts == 3) {
+            mbar_wait(hl_full, 0);
+            tc_fence_after();
+        }
+
         double tr = 0.0, sq = 0.0;
         bool bad_nf = false, bad_hr = false;
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
-#pragma unroll 1
-        for (int ch = 0; ch < kBN / 32; ++ch) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + ch * 32, v);
-            const int gj0 = J * kBN + ch * 32;
-            const size_t off = mat + (size_t)gi * np + gj0;
-            float xo[32], ao[32];
 #pragma unroll
-            for (int e = 0; e < 32; e += 4) {
+        for (int ch = 0; ch < kEpiCols / 16; ++ch) {
+            float yv[16];
+            if (Tr::kProducts == 3) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(trow + kHL + ch * 16, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) yv[e] = (yacc[ch * 16 + e] + __uint_as_float(v[e])) * inv_s2;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) yv[e] = yacc[ch * 16 + e] * inv_s2;
+            }
+            const int gj0 = J * kBN + hc * kEpiCols + ch * 16;
+            const size_t off = mat + (size_t)gi * np + gj0;
+            float xo[16], ao[16];
+#pragma unroll
+            for (int e = 0; e < 16; e += 4) {
                 const float4 xv = *reinterpret_cast<const float4*>(p.X + off + e);
                 const float4 av = *reinterpret_cast<const float4*>(p.A + off + e);
                 xo[e] = xv.x; xo[e + 1] = xv.y; xo[e + 2] = xv.z; xo[e + 3] = xv.w;
                 ao[e] = av.x; ao[e + 1] = av.y; ao[e + 2] = av.z; ao[e + 3] = av.w;
             }
-            tmem_ld_wait();
-            uint16_t hb[32], lb[32];
+            uint16_t hb[16], lb[16];
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
+            for (int e = 0; e < 16; ++e) {
                 const int gj = gj0 + e;
-                const float y = __uint_as_float(v[e]) * inv_s2;
-                double xd = p.a * (double)y + p.b * (double)xo[e];
+                double xd = p.a * (double)yv[e] + p.b * (double)xo[e];
                 if (gi == gj && gi < n) xd += p.c;
                 const float xn = (float)xd;
                 const bool own = !diag || gj >= gi;
@@ -395,16 +465,15 @@ __global__ void __launch_bounds__(192, 1)
             }
             if (!p.last) {
 #pragma unroll
-                for (int e = 0; e < 32; e += 4) {
+                for (int e = 0; e < 16; e += 4) {
                     *reinterpret_cast<float4*>(p.X + off + e) =
                         make_float4(xo[e], xo[e + 1], xo[e + 2], xo[e + 3]);
                     *reinterpret_cast<float4*>(p.A + off + e) =
                         make_float4(ao[e], ao[e + 1], ao[e + 2], ao[e + 3]);
                 }
-                // direct store of the owned part of row gi
                 if (!diag) {
 #pragma unroll
-                    for (int e = 0; e < 32; e += 8) {
+                    for (int e = 0; e < 16; e += 8) {
                         uint4 hv, lv;
                         hv.x = hb[e] | ((uint32_t)hb[e + 1] << 16);
                         hv.y = hb[e + 2] | ((uint32_t)hb[e + 3] << 16);
@@ -421,7 +490,7 @@ __global__ void __launch_bounds__(192, 1)
                     }
                 } else {
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
+                    for (int e = 0; e < 16; ++e) {
                         if (gj0 + e >= gi) {
                             p.hi_dst[off + e] = hb[e];
                             if (Tr::kHasLo) p.lo_dst[off + e] = lb[e];
@@ -430,7 +499,7 @@ __global__ void __launch_bounds__(192, 1)
                 }
                 // mirrored store: element (gi, gj) -> (gj, gi); lanes cover consecutive gi
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
+                for (int e = 0; e < 16; ++e) {
                     const int gj = gj0 + e;
                     if (gj > gi) {
                         const size_t moff = mat + (size_t)gj * np + gi;
@@ -454,10 +523,13 @@ __global__ void __launch_bounds__(192, 1)
                 red[2 * (warp - 2) + 0] = tr;
                 red[2 * (warp - 2) + 1] = sq;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
             if (warp == 2 && lane == 0) {
-                const double T0 = ((red[0] + red[2]) + (red[4] + red[6]));
-                const double T1 = ((red[1] + red[3]) + (red[5] + red[7]));
+                double T0 = 0.0, T1 = 0.0;
+                for (int w = 0; w < kEpiWarps; ++w) {  // fixed order
+                    T0 += red[2 * w + 0];
+                    T1 += red[2 * w + 1];
+                }
                 p.partials[(size_t)m * p.T + t] = make_double2(T0, T1);
             }
         }
@@ -466,7 +538,7 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 128);
+        tmem_dealloc(tmem, 512);
     }
 }
 
