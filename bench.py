@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MLSP2 finite-temperature density-matrix builder.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Workload (one "step"): a batch of B_per_gpu independent N=1024 2-D tight-binding
+Hamiltonians per GPU (BASELINE.json configs[1] Hamiltonians, batched the way
+configs[3] varies mu_k / kT_k), the FP32-emulated MLSP2 recursion with the
+reference-trained M1500 coefficients (beta0=1500, mu0=1/3, L=30): H -> D, Tr D,
+Tr D^2 for every matrix, results gathered to rank 0 (NCCL) when N > 1.
+Weak scaling: the per-GPU batch is fixed as N grows.
+
+`value` is whole-job density matrices/s with inputs resident in HBM (device
+entry point ffg_density_matrices_dev); `e2e` is the same metric through the
+host C-ABI call ffg_density_matrices on pinned host buffers (H2D of H and D2H of
+D inside the timed region).  `roofline` is the dominant kernel (K2 mlsp2_layer)
+timed with CUDA events on its stream; `cpu_baseline` is the CPU oracle port
+(fp64 recursion, BLAS) on a bounded sample, rank 0 only.
+
+--impl reference times the reference's CPU implementation of the path: the
+reference ships no matrix engine (SPEC-only), so this is the oracle port of its
+recursion (oracle/oracle.py, evaluate_mlsp2 lifted to matrices) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "finite-T density matrices/sec vs N (FP32-emul & BF16); GEMM TFLOP/s % of peak"
+UNIT = "density matrices/s"
+N_DEFAULT = 1024
+BATCH_DEFAULT = 16
+WORKLOAD = ("batched N=1024 periodic 2-D tight-binding H (32x32 lattice, t=-1, eps~U(-.5,.5)), "
+            "mu_k~U(-0.5,0.25), kT_k~U(0.010,0.0125), M1500 coefficients (beta0=1500, mu0=1/3, L=30), "
+            "FP32-emulated mode; per step: H -> D, Tr D, Tr D^2 for B_per_gpu matrices per GPU")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_recursion_sample(n: int, count: int, budget_s: float, seed0: int = 10000):
+    """Time the CPU oracle port (fp64 recursion, numpy/BLAS, all host cores)."""
+    from oracle import oracle as O
+    from paper_2605_08523_b200.hamiltonians import tight_binding, batch_params
+
+    m = O.load_coefficients("M1500")
+    mu, kT = batch_params(max(count, 1))
+    Hs = [tight_binding(n, seed=seed0 + k) for k in range(count)]
+    O.density_matrix_f64(Hs[0], mu[0], kT[0], m["abcd"], 1500.0, 1 / 3)  # warm BLAS threads
+    done, t0 = 0, time.perf_counter()
+    for k in range(count):
+        O.density_matrix_f64(Hs[k], mu[k], kT[k], m["abcd"], 1500.0, 1 / 3)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return done / dt, done, dt
+
+
+def cpu_eigh_sample(n: int, reps: int = 3):
+    from paper_2605_08523_b200.hamiltonians import tight_binding
+
+    H = tight_binding(n, seed=10000)
+    np.linalg.eigh(H)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        lam, V = np.linalg.eigh(H)
+        f = 1.0 / (1.0 + np.exp(np.clip(lam / 0.01, -700, 700)))
+        (V * f) @ V.T
+    return reps / (time.perf_counter() - t0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+        return False
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9 and f[1].isdigit():
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [int(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(statistics.median(sm)), "sm_max_mhz": int(rows[0][2]),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace('.', '', 1).isdigit())}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the CPU implementation of the path (oracle port), rank 0 only."""
+    if rank != 0:
+        return 0
+    n = args.n
+    cores = cpu_cores()
+    per_step = []
+    for _ in range(args.warmup):
+        cpu_recursion_sample(n, 1, 1e9)
+    for _ in range(args.steps):
+        v, done, dt = cpu_recursion_sample(n, 1, 1e9)
+        per_step.append(dt)
+    t = sum(per_step) / len(per_step)
+    value = 1.0 / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD.replace("per GPU", "per host (CPU)"), "n": n,
+                   "batch_per_step": 1, "coefficients": "M1500", "cache": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"1 matrix N={n} per step, fp64 MLSP2 recursion (oracle/oracle.py "
+                                   f"density_matrix_f64, numpy/OpenBLAS on {cores} threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference ships no matrix engine (SPEC.md:288-425 unimplemented); its recursion "
+                "(scalar_models.cpp:243-252) is timed through the oracle port",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--batch", type=int, default=BATCH_DEFAULT, help="matrices per GPU per step")
+    ap.add_argument("--mode", default="MIXED_EMULATED")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2605_08523_b200 import engine as E
+    from paper_2605_08523_b200 import distributed as FD
+    from paper_2605_08523_b200.hamiltonians import tight_binding, batch_params
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if not E.device_available():
+        raise SystemExit("no sm_100 device: " + E.lib().ffg_last_error().decode())
+
+    mode = E.PrecisionMode[args.mode]
+    model = E.load_model("M1500")
+    n, B = args.n, args.batch
+    # this rank's shard of the global batch (weak scaling: B per GPU)
+    g_mu, g_kT = batch_params(B * world)
+    lo, hi = FD.shard_range(B * world, world, rank)
+    mu, kT = g_mu[lo:hi], g_kT[lo:hi]
+    H_host = np.stack([tight_binding(n, seed=10000 + k) for k in range(lo, hi)])
+    H_dev = torch.from_numpy(H_host).to(dev)
+    D_dev = torch.empty_like(H_dev)
+    stats_dev = torch.empty((B, 2), dtype=torch.float64, device=dev)
+    status_dev = torch.empty((B,), dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    gatherer = FD.ResultGather(world, rank, B, dev) if world > 1 else None
+
+    def step():
+        E.compute_density_matrices_device(H_dev, mu, kT, model, mode, D_dev=D_dev,
+                                          stats_dev=stats_dev, status_dev=status_dev, stream=stream)
+        if gatherer is not None:
+            with torch.cuda.stream(stream):
+                gatherer.gather(stats_dev, status_dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    # ---------------------------------------------------------------- device-resident timing
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = status_dev.cpu().numpy()
+    if (st != 0).any():
+        raise SystemExit(f"rank {rank}: matrices failed with status {st.tolist()}")
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    t_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms_total = float(t_ms.item())
+    ms_per_step = ms_total / args.steps
+    value = world * B * args.steps / (ms_total / 1e3)
+
+    # ---------------------------------------------------------------- dominant kernel (K2)
+    E.profile_layers(True)
+    E.profile_read()
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    k2_ms, k2_launches = E.profile_read()
+    E.profile_layers(False)
+    k2_avg_s = (k2_ms / 1e3) / max(k2_launches, 1)
+    flops_per_launch = B * E.algorithmic_flops(n, 1, mode)
+    pk, pk_kind = peaks()
+    achieved_tf = flops_per_launch / k2_avg_s / 1e12
+    peak_tf = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("n") == n and tr.get("batch") == B and tr.get("mode") == args.mode:
+            traffic = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    launches_per_step = E.kernel_launches(B, n, model, mode)
+
+    # ---------------------------------------------------------------- e2e through the host C ABI
+    H_pin = torch.from_numpy(H_host).pin_memory()
+    D_pin = torch.empty_like(H_pin).pin_memory()
+    Hp = [H_pin[k].numpy() for k in range(B)]
+    Dp = [D_pin[k].numpy() for k in range(B)]
+    import ctypes
+    Harr = (E._D * B)(*[E._dp(h) for h in Hp])
+    Darr = (E._D * B)(*[E._dp(d) for d in Dp])
+    mu_c = np.ascontiguousarray(mu)
+    kT_c = np.ascontiguousarray(kT)
+    stats_h = np.zeros((B, 2))
+    m_c = model._c()
+
+    def e2e_step():
+        E._check(E.lib().ffg_density_matrices(B, Harr, n, E._dp(mu_c), E._dp(kT_c), ctypes.byref(m_c),
+                                              int(mode), Darr, E._dp(stats_h), None))
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(2, args.steps // 2)
+    for _ in range(e2e_steps):
+        e2e_step()
+    t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * e2e_steps / float(t_e2e.item())
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, done, dt = cpu_recursion_sample(n, 50, args.cpu_budget)
+        cores = cpu_cores()
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{done} matrices N={n} ({dt:.1f} s): fp64 MLSP2 recursion of the oracle port "
+                         f"(numpy/OpenBLAS, {cores} threads), same H/mu/kT family",
+               "diagonalization_value": cpu_eigh_sample(n), "diagonalization_note":
+               "numpy eigh (LAPACK syevd) + V f(lambda) V^T, N=1024, matrices/s"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": {"MIXED_EMULATED": "f32-emulated (f16 hi/lo x3 products, f32 accumulate)",
+                      "BF16": "bf16 (f32 accumulate)", "FP16": "f16 (f32 accumulate)"}[args.mode],
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": n, "batch_per_gpu": B, "global_batch": B * world,
+                       "layers": model.layer_count, "coefficients": "M1500", "mode": args.mode,
+                       "parallelism": f"batch-sharded x{world}, NCCL gather of results",
+                       "cache": f"inputs larger than L2: H {B * n * n * 8 / 2**20:.0f} MiB + workspace "
+                                f"{B * n * n * 16 / 2**20:.0f} MiB per GPU"},
+            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved_tf / peak_tf, "traffic": traffic,
+                         "kernel": "mlsp2_layer (K2)", "peak_kind": f"{pk_kind} bf16 sustained",
+                         "frac_of_burst_peak": achieved_tf / pk["bf16_tflops"],
+                         "algorithmic_flops_per_launch": flops_per_launch,
+                         "avg_launch_ms": k2_avg_s * 1e3,
+                         "k2_share_of_step": (k2_ms / 2) / ms_per_step if ms_per_step else None},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * n * n * 8,
+                    "d2h_bytes_per_step": B * n * n * 8 + B * 16},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "gemm_fp32_equiv_tflops": world * B * model.layer_count * 2.0 * n ** 3 / (ms_per_step / 1e3) / 1e12,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -148,6 +148,12 @@ int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, cons
 /* Number of kernels ffg_density_matrices_dev launches for one call (for accounting). */
 int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, int32_t mode);
 
+/* Measurement hooks (bench.py): when enabled, every layer-kernel (K2) launch is
+ * bracketed by CUDA events on its stream; ffg_profile_read() synchronises them and
+ * returns the summed device time and launch count since the last read. */
+int ffg_profile_layers(int enable);
+int ffg_profile_read(double* total_ms, int64_t* launches);
+
 /* Release cached device workspaces of the calling process. */
 void ffg_release_workspaces(void);
 

@@ -115,17 +115,20 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 16-bit operand matrix [rows][np] viewed by TMA as 128-row x 64-col boxes, 128B swizzle.
-int make_operand_map(CUtensorMap* tm, void* base, int64_t rows, int64_t np) {
+// Row-major matrix [rows][np] of 16-bit (elem=2) or fp32 (elem=4) values viewed by TMA as
+// box_rows x box_cols boxes with the 128-byte swizzle (box_cols * elem == 128).
+int make_map(CUtensorMap* tm, void* base, int64_t rows, int64_t np, int elem, int box_cols,
+             int box_rows) {
     EncodeTiledFn enc = encode_fn();
     if (!enc) return set_err(FFG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)np, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)np * 2};
-    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    cuuint64_t strides[1] = {(cuuint64_t)np * elem};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(tm, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(FFG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return FFG_OK;
 }
@@ -153,9 +156,10 @@ struct Workspace {
     void* host_small = nullptr;     // pinned readback: stats, bounds, status, flags
     size_t host_small_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // tensor-map cache
+    // tensor-map cache: [0..3] operands hi0 lo0 hi1 lo1 (64x128 boxes), [4..7] the same
+    // arrays as 64x64 mirror boxes, [8] X, [9] A (fp32, 32x128 boxes)
     int tm_B = -1, tm_np = -1;
-    CUtensorMap tm[4];
+    CUtensorMap tm[10];
     std::mutex mu;
 };
 
@@ -280,6 +284,14 @@ __global__ void row_stats_kernel(const double* D, int n, double2* partials) {
     if (lane == 0) partials[i] = make_double2(dg, sq);
 }
 
+int debug_flags() {
+    static int v = [] {
+        const char* e = getenv("FFG_DEBUG_K2");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 int drain_granularity() {
     static int dr = [] {
         const char* e = getenv("FFG_DRAIN_K16");
@@ -290,8 +302,7 @@ int drain_granularity() {
 }
 
 template <int MODE, int DR>
-int launch_layer_dr(const CUtensorMap& hi, const CUtensorMap& lo, const LayerParams& p, int grid,
-                    cudaStream_t st) {
+int launch_layer_dr(const LayerMaps& maps, const LayerParams& p, int grid, cudaStream_t st) {
     static bool configured = false;
     constexpr int smem = layer_smem_bytes<MODE>();
     if (!configured) {
@@ -299,19 +310,42 @@ int launch_layer_dr(const CUtensorMap& hi, const CUtensorMap& lo, const LayerPar
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         configured = true;
     }
-    mlsp2_layer_kernel<MODE, DR><<<grid, kLayerThreads, smem, st>>>(hi, lo, p);
+    mlsp2_layer_kernel<MODE, DR><<<grid, kLayerThreads, smem, st>>>(maps, p);
     CK(cudaGetLastError());
     return FFG_OK;
 }
 
 template <int MODE>
-int launch_layer(const CUtensorMap& hi, const CUtensorMap& lo, const LayerParams& p, int grid,
-                 cudaStream_t st) {
+int launch_layer(const LayerMaps& maps, const LayerParams& p, int grid, cudaStream_t st) {
     switch (drain_granularity()) {
-        case 4: return launch_layer_dr<MODE, 4>(hi, lo, p, grid, st);
-        case 2: return launch_layer_dr<MODE, 2>(hi, lo, p, grid, st);
-        default: return launch_layer_dr<MODE, 1>(hi, lo, p, grid, st);
+        case 4: return launch_layer_dr<MODE, 4>(maps, p, grid, st);
+        case 2: return launch_layer_dr<MODE, 2>(maps, p, grid, st);
+        default: return launch_layer_dr<MODE, 1>(maps, p, grid, st);
     }
+}
+
+// Optional CUDA-event timing of every K2 (layer) launch, for the roofline figure.
+struct LayerProfile {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t used = 0;
+    std::mutex mu;
+} g_prof;
+
+int prof_begin(cudaStream_t st, cudaEvent_t* stop) {
+    *stop = nullptr;
+    if (!g_prof.on) return FFG_OK;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (g_prof.used == g_prof.ev.size()) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        g_prof.ev.emplace_back(a, b);
+    }
+    auto& pr = g_prof.ev[g_prof.used++];
+    CK(cudaEventRecord(pr.first, st));
+    *stop = pr.second;
+    return FFG_OK;
 }
 
 struct Job {
@@ -341,8 +375,12 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     int rc;
     if ((rc = ensure(w, B, np, T, true))) return rc;
     if (w.tm_B != B || w.tm_np != (int)np) {
-        for (int k = 0; k < 4; ++k)
-            if ((rc = make_operand_map(&w.tm[k], w.op[k], (int64_t)B * np, np))) return rc;
+        for (int k = 0; k < 4; ++k) {
+            if ((rc = make_map(&w.tm[k], w.op[k], (int64_t)B * np, np, 2, 64, 128))) return rc;
+            if ((rc = make_map(&w.tm[4 + k], w.op[k], (int64_t)B * np, np, 2, 64, 64))) return rc;
+        }
+        if ((rc = make_map(&w.tm[8], w.X, (int64_t)B * np, np, 4, 32, 128))) return rc;
+        if ((rc = make_map(&w.tm[9], w.A, (int64_t)B * np, np, 4, 32, 128))) return rc;
         w.tm_B = B;
         w.tm_np = (int)np;
     }
@@ -397,15 +435,26 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         lp.nb = nb;
         lp.T = (int)T;
         lp.layer = l;
-        const CUtensorMap& thi = w.tm[2 * par + 0];
-        const CUtensorMap& tlo = w.tm[2 * par + 1];
+        lp.dbg = debug_flags();
+        LayerMaps maps;
+        maps.hi = w.tm[2 * par + 0];
+        maps.lo = w.tm[2 * par + 1];
+        maps.hid = w.tm[2 * (par ^ 1) + 0];
+        maps.lod = w.tm[2 * (par ^ 1) + 1];
+        maps.him = w.tm[4 + 2 * (par ^ 1) + 0];
+        maps.lom = w.tm[4 + 2 * (par ^ 1) + 1];
+        maps.x = w.tm[8];
+        maps.a = w.tm[9];
         const int grid = (int)(B * T);
+        cudaEvent_t stop;
+        if ((rc = prof_begin(st, &stop))) return rc;
         switch (j.mode) {
-            case kModeF32E: rc = launch_layer<kModeF32E>(thi, tlo, lp, grid, st); break;
-            case kModeF16: rc = launch_layer<kModeF16>(thi, tlo, lp, grid, st); break;
-            default: rc = launch_layer<kModeBF16>(thi, tlo, lp, grid, st); break;
+            case kModeF32E: rc = launch_layer<kModeF32E>(maps, lp, grid, st); break;
+            case kModeF16: rc = launch_layer<kModeF16>(maps, lp, grid, st); break;
+            default: rc = launch_layer<kModeBF16>(maps, lp, grid, st); break;
         }
         if (rc) return rc;
+        if (stop) CK(cudaEventRecord(stop, st));
     }
     FinalizeParams fp{};
     fp.partials = w.partials;
@@ -746,6 +795,28 @@ int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, in
     (void)mode;
     if (!model) return 0;
     return 3 + (int64_t)model->n_layers;  // reset + K1 + L x K2 + K3
+}
+
+int ffg_profile_layers(int enable) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = enable != 0;
+    g_prof.used = 0;
+    return FFG_OK;
+}
+
+int ffg_profile_read(double* total_ms, int64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    double t = 0.0;
+    for (size_t i = 0; i < g_prof.used; ++i) {
+        CK(cudaEventSynchronize(g_prof.ev[i].second));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, g_prof.ev[i].first, g_prof.ev[i].second));
+        t += ms;
+    }
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = (int64_t)g_prof.used;
+    g_prof.used = 0;
+    return FFG_OK;
 }
 
 void ffg_release_workspaces(void) {

@@ -226,6 +226,7 @@ struct LayerParams {
     double a, b, c, d_next;
     int n, np, nb, T;     // nb = np/128 tile rows, T = nb(nb+1)/2 upper tiles
     int layer, last;      // layer index l (produces X_{l+1})
+    int dbg;              // measurement only: bit0 skip epilogue memory traffic, bit1 skip drain
 };
 
 __device__ __forceinline__ void decode_upper_tile(int t, int nb, int& I, int& J) {
@@ -240,31 +241,48 @@ __device__ __forceinline__ void decode_upper_tile(int t, int nb, int& I, int& J)
     J = I_ + t;
 }
 
-// Warp roles: 0 = TMA producer, 1 = TMEM allocator + UMMA issuer, 2..9 = accumulator /
-// epilogue warps (warp w reads TMEM lanes 32*(w%4) .. +31 and column half (w-2)/4).
-// One 128x128 upper-triangular output tile per CTA; grid = B * T.
+struct LayerMaps {
+    CUtensorMap hi, lo;      // operand source (parity l&1): box 64 x 128, SW128
+    CUtensorMap hid, lod;    // operand destination (parity (l+1)&1): box 64 x 128, SW128
+    CUtensorMap him, lom;    // mirrored destination: box 64 x 64, SW128
+    CUtensorMap x, a;        // fp32 master X / accumulator A: box 32 x 128, SW128
+};
+
+// byte offset of 16-byte chunk `c` of row `r` in a 128-byte-row tile with the TMA/UMMA
+// 128B swizzle (tile base 1024-aligned)
+__device__ __forceinline__ uint32_t sw128(uint32_t r, uint32_t c) {
+    return r * 128u + ((c ^ (r & 7u)) << 4);
+}
+
+// Warp roles: 0 = TMA producer (+ epilogue TMA issue), 1 = TMEM allocator + UMMA issuer,
+// 2..9 = accumulator-drain / epilogue warps (warp w reads TMEM lanes 32*(w%4)..+31; its
+// column half during the drain is (w-2)/4).  One 128x128 upper-triangular tile per CTA.
 //
-// Accumulation precision.  tcgen05 FP32 accumulation truncates (round-toward-zero)
-// at every MMA.  Summing hi*lo terms into the large hi*hi accumulator, or letting
-// the hi*hi accumulator run over the whole K extent, biases Tr D by ~3e-6 (measured
-// and reproduced by emulation).  So:
-//   * hi*lo + lo*hi go to their own TMEM accumulator (2^-11 smaller: its truncation
-//     is negligible);
-//   * hi*hi goes to a ping-pong pair of TMEM accumulators, restarted every K-block;
-//     the epilogue warps drain each finished K-block into an fp32 register sum
-//     with round-to-nearest while the tensor core fills the other buffer.
-// TMEM columns: [0,128) hh0, [128,256) hh1, [256,384) hl.
+// Accumulation precision.  tcgen05 FP32 accumulation truncates inside every MMA.  Summing
+// hi*lo terms into the large hi*hi accumulator, or letting hi*hi accumulate over the whole
+// K extent, biases Tr D by ~3e-6 (measured on B200, reproduced by emulation).
+// So hi*lo + lo*hi go to their own TMEM accumulator (2^-11 smaller, its truncation is
+// negligible) and every hi*hi MMA (DR=1) lands in a fresh buffer of a 3-deep TMEM ring that
+// the epilogue warps drain into fp32 registers with round-to-nearest adds (FADD2) while the
+// tensor core fills the next buffer.
+// TMEM columns: [0,384) hi*hi ring, [384,512) cross terms, then the final Y.
+//
+// Epilogue (layers 0..L-2): Y = drained hi*hi + cross terms is written back to TMEM; X and A
+// tiles come in by TMA into the (now idle) pipeline SMEM; X' = aY + bX + cI, A += d' X' and
+// the split of X' are computed in swizzled SMEM and leave by TMA bulk stores: X, A and the
+// direct hi/lo tile at (I,J), the transposed hi/lo tile at (J,I) (for a diagonal tile one
+// symmetric 128x128 tile assembled from its upper triangle).  Last layer: D = A + X_L with
+// direct fp64 stores and the per-tile statistics.
 template <int MODE, int DR>
 __global__ void __launch_bounds__(kLayerThreads, 1)
-    mlsp2_layer_kernel(const __grid_constant__ CUtensorMap tm_hi,
-                       const __grid_constant__ CUtensorMap tm_lo,
-                       const __grid_constant__ LayerParams p) {
+    mlsp2_layer_kernel(const __grid_constant__ LayerMaps tm, const __grid_constant__ LayerParams p) {
     using Tr = ModeTraits<MODE>;
     constexpr int S = Tr::kStages;
     constexpr int SB = stage_bytes<MODE>();
-    constexpr uint32_t kHL = 384;  // TMEM column of the cross-term accumulator
-    constexpr int NHB = 3;         // hi*hi accumulator buffers, each filled by DR K16-MMAs
+    constexpr uint32_t kHL = 384;  // TMEM column of the cross-term accumulator / final Y
+    constexpr int NHB = 3;         // hi*hi accumulator ring
     static_assert(DR == 1 || DR == 2 || DR == 4, "drain granularity");
+    static_assert(S * SB >= 192 * 1024, "epilogue staging reuses 192 KB of pipeline smem");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -273,8 +291,19 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
     uint64_t* hh_full = empty + S;       // [NHB]
     uint64_t* hh_empty = hh_full + NHB;  // [NHB]
     uint64_t* hl_full = hh_empty + NHB;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hl_full + 1);
+    uint64_t* xa_full = hl_full + 1;     // X/A tiles landed in smem
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_full + 1);
     double* red = reinterpret_cast<double*>(smem + S * SB + 512);
+
+    // epilogue staging inside the pipeline smem (valid once the mainloop is done)
+    uint8_t* sX = smem;                  // [half][box 0..1] 128 rows x 32 fp32, 16 KB boxes
+    uint8_t* sA = smem + 64 * 1024;
+    uint8_t* sHi = smem + 128 * 1024;    // off-diag: direct 128x64 (16 KB); diag: 2 boxes 128x64
+    uint8_t* sLo = smem + 144 * 1024;
+    uint8_t* sHiT = smem + 160 * 1024;   // off-diag: mirrored 64x128 as 2 boxes 64x64 (8 KB)
+    uint8_t* sLoT = smem + 176 * 1024;
+    uint8_t* sHiD = smem + 128 * 1024;   // diag: symmetric 128x128 hi as 2 boxes 128x64 (32 KB)
+    uint8_t* sLoD = smem + 160 * 1024;   // diag: symmetric 128x128 lo
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.x / p.T;
@@ -283,6 +312,9 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
     decode_upper_tile(t, p.nb, I, J);
     const bool diag = (I == J);
     const int nk = p.np / kBK;
+    const bool tma_epi = !p.last && !(p.dbg & 1);
+    const int rowI = m * p.np + I * kBM;
+    const int rowJ = m * p.np + J * kBN;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -294,9 +326,10 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
             mbar_init(&hh_empty[b], kEpiWarps);  // one arrive per epilogue warp
         }
         mbar_init(hl_full, 1);
+        mbar_init(xa_full, 1);
         fence_barrier_init();
-        tma_prefetch_desc(&tm_hi);
-        if (Tr::kHasLo) tma_prefetch_desc(&tm_lo);
+        tma_prefetch_desc(&tm.hi);
+        if (Tr::kHasLo) tma_prefetch_desc(&tm.lo);
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
@@ -307,8 +340,12 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
-            const int rowI = m * p.np + I * kBM;
-            const int rowJ = m * p.np + J * kBN;
+            if (tma_epi) {  // warm L2 with this tile's X / A for the epilogue
+                for (int b = 0; b < 4; ++b) {
+                    tma_prefetch_l2_2d(&tm.x, J * kBN + 32 * b, rowI);
+                    tma_prefetch_l2_2d(&tm.a, J * kBN + 32 * b, rowI);
+                }
+            }
             const uint32_t bytes = (diag ? (Tr::kHasLo ? 2 : 1) : (Tr::kHasLo ? 4 : 2)) * kOpBytes;
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % S;
@@ -316,13 +353,22 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
                 mbar_wait(&empty[s], ph ^ 1);
                 mbar_expect_tx(&full[s], bytes);
                 uint8_t* st = smem + s * SB;
-                tma_load_2d(st + 0 * kOpBytes, &tm_hi, &full[s], kb * kBK, rowI);
-                if (Tr::kHasLo) tma_load_2d(st + 1 * kOpBytes, &tm_lo, &full[s], kb * kBK, rowI);
+                tma_load_2d(st + 0 * kOpBytes, &tm.hi, &full[s], kb * kBK, rowI);
+                if (Tr::kHasLo) tma_load_2d(st + 1 * kOpBytes, &tm.lo, &full[s], kb * kBK, rowI);
                 if (!diag) {
                     const int ob = Tr::kHasLo ? 2 : 1;
-                    tma_load_2d(st + ob * kOpBytes, &tm_hi, &full[s], kb * kBK, rowJ);
+                    tma_load_2d(st + ob * kOpBytes, &tm.hi, &full[s], kb * kBK, rowJ);
                     if (Tr::kHasLo)
-                        tma_load_2d(st + (ob + 1) * kOpBytes, &tm_lo, &full[s], kb * kBK, rowJ);
+                        tma_load_2d(st + (ob + 1) * kOpBytes, &tm.lo, &full[s], kb * kBK, rowJ);
+                }
+            }
+            if (tma_epi) {
+                // all MMAs retired -> every pipeline stage is free: bring X, A (both halves)
+                mbar_wait(hl_full, 0);
+                mbar_expect_tx(xa_full, 128 * 1024);
+                for (int b = 0; b < 4; ++b) {
+                    tma_load_2d(sX + b * 16384, &tm.x, xa_full, J * kBN + 32 * b, rowI);
+                    tma_load_2d(sA + b * 16384, &tm.a, xa_full, J * kBN + 32 * b, rowI);
                 }
             }
         }
@@ -346,14 +392,14 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
                 for (int kk = 0; kk < kBK / kUK; ++kk) {
                     const uint32_t koff = kk * kUK * 2;  // bytes along K inside the atom
                     const int hb = g % NHB;
-                    if (kk % DR == 0) {
+                    if (kk % DR == 0 && !(p.dbg & 2)) {
                         mbar_wait(&hh_empty[hb], ((g / NHB) & 1) ^ 1);  // drained by the epilogue
                         tc_fence_after();
                     }
                     umma_f16(tmem + hb * 128, umma_desc_sw128(a_hi + koff),
                              umma_desc_sw128(b_hi + koff), idesc, (kk % DR) != 0);
                     if (kk % DR == DR - 1) {
-                        umma_commit(&hh_full[hb]);  // this fill's hi*hi partial is ready
+                        if (!(p.dbg & 2)) umma_commit(&hh_full[hb]);
                         ++g;
                     }
                     if (Tr::kProducts == 3) {
@@ -369,28 +415,27 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------ accumulator drain + epilogue
+        // ------------------------------------------------ accumulator drain
         const int q = warp & 3;
-        const int hc = (warp - 2) >> 2;  // column half owned by this warp
-        const int r = q * 32 + lane;
+        const int hc = (warp - 2) >> 2;  // column half owned during the drain
+        const int r = q * 32 + lane;     // tile row of this thread
         const int gi = I * kBM + r;
         const int np = p.np, n = p.n;
-        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + hc * kEpiCols;
+        const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
         const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
-        const size_t mat = (size_t)m * np * np;
 
         float yacc[kEpiCols];
 #pragma unroll
         for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
 #pragma unroll 1
-        for (int g = 0; g < nk * (kBK / kUK) / DR; ++g) {
+        for (int g = 0; g < ((p.dbg & 2) ? 0 : nk * (kBK / kUK) / DR); ++g) {
             const int hb = g % NHB;
             mbar_wait(&hh_full[hb], (g / NHB) & 1);
             tc_fence_after();
 #pragma unroll
             for (int ch = 0; ch < kEpiCols / 32; ++ch) {
                 uint32_t v[32];
-                tmem_ld_32x32b_x32(trow + hb * 128 + ch * 32, v);
+                tmem_ld_32x32b_x32(tlane + hb * 128 + hc * kEpiCols + ch * 32, v);
                 tmem_ld_wait();
 #pragma unroll
                 for (int e = 0; e < 32; e += 2) {
@@ -404,107 +449,187 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&hh_empty[hb]);
         }
-        if (Tr::kProducts == 3) {
-            mbar_wait(hl_full, 0);
-            tc_fence_after();
+        // Y = (hi*hi + cross terms) / scale^2, written over the cross-term columns
+        mbar_wait(hl_full, 0);
+        tc_fence_after();
+#pragma unroll
+        for (int ch = 0; ch < kEpiCols / 32; ++ch) {
+            const uint32_t ta = tlane + kHL + hc * kEpiCols + ch * 32;
+            uint32_t v[32];
+            if (Tr::kProducts == 3) {
+                tmem_ld_32x32b_x32(ta, v);
+                tmem_ld_wait();
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+                const float y = Tr::kProducts == 3 ? yacc[ch * 32 + e] + __uint_as_float(v[e])
+                                                   : yacc[ch * 32 + e];
+                v[e] = __float_as_uint(y * inv_s2);
+            }
+            if (p.dbg & 2) {  // measurement only: no drain -> Y is the cross-term accumulator
+                tmem_ld_32x32b_x32(ta, v);
+                tmem_ld_wait();
+            }
+            tmem_st_32x32b_x32(ta, v);
         }
+        tmem_st_wait();
+        tc_fence_before();
+        named_bar_sync(2, kEpiWarps * 32);  // all of Y is in TMEM
+        tc_fence_after();
 
         double tr = 0.0, sq = 0.0;
         bool bad_nf = false, bad_hr = false;
-#pragma unroll
-        for (int ch = 0; ch < kEpiCols / 16; ++ch) {
-            float yv[16];
-            if (Tr::kProducts == 3) {
-                uint32_t v[16];
-                tmem_ld_32x32b_x16(trow + kHL + ch * 16, v);
+        const size_t mat = (size_t)m * np * np;
+        if (p.dbg & 1) {
+            // measurement only: no epilogue memory traffic
+        } else if (!p.last) {
+            // ============================== TMA epilogue (layers 0..L-2)
+            const int sub = hc;  // 32-column block of the current half handled by this warp
+            mbar_wait(xa_full, 0);
+            for (int h = 0; h < 2; ++h) {
+                const int cl0 = h * 64 + sub * 32;  // first tile column of this warp's block
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tlane + kHL + cl0, v);
+                uint8_t* bx = sX + (h * 2 + sub) * 16384;
+                uint8_t* ba = sA + (h * 2 + sub) * 16384;
                 tmem_ld_wait();
+                uint16_t hb[32], lb[32];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) yv[e] = (yacc[ch * 16 + e] + __uint_as_float(v[e])) * inv_s2;
-            } else {
+                for (int c4 = 0; c4 < 8; ++c4) {
+                    float4* px = reinterpret_cast<float4*>(bx + sw128(r, c4));
+                    float4* pa = reinterpret_cast<float4*>(ba + sw128(r, c4));
+                    float4 xv = *px, av = *pa;
+                    float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+                    float as[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-                for (int e = 0; e < 16; ++e) yv[e] = yacc[ch * 16 + e] * inv_s2;
-            }
-            const int gj0 = J * kBN + hc * kEpiCols + ch * 16;
-            const size_t off = mat + (size_t)gi * np + gj0;
-            float xo[16], ao[16];
-#pragma unroll
-            for (int e = 0; e < 16; e += 4) {
-                const float4 xv = *reinterpret_cast<const float4*>(p.X + off + e);
-                const float4 av = *reinterpret_cast<const float4*>(p.A + off + e);
-                xo[e] = xv.x; xo[e + 1] = xv.y; xo[e + 2] = xv.z; xo[e + 3] = xv.w;
-                ao[e] = av.x; ao[e + 1] = av.y; ao[e + 2] = av.z; ao[e + 3] = av.w;
-            }
-            uint16_t hb[16], lb[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const int gj = gj0 + e;
-                double xd = p.a * (double)yv[e] + p.b * (double)xo[e];
-                if (gi == gj && gi < n) xd += p.c;
-                const float xn = (float)xd;
-                const bool own = !diag || gj >= gi;
-                bad_nf |= own && !isfinite(xn);
-                if (!p.last) {
-                    ao[e] = (float)((double)ao[e] + p.d_next * (double)xn);
-                    xo[e] = xn;
-                    bad_hr |= own && half_range_bad<MODE>(xn);
-                    split16<MODE>(xn, hb[e], lb[e]);
-                } else if (own && gi < n && gj < n) {
-                    const double dv = (double)ao[e] + (double)xn;
-                    if (p.D) {
-                        double* Dm = p.D + (size_t)m * n * n;
-                        Dm[(size_t)gi * n + gj] = dv;
-                        if (gi != gj) Dm[(size_t)gj * n + gi] = dv;
+                    for (int e = 0; e < 4; ++e) {
+                        const int cl = cl0 + c4 * 4 + e;
+                        const int gj = J * kBN + cl;
+                        const float y = __uint_as_float(v[c4 * 4 + e]);
+                        double xd = p.a * (double)y + p.b * (double)xs[e];
+                        if (gi == gj && gi < n) xd += p.c;
+                        const float xn = (float)xd;
+                        const bool own = !diag || cl >= r;
+                        bad_nf |= own && !isfinite(xn);
+                        bad_hr |= own && half_range_bad<MODE>(xn);
+                        as[e] = (float)((double)as[e] + p.d_next * (double)xn);
+                        xs[e] = xn;
+                        split16<MODE>(xn, hb[c4 * 4 + e], lb[c4 * 4 + e]);
                     }
-                    if (gi != gj) {
-                        sq += 2.0 * dv * dv;
-                    } else {
-                        tr += dv;
-                        sq += dv * dv;
-                    }
-                }
-            }
-            if (!p.last) {
-#pragma unroll
-                for (int e = 0; e < 16; e += 4) {
-                    *reinterpret_cast<float4*>(p.X + off + e) =
-                        make_float4(xo[e], xo[e + 1], xo[e + 2], xo[e + 3]);
-                    *reinterpret_cast<float4*>(p.A + off + e) =
-                        make_float4(ao[e], ao[e + 1], ao[e + 2], ao[e + 3]);
+                    *px = make_float4(xs[0], xs[1], xs[2], xs[3]);
+                    *pa = make_float4(as[0], as[1], as[2], as[3]);
                 }
                 if (!diag) {
+                    // direct tile (rows I, 64 columns of half h): row r, 16-B chunks 4*sub..
 #pragma unroll
-                    for (int e = 0; e < 16; e += 8) {
+                    for (int c8 = 0; c8 < 4; ++c8) {
                         uint4 hv, lv;
-                        hv.x = hb[e] | ((uint32_t)hb[e + 1] << 16);
-                        hv.y = hb[e + 2] | ((uint32_t)hb[e + 3] << 16);
-                        hv.z = hb[e + 4] | ((uint32_t)hb[e + 5] << 16);
-                        hv.w = hb[e + 6] | ((uint32_t)hb[e + 7] << 16);
-                        *reinterpret_cast<uint4*>(p.hi_dst + off + e) = hv;
+                        hv.x = hb[c8 * 8 + 0] | ((uint32_t)hb[c8 * 8 + 1] << 16);
+                        hv.y = hb[c8 * 8 + 2] | ((uint32_t)hb[c8 * 8 + 3] << 16);
+                        hv.z = hb[c8 * 8 + 4] | ((uint32_t)hb[c8 * 8 + 5] << 16);
+                        hv.w = hb[c8 * 8 + 6] | ((uint32_t)hb[c8 * 8 + 7] << 16);
+                        *reinterpret_cast<uint4*>(sHi + sw128(r, sub * 4 + c8)) = hv;
                         if (Tr::kHasLo) {
-                            lv.x = lb[e] | ((uint32_t)lb[e + 1] << 16);
-                            lv.y = lb[e + 2] | ((uint32_t)lb[e + 3] << 16);
-                            lv.z = lb[e + 4] | ((uint32_t)lb[e + 5] << 16);
-                            lv.w = lb[e + 6] | ((uint32_t)lb[e + 7] << 16);
-                            *reinterpret_cast<uint4*>(p.lo_dst + off + e) = lv;
+                            lv.x = lb[c8 * 8 + 0] | ((uint32_t)lb[c8 * 8 + 1] << 16);
+                            lv.y = lb[c8 * 8 + 2] | ((uint32_t)lb[c8 * 8 + 3] << 16);
+                            lv.z = lb[c8 * 8 + 4] | ((uint32_t)lb[c8 * 8 + 5] << 16);
+                            lv.w = lb[c8 * 8 + 6] | ((uint32_t)lb[c8 * 8 + 7] << 16);
+                            *reinterpret_cast<uint4*>(sLo + sw128(r, sub * 4 + c8)) = lv;
                         }
                     }
-                } else {
+                    // mirrored tile (rows = 64 columns of half h, cols = 128 rows of I):
+                    // element (r, cl) -> row cl - 64h, col r; box r/64 of 64x64
+                    uint8_t* mh = sHiT + (r >> 6) * 8192;
+                    uint8_t* ml = sLoT + (r >> 6) * 8192;
+                    const uint32_t cb = (uint32_t)(r & 63);
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        if (gj0 + e >= gi) {
-                            p.hi_dst[off + e] = hb[e];
-                            if (Tr::kHasLo) p.lo_dst[off + e] = lb[e];
+                    for (int e = 0; e < 32; ++e) {
+                        const uint32_t mr = sub * 32 + e;
+                        const uint32_t off = sw128(mr, cb >> 3) + (cb & 7) * 2;
+                        *reinterpret_cast<uint16_t*>(mh + off) = hb[e];
+                        if (Tr::kHasLo) *reinterpret_cast<uint16_t*>(ml + off) = lb[e];
+                    }
+                } else {
+                    // diagonal tile: symmetric 128x128 assembled from the upper triangle,
+                    // 2 boxes of 128 rows x 64 cols
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const uint32_t cl = cl0 + e;
+                        if ((int)cl >= r) {
+                            uint32_t off = (cl >> 6) * 16384 + sw128(r, (cl & 63) >> 3) + (cl & 7) * 2;
+                            *reinterpret_cast<uint16_t*>(sHiD + off) = hb[e];
+                            if (Tr::kHasLo) *reinterpret_cast<uint16_t*>(sLoD + off) = lb[e];
+                            off = (r >> 6) * 16384 + sw128(cl, (r & 63) >> 3) + (r & 7) * 2;
+                            *reinterpret_cast<uint16_t*>(sHiD + off) = hb[e];
+                            if (Tr::kHasLo) *reinterpret_cast<uint16_t*>(sLoD + off) = lb[e];
                         }
                     }
                 }
-                // mirrored store: element (gi, gj) -> (gj, gi); lanes cover consecutive gi
+                fence_proxy_async_smem();
+                named_bar_sync(2, kEpiWarps * 32);
+                if (warp == 2 && lane == 0) {
+                    for (int b = 0; b < 2; ++b) {
+                        tma_store_2d(&tm.x, sX + (h * 2 + b) * 16384, J * kBN + h * 64 + 32 * b, rowI);
+                        tma_store_2d(&tm.a, sA + (h * 2 + b) * 16384, J * kBN + h * 64 + 32 * b, rowI);
+                    }
+                    if (!diag) {
+                        tma_store_2d(&tm.hid, sHi, J * kBN + h * 64, rowI);
+                        if (Tr::kHasLo) tma_store_2d(&tm.lod, sLo, J * kBN + h * 64, rowI);
+                        for (int b = 0; b < 2; ++b) {
+                            tma_store_2d(&tm.him, sHiT + b * 8192, I * kBM + 64 * b, rowJ + h * 64);
+                            if (Tr::kHasLo)
+                                tma_store_2d(&tm.lom, sLoT + b * 8192, I * kBM + 64 * b, rowJ + h * 64);
+                        }
+                    } else if (h == 1) {
+                        for (int b = 0; b < 2; ++b) {
+                            tma_store_2d(&tm.hid, sHiD + b * 16384, I * kBM + 64 * b, rowI);
+                            if (Tr::kHasLo) tma_store_2d(&tm.lod, sLoD + b * 16384, I * kBM + 64 * b, rowI);
+                        }
+                    }
+                    tma_store_commit();
+                    tma_store_wait_read();  // staging reusable for the next half
+                }
+                named_bar_sync(2, kEpiWarps * 32);
+            }
+            if (warp == 2 && lane == 0) tma_store_wait_all();
+        } else {
+            // ============================== last layer: D = A + X_L, statistics
+#pragma unroll
+            for (int ch = 0; ch < kEpiCols / 16; ++ch) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tlane + kHL + hc * kEpiCols + ch * 16, v);
+                const int gj0 = J * kBN + hc * kEpiCols + ch * 16;
+                const size_t off = mat + (size_t)gi * np + gj0;
+                float xo[16], ao[16];
+#pragma unroll
+                for (int e = 0; e < 16; e += 4) {
+                    const float4 xv = *reinterpret_cast<const float4*>(p.X + off + e);
+                    const float4 av = *reinterpret_cast<const float4*>(p.A + off + e);
+                    xo[e] = xv.x; xo[e + 1] = xv.y; xo[e + 2] = xv.z; xo[e + 3] = xv.w;
+                    ao[e] = av.x; ao[e + 1] = av.y; ao[e + 2] = av.z; ao[e + 3] = av.w;
+                }
+                tmem_ld_wait();
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     const int gj = gj0 + e;
-                    if (gj > gi) {
-                        const size_t moff = mat + (size_t)gj * np + gi;
-                        p.hi_dst[moff] = hb[e];
-                        if (Tr::kHasLo) p.lo_dst[moff] = lb[e];
+                    double xd = p.a * (double)__uint_as_float(v[e]) + p.b * (double)xo[e];
+                    if (gi == gj && gi < n) xd += p.c;
+                    const float xn = (float)xd;
+                    const bool own = !diag || gj >= gi;
+                    bad_nf |= own && !isfinite(xn);
+                    if (own && gi < n && gj < n) {
+                        const double dv = (double)ao[e] + (double)xn;
+                        if (p.D) {
+                            double* Dm = p.D + (size_t)m * n * n;
+                            Dm[(size_t)gi * n + gj] = dv;
+                            if (gi != gj) Dm[(size_t)gj * n + gi] = dv;
+                        }
+                        if (gi != gj) {
+                            sq += 2.0 * dv * dv;
+                        } else {
+                            tr += dv;
+                            sq += dv * dv;
+                        }
                     }
                 }
             }
@@ -523,7 +648,7 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
                 red[2 * (warp - 2) + 0] = tr;
                 red[2 * (warp - 2) + 1] = sq;
             }
-            asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+            named_bar_sync(1, kEpiWarps * 32);
             if (warp == 2 && lane == 0) {
                 double T0 = 0.0, T1 = 0.0;
                 for (int w = 0; w < kEpiWarps; ++w) {  // fixed order

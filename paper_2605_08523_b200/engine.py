@@ -109,7 +109,8 @@ class _Prov(ctypes.Structure):
 SYMBOLS = ("ffg_abi_version", "ffg_last_error", "ffg_device_available", "ffg_in_region_of_validity",
            "ffg_spectral_bounds", "ffg_apply_model", "ffg_mixed_square", "ffg_density_statistics",
            "ffg_density_matrix", "ffg_density_matrices", "ffg_density_matrices_dev",
-           "ffg_kernel_launches", "ffg_release_workspaces")
+           "ffg_kernel_launches", "ffg_profile_layers", "ffg_profile_read",
+           "ffg_release_workspaces")
 
 
 @lru_cache(maxsize=None)
@@ -141,6 +142,8 @@ def lib() -> ctypes.CDLL:
     L.ffg_kernel_launches.restype = ctypes.c_int64
     L.ffg_kernel_launches.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(_Model),
                                       ctypes.c_int32]
+    L.ffg_profile_layers.argtypes = [ctypes.c_int]
+    L.ffg_profile_read.argtypes = [_D, ctypes.POINTER(ctypes.c_int64)]
     L.ffg_release_workspaces.restype = None
     assert L.ffg_abi_version() == 1
     return L
@@ -365,6 +368,19 @@ def compute_density_matrices_device(H_dev, mu, kT, model: Mlsp2Model,
 def kernel_launches(batch: int, n: int, model: Mlsp2Model, mode=PrecisionMode.MIXED_EMULATED) -> int:
     m = model._c()
     return int(lib().ffg_kernel_launches(batch, n, ctypes.byref(m), int(mode)))
+
+
+def profile_layers(enable: bool) -> None:
+    """Bracket every layer-kernel launch with CUDA events (measurement only)."""
+    _check(lib().ffg_profile_layers(1 if enable else 0))
+
+
+def profile_read() -> tuple[float, int]:
+    """(summed layer-kernel device ms, launches) since the last read."""
+    t = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(lib().ffg_profile_read(ctypes.byref(t), ctypes.byref(n)))
+    return t.value, n.value
 
 
 def algorithmic_flops(n: int, layers: int, mode: PrecisionMode) -> float:
