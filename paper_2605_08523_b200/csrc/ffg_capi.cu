@@ -315,8 +315,19 @@ int launch_layer_dr(const LayerMaps& maps, const LayerParams& p, int grid, cudaS
     return FFG_OK;
 }
 
+// Layers whose rounding errors are least amplified by the rest of the recursion (the last
+// `tail` ones) may drain the hi*hi accumulator per K-block instead of per MMA.
+int drain_tail() {
+    static int v = [] {
+        const char* e = getenv("FFG_DRAIN_TAIL");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <int MODE>
 int launch_layer(const LayerMaps& maps, const LayerParams& p, int grid, cudaStream_t st) {
+    if (p.layer >= p.n_layers - drain_tail()) return launch_layer_dr<MODE, 4>(maps, p, grid, st);
     switch (drain_granularity()) {
         case 4: return launch_layer_dr<MODE, 4>(maps, p, grid, st);
         case 2: return launch_layer_dr<MODE, 2>(maps, p, grid, st);
@@ -435,6 +446,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         lp.nb = nb;
         lp.T = (int)T;
         lp.layer = l;
+        lp.n_layers = md.n_layers;
         lp.dbg = debug_flags();
         LayerMaps maps;
         maps.hi = w.tm[2 * par + 0];

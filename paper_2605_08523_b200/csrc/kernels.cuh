@@ -46,8 +46,11 @@ constexpr int kLayerThreads = 64 + kEpiWarps * 32;
 template <int MODE>
 struct ModeTraits;
 template <>
+#ifndef FFG_F32E_STAGES
+#define FFG_F32E_STAGES 3
+#endif
 struct ModeTraits<kModeF32E> {  // FP32-emulated: hi*hi + hi*lo + lo*hi, one accumulator
-    static constexpr int kProducts = 3, kFmt = 0, kHasLo = 1, kStages = 3;
+    static constexpr int kProducts = 3, kFmt = 0, kHasLo = 1, kStages = FFG_F32E_STAGES;
     static constexpr float kScale = kHalfScale;
 };
 template <>
@@ -66,9 +69,14 @@ constexpr int stage_bytes() {
     return (ModeTraits<MODE>::kHasLo ? 4 : 2) * kOpBytes;
 }
 template <int MODE>
+constexpr int layer_pipe_bytes() {  // pipeline stages; reused as epilogue staging (192 KB)
+    return ModeTraits<MODE>::kStages * stage_bytes<MODE>() > 192 * 1024
+               ? ModeTraits<MODE>::kStages * stage_bytes<MODE>()
+               : 192 * 1024;
+}
+template <int MODE>
 constexpr int layer_smem_bytes() {
-    return ModeTraits<MODE>::kStages * stage_bytes<MODE>() + 1024 /*barriers, scratch*/ +
-           1024 /*alignment slack*/;
+    return layer_pipe_bytes<MODE>() + 1024 /*barriers, scratch*/ + 1024 /*alignment slack*/;
 }
 
 // 16-bit operand encodings (raw bits) -------------------------------------------------
@@ -226,6 +234,7 @@ struct LayerParams {
     double a, b, c, d_next;
     int n, np, nb, T;     // nb = np/128 tile rows, T = nb(nb+1)/2 upper tiles
     int layer, last;      // layer index l (produces X_{l+1})
+    int n_layers;
     int dbg;              // measurement only: bit0 skip epilogue memory traffic, bit1 skip drain
 };
 
@@ -282,18 +291,19 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
     constexpr uint32_t kHL = 384;  // TMEM column of the cross-term accumulator / final Y
     constexpr int NHB = 3;         // hi*hi accumulator ring
     static_assert(DR == 1 || DR == 2 || DR == 4, "drain granularity");
-    static_assert(S * SB >= 192 * 1024, "epilogue staging reuses 192 KB of pipeline smem");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
+    constexpr int kPipe = layer_pipe_bytes<MODE>();
+    constexpr bool kDrain = Tr::kProducts == 3;  // single-product modes accumulate in TMEM
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPipe);
     uint64_t* empty = full + S;
     uint64_t* hh_full = empty + S;       // [NHB]
     uint64_t* hh_empty = hh_full + NHB;  // [NHB]
     uint64_t* hl_full = hh_empty + NHB;
     uint64_t* xa_full = hl_full + 1;     // X/A tiles landed in smem
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_full + 1);
-    double* red = reinterpret_cast<double*>(smem + S * SB + 512);
+    double* red = reinterpret_cast<double*>(smem + kPipe + 512);
 
     // epilogue staging inside the pipeline smem (valid once the mainloop is done)
     uint8_t* sX = smem;                  // [half][box 0..1] 128 rows x 32 fp32, 16 KB boxes
@@ -392,15 +402,20 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
                 for (int kk = 0; kk < kBK / kUK; ++kk) {
                     const uint32_t koff = kk * kUK * 2;  // bytes along K inside the atom
                     const int hb = g % NHB;
-                    if (kk % DR == 0 && !(p.dbg & 2)) {
-                        mbar_wait(&hh_empty[hb], ((g / NHB) & 1) ^ 1);  // drained by the epilogue
-                        tc_fence_after();
-                    }
-                    umma_f16(tmem + hb * 128, umma_desc_sw128(a_hi + koff),
-                             umma_desc_sw128(b_hi + koff), idesc, (kk % DR) != 0);
-                    if (kk % DR == DR - 1) {
-                        if (!(p.dbg & 2)) umma_commit(&hh_full[hb]);
-                        ++g;
+                    if (!kDrain) {
+                        umma_f16(tmem + kHL, umma_desc_sw128(a_hi + koff),
+                                 umma_desc_sw128(b_hi + koff), idesc, (kb | kk) != 0);
+                    } else {
+                        if (kk % DR == 0 && !(p.dbg & 2)) {
+                            mbar_wait(&hh_empty[hb], ((g / NHB) & 1) ^ 1);  // drained by the epilogue
+                            tc_fence_after();
+                        }
+                        umma_f16(tmem + hb * 128, umma_desc_sw128(a_hi + koff),
+                                 umma_desc_sw128(b_hi + koff), idesc, (kk % DR) != 0);
+                        if (kk % DR == DR - 1) {
+                            if (!(p.dbg & 2)) umma_commit(&hh_full[hb]);
+                            ++g;
+                        }
                     }
                     if (Tr::kProducts == 3) {
                         umma_f16(tmem + kHL, umma_desc_sw128(a_hi + koff),
@@ -427,23 +442,26 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
         float yacc[kEpiCols];
 #pragma unroll
         for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
+        static_assert(kEpiCols == 64, "drain loads two 32-column chunks");
 #pragma unroll 1
-        for (int g = 0; g < ((p.dbg & 2) ? 0 : nk * (kBK / kUK) / DR); ++g) {
+        for (int g = 0; g < ((p.dbg & 2) || !kDrain ? 0 : nk * (kBK / kUK) / DR); ++g) {
             const int hb = g % NHB;
             mbar_wait(&hh_full[hb], (g / NHB) & 1);
             tc_fence_after();
+            uint32_t v0[32], v1[32];
+            tmem_ld_32x32b_x32(tlane + hb * 128 + hc * kEpiCols, v0);
+            tmem_ld_32x32b_x32(tlane + hb * 128 + hc * kEpiCols + 32, v1);
+            tmem_ld_wait();
 #pragma unroll
-            for (int ch = 0; ch < kEpiCols / 32; ++ch) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tlane + hb * 128 + hc * kEpiCols + ch * 32, v);
-                tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    float2 acc = make_float2(yacc[ch * 32 + e], yacc[ch * 32 + e + 1]);
-                    acc = add_f32x2(acc, make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
-                    yacc[ch * 32 + e] = acc.x;
-                    yacc[ch * 32 + e + 1] = acc.y;
-                }
+            for (int e = 0; e < 32; e += 2) {
+                float2 acc = make_float2(yacc[e], yacc[e + 1]);
+                acc = add_f32x2(acc, make_float2(__uint_as_float(v0[e]), __uint_as_float(v0[e + 1])));
+                yacc[e] = acc.x;
+                yacc[e + 1] = acc.y;
+                acc = make_float2(yacc[32 + e], yacc[32 + e + 1]);
+                acc = add_f32x2(acc, make_float2(__uint_as_float(v1[e]), __uint_as_float(v1[e + 1])));
+                yacc[32 + e] = acc.x;
+                yacc[32 + e + 1] = acc.y;
             }
             tc_fence_before();
             __syncwarp();
@@ -456,14 +474,11 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
         for (int ch = 0; ch < kEpiCols / 32; ++ch) {
             const uint32_t ta = tlane + kHL + hc * kEpiCols + ch * 32;
             uint32_t v[32];
-            if (Tr::kProducts == 3) {
-                tmem_ld_32x32b_x32(ta, v);
-                tmem_ld_wait();
-            }
+            tmem_ld_32x32b_x32(ta, v);
+            tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
-                const float y = Tr::kProducts == 3 ? yacc[ch * 32 + e] + __uint_as_float(v[e])
-                                                   : yacc[ch * 32 + e];
+                const float y = kDrain ? yacc[ch * 32 + e] + __uint_as_float(v[e]) : __uint_as_float(v[e]);
                 v[e] = __float_as_uint(y * inv_s2);
             }
             if (p.dbg & 2) {  // measurement only: no drain -> Y is the cross-term accumulator

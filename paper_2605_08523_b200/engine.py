@@ -30,7 +30,7 @@ from typing import Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libfermiforge_b200.so")
+LIB_PATH = os.environ.get("FFG_LIB_PATH") or os.path.join(_PKG, "lib", "libfermiforge_b200.so")
 
 _D = ctypes.POINTER(ctypes.c_double)
 _F = ctypes.POINTER(ctypes.c_float)
