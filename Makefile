@@ -17,10 +17,6 @@ $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; false)
 	@grep -E "registers|spill" $(PKG)/lib/ptxas.log | sed 's/^/  /' | head -20
 
-# experiment: 2-stage FP32-emulated pipeline (not the product build)
-lib-s2: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -DFFG_F32E_STAGES=2 -shared -o $(PKG)/lib/libfermiforge_b200_s2.so $(SRCS) 2> /dev/null
-
 oracle:
 	$(MAKE) -s -C oracle
 

@@ -116,9 +116,9 @@ EncodeTiledFn encode_fn() {
 }
 
 // Row-major matrix [rows][np] of 16-bit (elem=2) or fp32 (elem=4) values viewed by TMA as
-// box_rows x box_cols boxes with the 128-byte swizzle (box_cols * elem == 128).
+// box_rows x box_cols boxes with a 128-byte (box_cols * elem == 128) or 64-byte swizzle.
 int make_map(CUtensorMap* tm, void* base, int64_t rows, int64_t np, int elem, int box_cols,
-             int box_rows) {
+             int box_rows, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeTiledFn enc = encode_fn();
     if (!enc) return set_err(FFG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)np, (cuuint64_t)rows};
@@ -127,7 +127,7 @@ int make_map(CUtensorMap* tm, void* base, int64_t rows, int64_t np, int elem, in
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(tm, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                      2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(FFG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return FFG_OK;
@@ -156,10 +156,10 @@ struct Workspace {
     void* host_small = nullptr;     // pinned readback: stats, bounds, status, flags
     size_t host_small_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // tensor-map cache: [0..3] operands hi0 lo0 hi1 lo1 (64x128 boxes), [4..7] the same
-    // arrays as 64x64 mirror boxes, [8] X, [9] A (fp32, 32x128 boxes)
+    // tensor-map cache over the operand arrays hi0 lo0 hi1 lo1: [0..3] 64x128 operand boxes
+    // (SW128), [4..7] 32x32 epilogue pieces (SW64)
     int tm_B = -1, tm_np = -1;
-    CUtensorMap tm[10];
+    CUtensorMap tm[8];
     std::mutex mu;
 };
 
@@ -284,6 +284,16 @@ __global__ void row_stats_kernel(const double* D, int n, double2* partials) {
     if (lane == 0) partials[i] = make_double2(dg, sq);
 }
 
+// Layers 0..exact-1 drain the hi*hi accumulator after every MMA, later layers once per
+// K-block (their rounding is amplified far less by the remaining recursion).
+int exact_drain_layers() {
+    static int v = [] {
+        const char* e = getenv("FFG_EXACT_DRAIN_LAYERS");
+        return e ? atoi(e) : 10;
+    }();
+    return v;
+}
+
 int debug_flags() {
     static int v = [] {
         const char* e = getenv("FFG_DEBUG_K2");
@@ -292,47 +302,28 @@ int debug_flags() {
     return v;
 }
 
-int drain_granularity() {
-    static int dr = [] {
-        const char* e = getenv("FFG_DRAIN_K16");
-        const int v = e ? atoi(e) : 1;
-        return (v == 2 || v == 4) ? v : 1;
-    }();
-    return dr;
-}
-
-template <int MODE, int DR>
-int launch_layer_dr(const LayerMaps& maps, const LayerParams& p, int grid, cudaStream_t st) {
-    static bool configured = false;
-    constexpr int smem = layer_smem_bytes<MODE>();
-    if (!configured) {
-        CK(cudaFuncSetAttribute(mlsp2_layer_kernel<MODE, DR>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        configured = true;
-    }
-    mlsp2_layer_kernel<MODE, DR><<<grid, kLayerThreads, smem, st>>>(maps, p);
-    CK(cudaGetLastError());
-    return FFG_OK;
-}
-
-// Layers whose rounding errors are least amplified by the rest of the recursion (the last
-// `tail` ones) may drain the hi*hi accumulator per K-block instead of per MMA.
-int drain_tail() {
+int num_sms() {
     static int v = [] {
-        const char* e = getenv("FFG_DRAIN_TAIL");
-        return e ? atoi(e) : 0;
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
     }();
     return v;
 }
 
 template <int MODE>
-int launch_layer(const LayerMaps& maps, const LayerParams& p, int grid, cudaStream_t st) {
-    if (p.layer >= p.n_layers - drain_tail()) return launch_layer_dr<MODE, 4>(maps, p, grid, st);
-    switch (drain_granularity()) {
-        case 4: return launch_layer_dr<MODE, 4>(maps, p, grid, st);
-        case 2: return launch_layer_dr<MODE, 2>(maps, p, grid, st);
-        default: return launch_layer_dr<MODE, 1>(maps, p, grid, st);
+int launch_layer(const LayerMaps& maps, const LayerParams& p, int tiles, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        CK(cudaFuncSetAttribute(mlsp2_layer_persistent<MODE>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kPersistSmem));
+        configured = true;
     }
+    const int grid = std::min(tiles, num_sms());
+    mlsp2_layer_persistent<MODE><<<grid, kPersistThreads, kPersistSmem, st>>>(maps, p);
+    CK(cudaGetLastError());
+    return FFG_OK;
 }
 
 // Optional CUDA-event timing of every K2 (layer) launch, for the roofline figure.
@@ -388,10 +379,10 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     if (w.tm_B != B || w.tm_np != (int)np) {
         for (int k = 0; k < 4; ++k) {
             if ((rc = make_map(&w.tm[k], w.op[k], (int64_t)B * np, np, 2, 64, 128))) return rc;
-            if ((rc = make_map(&w.tm[4 + k], w.op[k], (int64_t)B * np, np, 2, 64, 64))) return rc;
+            if ((rc = make_map(&w.tm[4 + k], w.op[k], (int64_t)B * np, np, 2, 32, 32,
+                               CU_TENSOR_MAP_SWIZZLE_64B)))
+                return rc;
         }
-        if ((rc = make_map(&w.tm[8], w.X, (int64_t)B * np, np, 4, 32, 128))) return rc;
-        if ((rc = make_map(&w.tm[9], w.A, (int64_t)B * np, np, 4, 32, 128))) return rc;
         w.tm_B = B;
         w.tm_np = (int)np;
     }
@@ -447,23 +438,21 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         lp.T = (int)T;
         lp.layer = l;
         lp.n_layers = md.n_layers;
+        lp.exact_layers = exact_drain_layers();
+        lp.B = B;
         lp.dbg = debug_flags();
         LayerMaps maps;
         maps.hi = w.tm[2 * par + 0];
         maps.lo = w.tm[2 * par + 1];
-        maps.hid = w.tm[2 * (par ^ 1) + 0];
-        maps.lod = w.tm[2 * (par ^ 1) + 1];
-        maps.him = w.tm[4 + 2 * (par ^ 1) + 0];
-        maps.lom = w.tm[4 + 2 * (par ^ 1) + 1];
-        maps.x = w.tm[8];
-        maps.a = w.tm[9];
-        const int grid = (int)(B * T);
+        maps.hip = w.tm[4 + 2 * (par ^ 1) + 0];
+        maps.lop = w.tm[4 + 2 * (par ^ 1) + 1];
+        const int tiles = (int)(B * T);
         cudaEvent_t stop;
         if ((rc = prof_begin(st, &stop))) return rc;
         switch (j.mode) {
-            case kModeF32E: rc = launch_layer<kModeF32E>(maps, lp, grid, st); break;
-            case kModeF16: rc = launch_layer<kModeF16>(maps, lp, grid, st); break;
-            default: rc = launch_layer<kModeBF16>(maps, lp, grid, st); break;
+            case kModeF32E: rc = launch_layer<kModeF32E>(maps, lp, tiles, st); break;
+            case kModeF16: rc = launch_layer<kModeF16>(maps, lp, tiles, st); break;
+            default: rc = launch_layer<kModeBF16>(maps, lp, tiles, st); break;
         }
         if (rc) return rc;
         if (stop) CK(cudaEventRecord(stop, st));

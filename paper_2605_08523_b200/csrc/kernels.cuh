@@ -108,9 +108,9 @@ struct RescaleParams {
     const double* alpha;        // [B] X0 = alpha_m H + gamma_m I
     const double* gamma;        // [B]
     double d0;                  // first accumulator weight: A1 = d0 X0
-    float* X;                   // [B][np][np]
-    float* A;                   // [B][np][np]
-    uint16_t* hi;               // [B][np][np] parity 0
+    float* X;                   // [B][np][np] tile-interleaved (xa_tile_base)
+    float* A;                   // [B][np][np] tile-interleaved
+    uint16_t* hi;               // [B][np][np] parity 0, row-major
     uint16_t* lo;               // [B][np][np] parity 0 (F32E only)
     unsigned long long* bounds; // [B][2] ordered keys of (eps_min, eps_max) before widening
     int* flags;                 // [B][2] first bad X_k index: [0] non-finite, [1] half range
@@ -158,13 +158,16 @@ __global__ void __launch_bounds__(256) rescale_gershgorin_kernel(const __grid_co
                 bad_nf |= !isfinite(x[e]);
             }
             if (p.write_operands) {
-                *reinterpret_cast<float4*>(p.X + orow + j0) = make_float4(x[0], x[1], x[2], x[3]);
+                // X / A: tile-interleaved layout (see xa_tile_base); hi / lo: row-major
+                const size_t xo = ((((size_t)m * (np / 128) + i / 128) * (np / 128) + j0 / 128) * 16384) +
+                                  ((size_t)((j0 & 127) >> 2) * 128 + (i & 127)) * 4;
+                *reinterpret_cast<float4*>(p.X + xo) = make_float4(x[0], x[1], x[2], x[3]);
                 const float d0 = (float)p.d0;
                 float a[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) a[e] = (float)(p.d0 * (double)x[e]);
                 (void)d0;
-                *reinterpret_cast<float4*>(p.A + orow + j0) = make_float4(a[0], a[1], a[2], a[3]);
+                *reinterpret_cast<float4*>(p.A + xo) = make_float4(a[0], a[1], a[2], a[3]);
                 uint16_t hb[4], lb[4];
                 if (p.mode == kModeBF16) {
 #pragma unroll
@@ -235,7 +238,9 @@ struct LayerParams {
     int n, np, nb, T;     // nb = np/128 tile rows, T = nb(nb+1)/2 upper tiles
     int layer, last;      // layer index l (produces X_{l+1})
     int n_layers;
-    int dbg;              // measurement only: bit0 skip epilogue memory traffic, bit1 skip drain
+    int exact_layers;     // layers draining hi*hi after every MMA (the rest: per K-block)
+    int B;                // matrices in this launch
+    int dbg;              // measurement only: 1 = skip epilogue work, 2 = skip loads/MMAs/drain
 };
 
 __device__ __forceinline__ void decode_upper_tile(int t, int nb, int& I, int& J) {
@@ -252,91 +257,91 @@ __device__ __forceinline__ void decode_upper_tile(int t, int nb, int& I, int& J)
 
 struct LayerMaps {
     CUtensorMap hi, lo;      // operand source (parity l&1): box 64 x 128, SW128
-    CUtensorMap hid, lod;    // operand destination (parity (l+1)&1): box 64 x 128, SW128
-    CUtensorMap him, lom;    // mirrored destination: box 64 x 64, SW128
-    CUtensorMap x, a;        // fp32 master X / accumulator A: box 32 x 128, SW128
+    CUtensorMap hip, lop;    // destination (parity (l+1)&1): 32 x 32 pieces, SW64
 };
 
-// byte offset of 16-byte chunk `c` of row `r` in a 128-byte-row tile with the TMA/UMMA
-// 128B swizzle (tile base 1024-aligned)
-__device__ __forceinline__ uint32_t sw128(uint32_t r, uint32_t c) {
-    return r * 128u + ((c ^ (r & 7u)) << 4);
+// X and A live in a tile-interleaved layout: tile (I,J) of matrix m is a contiguous
+// 128x128 fp32 block stored as [32 column-quads][128 rows][4]; element (r, c) of the tile
+// at ((c/4)*128 + r)*4 + c%4.  A warp whose lanes own consecutive rows then reads/writes
+// 512 contiguous bytes per float4 access.
+__host__ __device__ __forceinline__ size_t xa_tile_base(int m, int I, int J, int nb) {
+    return (((size_t)m * nb + I) * nb + J) * (size_t)(kBM * kBN);
+}
+__host__ __device__ __forceinline__ uint32_t xa_off(int r, int c4) {  // float offset of quad c4, row r
+    return ((uint32_t)c4 * kBM + (uint32_t)r) * 4u;
+}
+// byte offset of 16-byte chunk c of row r in a tile of 64-byte rows, 64B swizzle
+__device__ __forceinline__ uint32_t sw64(uint32_t r, uint32_t c) {
+    return r * 64u + ((c ^ ((r >> 1) & 3u)) << 4);
 }
 
-// Warp roles: 0 = TMA producer (+ epilogue TMA issue), 1 = TMEM allocator + UMMA issuer,
-// 2..9 = accumulator-drain / epilogue warps (warp w reads TMEM lanes 32*(w%4)..+31; its
-// column half during the drain is (w-2)/4).  One 128x128 upper-triangular tile per CTA.
+constexpr int kEpiWarps2 = 8;                                       // epilogue warps
+constexpr int kPersistThreads = 128 + kEpiWarps * 32 + kEpiWarps2 * 32;  // 640
+constexpr int kPipeStages = 2;                                      // 2 x 64 KB operand stages
+constexpr int kStageBytes = 4 * kOpBytes;
+constexpr int kStagingOff = kPipeStages * kStageBytes;              // 128 KB
+constexpr int kPieceBytes = 32 * 64;                                // 32x32 binary16 piece
+constexpr int kStagingBytes = kEpiWarps2 * 4 * kPieceBytes;         // 64 KB
+constexpr int kPersistSmem = kStagingOff + kStagingBytes + 1024 + 1024;
+// setmaxnreg budgets: they can only redistribute the launch allocation (640 threads x 96)
+constexpr int kRegsCtl = 32, kRegsDrain = 104, kRegsEpi = 120;
+static_assert(128 * kRegsCtl + kEpiWarps * 32 * kRegsDrain + kEpiWarps2 * 32 * kRegsEpi <= 640 * 96,
+              "setmaxnreg targets exceed the CTA register allocation (would deadlock)");
+
+// Persistent, warp-specialised MLSP2 layer.  One CTA per SM walks the (matrix, upper tile)
+// list; per tile the tensor core squares a 128x128 block while the epilogue of the previous
+// tile runs:
+//   warp 0        TMA producer of the hi/lo operand panels (2 x 64 KB stages)
+//   warp 1        TMEM allocator + UMMA issuer            (warps 2,3 idle; warpgroup 0)
+//   warps 4-11    drain the hi*hi TMEM ring into fp32 registers (round-to-nearest adds) and
+//                 form Y = (hi*hi + cross terms)/scale^2 in the tile's TMEM accumulator
+//   warps 12-19   epilogue: X' = aY + bX + cI, A += d'X', binary16 split.  X/A are read
+//                 and written in place (coalesced, tile-interleaved layout); the split
+//                 leaves as 32x32 direct and mirrored pieces through per-warp SMEM staging
+//                 and TMA stores.  Last layer: D = A + X_L and the statistics.
+// TMEM: [0,256) hi*hi ring (2 x 128), [256,384) / [384,512) per-tile accumulators (cross
+// terms, then Y), double-buffered across tiles.
 //
-// Accumulation precision.  tcgen05 FP32 accumulation truncates inside every MMA.  Summing
-// hi*lo terms into the large hi*hi accumulator, or letting hi*hi accumulate over the whole
-// K extent, biases Tr D by ~3e-6 (measured on B200, reproduced by emulation).
-// So hi*lo + lo*hi go to their own TMEM accumulator (2^-11 smaller, its truncation is
-// negligible) and every hi*hi MMA (DR=1) lands in a fresh buffer of a 3-deep TMEM ring that
-// the epilogue warps drain into fp32 registers with round-to-nearest adds (FADD2) while the
-// tensor core fills the next buffer.
-// TMEM columns: [0,384) hi*hi ring, [384,512) cross terms, then the final Y.
-//
-// Epilogue (layers 0..L-2): Y = drained hi*hi + cross terms is written back to TMEM; X and A
-// tiles come in by TMA into the (now idle) pipeline SMEM; X' = aY + bX + cI, A += d' X' and
-// the split of X' are computed in swizzled SMEM and leave by TMA bulk stores: X, A and the
-// direct hi/lo tile at (I,J), the transposed hi/lo tile at (J,I) (for a diagonal tile one
-// symmetric 128x128 tile assembled from its upper triangle).  Last layer: D = A + X_L with
-// direct fp64 stores and the per-tile statistics.
-template <int MODE, int DR>
-__global__ void __launch_bounds__(kLayerThreads, 1)
-    mlsp2_layer_kernel(const __grid_constant__ LayerMaps tm, const __grid_constant__ LayerParams p) {
+// Accumulation precision: tcgen05 FP32 accumulation truncates inside every MMA.  Cross
+// terms (2^-11 smaller) have their own accumulator; hi*hi is drained after every MMA for the
+// first `exact_layers` layers (their errors are amplified by all later layers, up to
+// beta0/4) and after every K-block afterwards ("accumulation precision").
+template <int MODE>
+__global__ void __launch_bounds__(kPersistThreads, 1)
+    mlsp2_layer_persistent(const __grid_constant__ LayerMaps tm, const __grid_constant__ LayerParams p) {
     using Tr = ModeTraits<MODE>;
-    constexpr int S = Tr::kStages;
-    constexpr int SB = stage_bytes<MODE>();
-    constexpr uint32_t kHL = 384;  // TMEM column of the cross-term accumulator / final Y
-    constexpr int NHB = 3;         // hi*hi accumulator ring
-    static_assert(DR == 1 || DR == 2 || DR == 4, "drain granularity");
+    constexpr bool kDrain = Tr::kProducts == 3;
+    constexpr int NHB = 2;
+    constexpr uint32_t kAcc0 = 256;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    constexpr int kPipe = layer_pipe_bytes<MODE>();
-    constexpr bool kDrain = Tr::kProducts == 3;  // single-product modes accumulate in TMEM
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPipe);
-    uint64_t* empty = full + S;
-    uint64_t* hh_full = empty + S;       // [NHB]
-    uint64_t* hh_empty = hh_full + NHB;  // [NHB]
-    uint64_t* hl_full = hh_empty + NHB;
-    uint64_t* xa_full = hl_full + 1;     // X/A tiles landed in smem
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xa_full + 1);
-    double* red = reinterpret_cast<double*>(smem + kPipe + 512);
-
-    // epilogue staging inside the pipeline smem (valid once the mainloop is done)
-    uint8_t* sX = smem;                  // [half][box 0..1] 128 rows x 32 fp32, 16 KB boxes
-    uint8_t* sA = smem + 64 * 1024;
-    uint8_t* sHi = smem + 128 * 1024;    // off-diag: direct 128x64 (16 KB); diag: 2 boxes 128x64
-    uint8_t* sLo = smem + 144 * 1024;
-    uint8_t* sHiT = smem + 160 * 1024;   // off-diag: mirrored 64x128 as 2 boxes 64x64 (8 KB)
-    uint8_t* sLoT = smem + 176 * 1024;
-    uint8_t* sHiD = smem + 128 * 1024;   // diag: symmetric 128x128 hi as 2 boxes 128x64 (32 KB)
-    uint8_t* sLoD = smem + 160 * 1024;   // diag: symmetric 128x128 lo
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStagingOff + kStagingBytes);
+    uint64_t* full = bars;                // [2]
+    uint64_t* empty = bars + 2;           // [2]
+    uint64_t* hh_full = bars + 4;         // [2]
+    uint64_t* hh_empty = bars + 6;        // [2]
+    uint64_t* acc_full = bars + 8;        // [2]
+    uint64_t* y_full = bars + 10;         // [2]
+    uint64_t* acc_empty = bars + 12;      // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    double* red = reinterpret_cast<double*>(bars + 16);  // [8][2]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m = blockIdx.x / p.T;
-    const int t = blockIdx.x - m * p.T;
-    int I, J;
-    decode_upper_tile(t, p.nb, I, J);
-    const bool diag = (I == J);
+    const int total = p.B * p.T;
     const int nk = p.np / kBK;
-    const bool tma_epi = !p.last && !(p.dbg & 1);
-    const int rowI = m * p.np + I * kBM;
-    const int rowJ = m * p.np + J * kBN;
+    const int drain_dr = (p.layer < p.exact_layers) ? 1 : 4;  // K16 MMAs per hi*hi fill
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+            mbar_init(&hh_full[i], 1);
+            mbar_init(&hh_empty[i], kEpiWarps);
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&y_full[i], kEpiWarps);
+            mbar_init(&acc_empty[i], kEpiWarps2);
         }
-        for (int b = 0; b < NHB; ++b) {
-            mbar_init(&hh_full[b], 1);
-            mbar_init(&hh_empty[b], kEpiWarps);  // one arrive per epilogue warp
-        }
-        mbar_init(hl_full, 1);
-        mbar_init(xa_full, 1);
         fence_barrier_init();
         tma_prefetch_desc(&tm.hi);
         if (Tr::kHasLo) tma_prefetch_desc(&tm.lo);
@@ -347,332 +352,320 @@ __global__ void __launch_bounds__(kLayerThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
-        // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            if (tma_epi) {  // warm L2 with this tile's X / A for the epilogue
-                for (int b = 0; b < 4; ++b) {
-                    tma_prefetch_l2_2d(&tm.x, J * kBN + 32 * b, rowI);
-                    tma_prefetch_l2_2d(&tm.a, J * kBN + 32 * b, rowI);
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsCtl) : "memory");
+        if (warp == 0 && lane == 0) {
+            // ============================================= TMA producer
+            int it = 0;
+            for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+                const int m = tile / p.T;
+                int I, J;
+                decode_upper_tile(tile - m * p.T, p.nb, I, J);
+                const bool diag = I == J;
+                const int rowI = m * p.np + I * kBM, rowJ = m * p.np + J * kBN;
+                if (!(p.dbg & 1)) {  // warm L2 with this tile's X / A for the epilogue
+                    const size_t tb = xa_tile_base(m, I, J, p.nb);
+                    tma_prefetch_l2_bulk(p.X + tb, kBM * kBN * 4);
+                    tma_prefetch_l2_bulk(p.A + tb, kBM * kBN * 4);
+                }
+                const uint32_t bytes = (diag ? (Tr::kHasLo ? 2 : 1) : (Tr::kHasLo ? 4 : 2)) * kOpBytes;
+                for (int kb = 0; kb < ((p.dbg & 2) ? 0 : nk); ++kb, ++it) {
+                    const int s = it & 1;
+                    mbar_wait(&empty[s], ((it >> 1) & 1) ^ 1);
+                    mbar_expect_tx(&full[s], bytes);
+                    uint8_t* st = smem + s * kStageBytes;
+                    tma_load_2d(st, &tm.hi, &full[s], kb * kBK, rowI);
+                    if (Tr::kHasLo) tma_load_2d(st + kOpBytes, &tm.lo, &full[s], kb * kBK, rowI);
+                    if (!diag) {
+                        tma_load_2d(st + 2 * kOpBytes, &tm.hi, &full[s], kb * kBK, rowJ);
+                        if (Tr::kHasLo) tma_load_2d(st + 3 * kOpBytes, &tm.lo, &full[s], kb * kBK, rowJ);
+                    }
                 }
             }
-            const uint32_t bytes = (diag ? (Tr::kHasLo ? 2 : 1) : (Tr::kHasLo ? 4 : 2)) * kOpBytes;
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % S;
-                const uint32_t ph = (kb / S) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                mbar_expect_tx(&full[s], bytes);
-                uint8_t* st = smem + s * SB;
-                tma_load_2d(st + 0 * kOpBytes, &tm.hi, &full[s], kb * kBK, rowI);
-                if (Tr::kHasLo) tma_load_2d(st + 1 * kOpBytes, &tm.lo, &full[s], kb * kBK, rowI);
-                if (!diag) {
-                    const int ob = Tr::kHasLo ? 2 : 1;
-                    tma_load_2d(st + ob * kOpBytes, &tm.hi, &full[s], kb * kBK, rowJ);
-                    if (Tr::kHasLo)
-                        tma_load_2d(st + (ob + 1) * kOpBytes, &tm.lo, &full[s], kb * kBK, rowJ);
-                }
-            }
-            if (tma_epi) {
-                // all MMAs retired -> every pipeline stage is free: bring X, A (both halves)
-                mbar_wait(hl_full, 0);
-                mbar_expect_tx(xa_full, 128 * 1024);
-                for (int b = 0; b < 4; ++b) {
-                    tma_load_2d(sX + b * 16384, &tm.x, xa_full, J * kBN + 32 * b, rowI);
-                    tma_load_2d(sA + b * 16384, &tm.a, xa_full, J * kBN + 32 * b, rowI);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------ UMMA issuer (one thread)
-        if (lane == 0) {
+        } else if (warp == 1 && lane == 0) {
+            // ============================================= UMMA issuer
             constexpr uint32_t idesc = umma_idesc_f16(Tr::kFmt, kBM, kBN);
-            int g = 0;  // index of the current hi*hi fill (DR K16 steps each)
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % S;
-                const uint32_t ph = (kb / S) & 1;
-                mbar_wait(&full[s], ph);
+            int it = 0, g = 0, u = 0;
+            for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++u) {
+                const int m = tile / p.T;
+                int I, J;
+                decode_upper_tile(tile - m * p.T, p.nb, I, J);
+                const bool diag = I == J;
+                const int ab = u & 1;
+                const uint32_t t_acc = tmem + kAcc0 + ab * 128;
+                mbar_wait(&acc_empty[ab], ((u >> 1) & 1) ^ 1);  // epilogue of tile u-2 read Y
                 tc_fence_after();
-                const uint32_t base = smem_u32(smem + s * SB);
-                const uint32_t a_hi = base;
-                const uint32_t a_lo = base + kOpBytes;
-                const uint32_t ob = diag ? 0 : (Tr::kHasLo ? 2 : 1) * kOpBytes;
-                const uint32_t b_hi = base + ob;
-                const uint32_t b_lo = base + ob + kOpBytes;
+                for (int kb = 0; kb < ((p.dbg & 2) ? 0 : nk); ++kb, ++it) {
+                    const int s = it & 1;
+                    mbar_wait(&full[s], (it >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t base = smem_u32(smem + s * kStageBytes);
+                    const uint32_t a_hi = base, a_lo = base + kOpBytes;
+                    const uint32_t ob = diag ? 0 : 2 * kOpBytes;
+                    const uint32_t b_hi = base + ob, b_lo = base + ob + kOpBytes;
 #pragma unroll
-                for (int kk = 0; kk < kBK / kUK; ++kk) {
-                    const uint32_t koff = kk * kUK * 2;  // bytes along K inside the atom
-                    const int hb = g % NHB;
-                    if (!kDrain) {
-                        umma_f16(tmem + kHL, umma_desc_sw128(a_hi + koff),
-                                 umma_desc_sw128(b_hi + koff), idesc, (kb | kk) != 0);
-                    } else {
-                        if (kk % DR == 0 && !(p.dbg & 2)) {
-                            mbar_wait(&hh_empty[hb], ((g / NHB) & 1) ^ 1);  // drained by the epilogue
-                            tc_fence_after();
-                        }
-                        umma_f16(tmem + hb * 128, umma_desc_sw128(a_hi + koff),
-                                 umma_desc_sw128(b_hi + koff), idesc, (kk % DR) != 0);
-                        if (kk % DR == DR - 1) {
-                            if (!(p.dbg & 2)) umma_commit(&hh_full[hb]);
-                            ++g;
+                    for (int kk = 0; kk < kBK / kUK; ++kk) {
+                        const uint32_t koff = kk * kUK * 2;
+                        if (!kDrain) {
+                            umma_f16(t_acc, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_hi + koff),
+                                     idesc, (kb | kk) != 0);
+                        } else {
+                            const int hb = g % NHB;
+                            if (kk % drain_dr == 0) {
+                                mbar_wait(&hh_empty[hb], ((g / NHB) & 1) ^ 1);
+                                tc_fence_after();
+                            }
+                            umma_f16(tmem + hb * 128, umma_desc_sw128(a_hi + koff),
+                                     umma_desc_sw128(b_hi + koff), idesc, (kk % drain_dr) != 0);
+                            if (kk % drain_dr == drain_dr - 1) {
+                                umma_commit(&hh_full[hb]);
+                                ++g;
+                            }
+                            umma_f16(t_acc, umma_desc_sw128(a_hi + koff), umma_desc_sw128(b_lo + koff),
+                                     idesc, (kb | kk) != 0);
+                            umma_f16(t_acc, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff),
+                                     idesc, 1u);
                         }
                     }
-                    if (Tr::kProducts == 3) {
-                        umma_f16(tmem + kHL, umma_desc_sw128(a_hi + koff),
-                                 umma_desc_sw128(b_lo + koff), idesc, (kb | kk) != 0);
-                        umma_f16(tmem + kHL, umma_desc_sw128(a_lo + koff),
-                                 umma_desc_sw128(b_hi + koff), idesc, 1u);
-                    }
+                    umma_commit(&empty[s]);
                 }
-                umma_commit(&empty[s]);  // frees the smem stage once these MMAs retire
+                umma_commit(&acc_full[ab]);
             }
-            umma_commit(hl_full);
         }
         __syncwarp();
-    } else {
-        // ------------------------------------------------ accumulator drain
+    } else if (warp < 4 + kEpiWarps) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsDrain) : "memory");
+        // ================================================= hi*hi drain -> Y
         const int q = warp & 3;
-        const int hc = (warp - 2) >> 2;  // column half owned during the drain
-        const int r = q * 32 + lane;     // tile row of this thread
-        const int gi = I * kBM + r;
-        const int np = p.np, n = p.n;
+        const int hc = (warp - 4) >> 2;
         const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
         const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
-
-        float yacc[kEpiCols];
+        int g = 0, u = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++u) {
+            const int ab = u & 1;
+            float yacc[kEpiCols];
 #pragma unroll
-        for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
-        static_assert(kEpiCols == 64, "drain loads two 32-column chunks");
+            for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
+            if (kDrain && !(p.dbg & 2)) {
+                const int fills = nk * (kBK / kUK) / drain_dr;
 #pragma unroll 1
-        for (int g = 0; g < ((p.dbg & 2) || !kDrain ? 0 : nk * (kBK / kUK) / DR); ++g) {
-            const int hb = g % NHB;
-            mbar_wait(&hh_full[hb], (g / NHB) & 1);
+                for (int f = 0; f < fills; ++f, ++g) {
+                    const int hb = g % NHB;
+                    mbar_wait(&hh_full[hb], (g / NHB) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int ch = 0; ch < 2; ++ch) {
+                        uint32_t v[32];
+                        tmem_ld_32x32b_x32(tlane + hb * 128 + hc * kEpiCols + ch * 32, v);
+                        tmem_ld_wait();
+                        if (ch == 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&hh_empty[hb]);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 32; e += 2) {
+                            const float2 acc = add_f32x2(
+                                make_float2(yacc[32 * ch + e], yacc[32 * ch + e + 1]),
+                                make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+                            yacc[32 * ch + e] = acc.x;
+                            yacc[32 * ch + e + 1] = acc.y;
+                        }
+                    }
+                }
+            }
+            mbar_wait(&acc_full[ab], (u >> 1) & 1);
             tc_fence_after();
-            uint32_t v0[32], v1[32];
-            tmem_ld_32x32b_x32(tlane + hb * 128 + hc * kEpiCols, v0);
-            tmem_ld_32x32b_x32(tlane + hb * 128 + hc * kEpiCols + 32, v1);
-            tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-                float2 acc = make_float2(yacc[e], yacc[e + 1]);
-                acc = add_f32x2(acc, make_float2(__uint_as_float(v0[e]), __uint_as_float(v0[e + 1])));
-                yacc[e] = acc.x;
-                yacc[e + 1] = acc.y;
-                acc = make_float2(yacc[32 + e], yacc[32 + e + 1]);
-                acc = add_f32x2(acc, make_float2(__uint_as_float(v1[e]), __uint_as_float(v1[e + 1])));
-                yacc[32 + e] = acc.x;
-                yacc[32 + e + 1] = acc.y;
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&hh_empty[hb]);
-        }
-        // Y = (hi*hi + cross terms) / scale^2, written over the cross-term columns
-        mbar_wait(hl_full, 0);
-        tc_fence_after();
-#pragma unroll
-        for (int ch = 0; ch < kEpiCols / 32; ++ch) {
-            const uint32_t ta = tlane + kHL + hc * kEpiCols + ch * 32;
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(ta, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) {
-                const float y = kDrain ? yacc[ch * 32 + e] + __uint_as_float(v[e]) : __uint_as_float(v[e]);
-                v[e] = __float_as_uint(y * inv_s2);
-            }
-            if (p.dbg & 2) {  // measurement only: no drain -> Y is the cross-term accumulator
+            for (int ch = 0; ch < kEpiCols / 32; ++ch) {
+                const uint32_t ta = tlane + kAcc0 + ab * 128 + hc * kEpiCols + ch * 32;
+                uint32_t v[32];
                 tmem_ld_32x32b_x32(ta, v);
                 tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const float y = kDrain ? yacc[ch * 32 + e] + __uint_as_float(v[e]) : __uint_as_float(v[e]);
+                    v[e] = __float_as_uint(y * inv_s2);
+                }
+                tmem_st_32x32b_x32(ta, v);
             }
-            tmem_st_32x32b_x32(ta, v);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&y_full[ab]);
         }
-        tmem_st_wait();
-        tc_fence_before();
-        named_bar_sync(2, kEpiWarps * 32);  // all of Y is in TMEM
-        tc_fence_after();
-
-        double tr = 0.0, sq = 0.0;
-        bool bad_nf = false, bad_hr = false;
-        const size_t mat = (size_t)m * np * np;
-        if (p.dbg & 1) {
-            // measurement only: no epilogue memory traffic
-        } else if (!p.last) {
-            // ============================== TMA epilogue (layers 0..L-2)
-            const int sub = hc;  // 32-column block of the current half handled by this warp
-            mbar_wait(xa_full, 0);
-            for (int h = 0; h < 2; ++h) {
-                const int cl0 = h * 64 + sub * 32;  // first tile column of this warp's block
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tlane + kHL + cl0, v);
-                uint8_t* bx = sX + (h * 2 + sub) * 16384;
-                uint8_t* ba = sA + (h * 2 + sub) * 16384;
-                tmem_ld_wait();
-                uint16_t hb[32], lb[32];
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsEpi) : "memory");
+        // ================================================= epilogue (8 warps)
+        const int q = warp & 3;            // TMEM lane quarter = 32-row block of the tile
+        const int s = (warp - 12) >> 2;    // handles column quarters s and s + 2
+        const int ew = warp - 12;          // epilogue warp index 0..7
+        const int r = q * 32 + lane;       // tile row of this thread
+        const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
+        const int np = p.np, n = p.n;
+        uint8_t* stg = smem + kStagingOff + ew * 4 * kPieceBytes;  // hi, lo, hiT, loT pieces
+        int u = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++u) {
+            const int ab = u & 1;
+            const int m = tile / p.T;
+            const int t = tile - m * p.T;
+            int I, J;
+            decode_upper_tile(t, p.nb, I, J);
+            const bool diag = I == J;
+            const int gi = I * kBM + r;
+            const uint32_t tacc = tlane + kAcc0 + ab * 128;
+            float* Xt = p.X + xa_tile_base(m, I, J, p.nb);
+            float* At = p.A + xa_tile_base(m, I, J, p.nb);
+            bool bad_nf = false, bad_hr = false;
+            double tr = 0.0, sq = 0.0;
+            mbar_wait(&y_full[ab], (u >> 1) & 1);
+            tc_fence_after();
+            for (int qi = 0; qi < 2; ++qi) {
+                const int qc = s + 2 * qi;  // column quarter (32 columns)
+                if (diag && qc < q) continue;  // lower block of a diagonal tile: mirrored elsewhere
+                if (p.dbg & 1) continue;
+                if (!p.last && lane == 0) tma_store_wait_read();  // staging pieces free again
+                __syncwarp();
 #pragma unroll
-                for (int c4 = 0; c4 < 8; ++c4) {
-                    float4* px = reinterpret_cast<float4*>(bx + sw128(r, c4));
-                    float4* pa = reinterpret_cast<float4*>(ba + sw128(r, c4));
-                    float4 xv = *px, av = *pa;
-                    float xs[4] = {xv.x, xv.y, xv.z, xv.w};
-                    float as[4] = {av.x, av.y, av.z, av.w};
+                for (int sub = 0; sub < 2; ++sub) {
+                    const int c0 = 32 * qc + 16 * sub;  // first tile column of this pass
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tacc + c0, v);
+                    float4 xq[4], aq[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int cl = cl0 + c4 * 4 + e;
-                        const int gj = J * kBN + cl;
-                        const float y = __uint_as_float(v[c4 * 4 + e]);
-                        double xd = p.a * (double)y + p.b * (double)xs[e];
-                        if (gi == gj && gi < n) xd += p.c;
-                        const float xn = (float)xd;
-                        const bool own = !diag || cl >= r;
-                        bad_nf |= own && !isfinite(xn);
-                        bad_hr |= own && half_range_bad<MODE>(xn);
-                        as[e] = (float)((double)as[e] + p.d_next * (double)xn);
-                        xs[e] = xn;
-                        split16<MODE>(xn, hb[c4 * 4 + e], lb[c4 * 4 + e]);
+                    for (int k = 0; k < 4; ++k) {
+                        xq[k] = *reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + k));
+                        aq[k] = *reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + k));
                     }
-                    *px = make_float4(xs[0], xs[1], xs[2], xs[3]);
-                    *pa = make_float4(as[0], as[1], as[2], as[3]);
+                    tmem_ld_wait();
+                    uint16_t hb[16], lb[16];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        float xs[4] = {xq[k].x, xq[k].y, xq[k].z, xq[k].w};
+                        float as[4] = {aq[k].x, aq[k].y, aq[k].z, aq[k].w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int cl = c0 + 4 * k + e;
+                            const int gj = J * kBN + cl;
+                            double xd = p.a * (double)__uint_as_float(v[4 * k + e]) + p.b * (double)xs[e];
+                            if (gi == gj && gi < n) xd += p.c;
+                            const float xn = (float)xd;
+                            const bool own = !diag || cl >= r;
+                            bad_nf |= own && !isfinite(xn);
+                            if (!p.last) {
+                                bad_hr |= own && half_range_bad<MODE>(xn);
+                                as[e] = (float)((double)as[e] + p.d_next * (double)xn);
+                                xs[e] = xn;
+                                split16<MODE>(xn, hb[4 * k + e], lb[4 * k + e]);
+                            } else if (own && gi < n && gj < n) {
+                                const double dv = (double)as[e] + (double)xn;
+                                if (p.D) {
+                                    double* Dm = p.D + (size_t)m * n * n;
+                                    Dm[(size_t)gi * n + gj] = dv;
+                                    if (gi != gj) Dm[(size_t)gj * n + gi] = dv;
+                                }
+                                if (gi != gj) {
+                                    sq += 2.0 * dv * dv;
+                                } else {
+                                    tr += dv;
+                                    sq += dv * dv;
+                                }
+                            }
+                        }
+                        if (!p.last) {
+                            *reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + k)) = make_float4(xs[0], xs[1], xs[2], xs[3]);
+                            *reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + k)) = make_float4(as[0], as[1], as[2], as[3]);
+                        }
+                    }
+                    if (!p.last) {
+                        // direct piece: row lane, columns 16*sub .. +15 of the 32x32 block
+                        uint4 hv0, hv1, lv0, lv1;
+                        hv0.x = hb[0] | ((uint32_t)hb[1] << 16);   hv0.y = hb[2] | ((uint32_t)hb[3] << 16);
+                        hv0.z = hb[4] | ((uint32_t)hb[5] << 16);   hv0.w = hb[6] | ((uint32_t)hb[7] << 16);
+                        hv1.x = hb[8] | ((uint32_t)hb[9] << 16);   hv1.y = hb[10] | ((uint32_t)hb[11] << 16);
+                        hv1.z = hb[12] | ((uint32_t)hb[13] << 16); hv1.w = hb[14] | ((uint32_t)hb[15] << 16);
+                        lv0.x = lb[0] | ((uint32_t)lb[1] << 16);   lv0.y = lb[2] | ((uint32_t)lb[3] << 16);
+                        lv0.z = lb[4] | ((uint32_t)lb[5] << 16);   lv0.w = lb[6] | ((uint32_t)lb[7] << 16);
+                        lv1.x = lb[8] | ((uint32_t)lb[9] << 16);   lv1.y = lb[10] | ((uint32_t)lb[11] << 16);
+                        lv1.z = lb[12] | ((uint32_t)lb[13] << 16); lv1.w = lb[14] | ((uint32_t)lb[15] << 16);
+                        const bool dblk = diag && qc == q;  // 32x32 block on the tile diagonal
+                        if (!dblk) {
+                            *reinterpret_cast<uint4*>(stg + sw64(lane, 2 * sub + 0)) = hv0;
+                            *reinterpret_cast<uint4*>(stg + sw64(lane, 2 * sub + 1)) = hv1;
+                            if (Tr::kHasLo) {
+                                *reinterpret_cast<uint4*>(stg + kPieceBytes + sw64(lane, 2 * sub + 0)) = lv0;
+                                *reinterpret_cast<uint4*>(stg + kPieceBytes + sw64(lane, 2 * sub + 1)) = lv1;
+                            }
+                        }
+                        // mirrored piece (or, on the diagonal block, the symmetric completion):
+                        // element (lane, 16*sub + e) -> row 16*sub + e, column lane
+                        uint8_t* mh = dblk ? stg : stg + 2 * kPieceBytes;
+                        uint8_t* ml = dblk ? stg + kPieceBytes : stg + 3 * kPieceBytes;
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const uint32_t col = 16 * sub + e;
+                            const uint32_t off = sw64(col, lane >> 3) + (lane & 7) * 2;
+                            if (!dblk || (int)col >= lane) {
+                                *reinterpret_cast<uint16_t*>(mh + off) = hb[e];
+                                if (Tr::kHasLo) *reinterpret_cast<uint16_t*>(ml + off) = lb[e];
+                            }
+                            if (dblk && (int)col >= lane) {
+                                const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
+                                *reinterpret_cast<uint16_t*>(stg + doff) = hb[e];
+                                if (Tr::kHasLo) *reinterpret_cast<uint16_t*>(stg + kPieceBytes + doff) = lb[e];
+                            }
+                        }
+                    }
                 }
-                if (!diag) {
-                    // direct tile (rows I, 64 columns of half h): row r, 16-B chunks 4*sub..
-#pragma unroll
-                    for (int c8 = 0; c8 < 4; ++c8) {
-                        uint4 hv, lv;
-                        hv.x = hb[c8 * 8 + 0] | ((uint32_t)hb[c8 * 8 + 1] << 16);
-                        hv.y = hb[c8 * 8 + 2] | ((uint32_t)hb[c8 * 8 + 3] << 16);
-                        hv.z = hb[c8 * 8 + 4] | ((uint32_t)hb[c8 * 8 + 5] << 16);
-                        hv.w = hb[c8 * 8 + 6] | ((uint32_t)hb[c8 * 8 + 7] << 16);
-                        *reinterpret_cast<uint4*>(sHi + sw128(r, sub * 4 + c8)) = hv;
-                        if (Tr::kHasLo) {
-                            lv.x = lb[c8 * 8 + 0] | ((uint32_t)lb[c8 * 8 + 1] << 16);
-                            lv.y = lb[c8 * 8 + 2] | ((uint32_t)lb[c8 * 8 + 3] << 16);
-                            lv.z = lb[c8 * 8 + 4] | ((uint32_t)lb[c8 * 8 + 5] << 16);
-                            lv.w = lb[c8 * 8 + 6] | ((uint32_t)lb[c8 * 8 + 7] << 16);
-                            *reinterpret_cast<uint4*>(sLo + sw128(r, sub * 4 + c8)) = lv;
+                if (!p.last) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int prow = m * np + I * kBM + 32 * q;   // direct piece origin
+                        const int pcol = J * kBN + 32 * qc;
+                        tma_store_2d(&tm.hip, stg, pcol, prow);
+                        if (Tr::kHasLo) tma_store_2d(&tm.lop, stg + kPieceBytes, pcol, prow);
+                        if (!(diag && qc == q)) {
+                            const int mrow = m * np + J * kBN + 32 * qc;
+                            const int mcol = I * kBM + 32 * q;
+                            tma_store_2d(&tm.hip, stg + 2 * kPieceBytes, mcol, mrow);
+                            if (Tr::kHasLo) tma_store_2d(&tm.lop, stg + 3 * kPieceBytes, mcol, mrow);
                         }
-                    }
-                    // mirrored tile (rows = 64 columns of half h, cols = 128 rows of I):
-                    // element (r, cl) -> row cl - 64h, col r; box r/64 of 64x64
-                    uint8_t* mh = sHiT + (r >> 6) * 8192;
-                    uint8_t* ml = sLoT + (r >> 6) * 8192;
-                    const uint32_t cb = (uint32_t)(r & 63);
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const uint32_t mr = sub * 32 + e;
-                        const uint32_t off = sw128(mr, cb >> 3) + (cb & 7) * 2;
-                        *reinterpret_cast<uint16_t*>(mh + off) = hb[e];
-                        if (Tr::kHasLo) *reinterpret_cast<uint16_t*>(ml + off) = lb[e];
-                    }
-                } else {
-                    // diagonal tile: symmetric 128x128 assembled from the upper triangle,
-                    // 2 boxes of 128 rows x 64 cols
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const uint32_t cl = cl0 + e;
-                        if ((int)cl >= r) {
-                            uint32_t off = (cl >> 6) * 16384 + sw128(r, (cl & 63) >> 3) + (cl & 7) * 2;
-                            *reinterpret_cast<uint16_t*>(sHiD + off) = hb[e];
-                            if (Tr::kHasLo) *reinterpret_cast<uint16_t*>(sLoD + off) = lb[e];
-                            off = (r >> 6) * 16384 + sw128(cl, (r & 63) >> 3) + (r & 7) * 2;
-                            *reinterpret_cast<uint16_t*>(sHiD + off) = hb[e];
-                            if (Tr::kHasLo) *reinterpret_cast<uint16_t*>(sLoD + off) = lb[e];
-                        }
-                    }
-                }
-                fence_proxy_async_smem();
-                named_bar_sync(2, kEpiWarps * 32);
-                if (warp == 2 && lane == 0) {
-                    for (int b = 0; b < 2; ++b) {
-                        tma_store_2d(&tm.x, sX + (h * 2 + b) * 16384, J * kBN + h * 64 + 32 * b, rowI);
-                        tma_store_2d(&tm.a, sA + (h * 2 + b) * 16384, J * kBN + h * 64 + 32 * b, rowI);
-                    }
-                    if (!diag) {
-                        tma_store_2d(&tm.hid, sHi, J * kBN + h * 64, rowI);
-                        if (Tr::kHasLo) tma_store_2d(&tm.lod, sLo, J * kBN + h * 64, rowI);
-                        for (int b = 0; b < 2; ++b) {
-                            tma_store_2d(&tm.him, sHiT + b * 8192, I * kBM + 64 * b, rowJ + h * 64);
-                            if (Tr::kHasLo)
-                                tma_store_2d(&tm.lom, sLoT + b * 8192, I * kBM + 64 * b, rowJ + h * 64);
-                        }
-                    } else if (h == 1) {
-                        for (int b = 0; b < 2; ++b) {
-                            tma_store_2d(&tm.hid, sHiD + b * 16384, I * kBM + 64 * b, rowI);
-                            if (Tr::kHasLo) tma_store_2d(&tm.lod, sLoD + b * 16384, I * kBM + 64 * b, rowI);
-                        }
-                    }
-                    tma_store_commit();
-                    tma_store_wait_read();  // staging reusable for the next half
-                }
-                named_bar_sync(2, kEpiWarps * 32);
-            }
-            if (warp == 2 && lane == 0) tma_store_wait_all();
-        } else {
-            // ============================== last layer: D = A + X_L, statistics
-#pragma unroll
-            for (int ch = 0; ch < kEpiCols / 16; ++ch) {
-                uint32_t v[16];
-                tmem_ld_32x32b_x16(tlane + kHL + hc * kEpiCols + ch * 16, v);
-                const int gj0 = J * kBN + hc * kEpiCols + ch * 16;
-                const size_t off = mat + (size_t)gi * np + gj0;
-                float xo[16], ao[16];
-#pragma unroll
-                for (int e = 0; e < 16; e += 4) {
-                    const float4 xv = *reinterpret_cast<const float4*>(p.X + off + e);
-                    const float4 av = *reinterpret_cast<const float4*>(p.A + off + e);
-                    xo[e] = xv.x; xo[e + 1] = xv.y; xo[e + 2] = xv.z; xo[e + 3] = xv.w;
-                    ao[e] = av.x; ao[e + 1] = av.y; ao[e + 2] = av.z; ao[e + 3] = av.w;
-                }
-                tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int gj = gj0 + e;
-                    double xd = p.a * (double)__uint_as_float(v[e]) + p.b * (double)xo[e];
-                    if (gi == gj && gi < n) xd += p.c;
-                    const float xn = (float)xd;
-                    const bool own = !diag || gj >= gi;
-                    bad_nf |= own && !isfinite(xn);
-                    if (own && gi < n && gj < n) {
-                        const double dv = (double)ao[e] + (double)xn;
-                        if (p.D) {
-                            double* Dm = p.D + (size_t)m * n * n;
-                            Dm[(size_t)gi * n + gj] = dv;
-                            if (gi != gj) Dm[(size_t)gj * n + gi] = dv;
-                        }
-                        if (gi != gj) {
-                            sq += 2.0 * dv * dv;
-                        } else {
-                            tr += dv;
-                            sq += dv * dv;
-                        }
+                        tma_store_commit();
                     }
                 }
             }
-        }
-        const bool any_nf = __any_sync(0xffffffffu, bad_nf);
-        const bool any_hr = __any_sync(0xffffffffu, bad_hr);
-        if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], p.layer + 1);
-        if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], p.layer + 1);
-        if (p.last) {
+            // this warp's Y reads for the tile are done: release the TMEM accumulator
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            const bool any_nf = __any_sync(0xffffffffu, bad_nf);
+            const bool any_hr = __any_sync(0xffffffffu, bad_hr);
+            if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], p.layer + 1);
+            if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], p.layer + 1);
+            if (p.last) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                tr += __shfl_xor_sync(0xffffffffu, tr, o);
-                sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            }
-            if (lane == 0) {
-                red[2 * (warp - 2) + 0] = tr;
-                red[2 * (warp - 2) + 1] = sq;
-            }
-            named_bar_sync(1, kEpiWarps * 32);
-            if (warp == 2 && lane == 0) {
-                double T0 = 0.0, T1 = 0.0;
-                for (int w = 0; w < kEpiWarps; ++w) {  // fixed order
-                    T0 += red[2 * w + 0];
-                    T1 += red[2 * w + 1];
+                for (int o = 16; o > 0; o >>= 1) {
+                    tr += __shfl_xor_sync(0xffffffffu, tr, o);
+                    sq += __shfl_xor_sync(0xffffffffu, sq, o);
                 }
-                p.partials[(size_t)m * p.T + t] = make_double2(T0, T1);
+                named_bar_sync(3, kEpiWarps2 * 32);  // previous tile's partial consumed
+                if (lane == 0) {
+                    red[2 * ew + 0] = tr;
+                    red[2 * ew + 1] = sq;
+                }
+                named_bar_sync(3, kEpiWarps2 * 32);
+                if (ew == 0 && lane == 0) {
+                    double T0 = 0.0, T1 = 0.0;
+                    for (int w = 0; w < kEpiWarps2; ++w) {  // fixed order
+                        T0 += red[2 * w + 0];
+                        T1 += red[2 * w + 1];
+                    }
+                    p.partials[(size_t)m * p.T + t] = make_double2(T0, T1);
+                }
             }
         }
+        if (lane == 0) tma_store_wait_all();
     }
     tc_fence_before();
     __syncthreads();

@@ -80,6 +80,10 @@ __device__ __forceinline__ void tma_prefetch_l2_2d(const void* tmap, int32_t c0,
                  "r"(c0), "r"(c1)
                  : "memory");
 }
+// contiguous global range -> L2 (bulk prefetch, no smem)
+__device__ __forceinline__ void tma_prefetch_l2_bulk(const void* gptr, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gptr), "r"(bytes) : "memory");
+}
 // generic-proxy smem writes -> visible to the async (TMA) proxy
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
