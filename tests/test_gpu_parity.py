@@ -259,3 +259,32 @@ def test_validation_errors(model):
     bad = E.Mlsp2Model(model.abcd, model.beta0, 1.5)
     with pytest.raises(E.ValidationError, match="mu0"):
         E.compute_density_matrix(H, 0.0, 0.01, bad)
+
+
+# ----------------------------------------------------------------- C++ drop-in (proj/core types)
+def _write_mm(path, M):
+    # Matrix Market array, symmetric: lower triangle column-major, %.17g
+    # (the format of write_matrix_market, symmetric_matrix.cpp:120-138)
+    n = M.shape[0]
+    with open(path, "w") as f:
+        f.write("%%MatrixMarket matrix array real symmetric\n%d %d\n" % (n, n))
+        for j in range(n):
+            for i in range(j, n):
+                f.write("%.17g\n" % M[i, j])
+
+
+def test_cpp_drop_in_shim(tmp_path, model):
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(O.HERE), "oracle", "_ref", "test_matrix_engine")
+    if not os.path.exists(exe):
+        pytest.skip("C++ shim test not built (needs the reference sources at build time)")
+    H = tight_binding(256, seed=1234)
+    Dref = O.density_matrix_f64(H, 0.0, 0.01, model.abcd, model.beta0, model.mu0)
+    _write_mm(tmp_path / "H.mtx", H)
+    _write_mm(tmp_path / "D.mtx", Dref)
+    coeffs = os.path.join(O.GOLDEN, "coefficients_M1500.json")
+    r = subprocess.run([exe, coeffs, str(tmp_path / "H.mtx"), str(tmp_path / "D.mtx"), "0", "0.01"],
+                       capture_output=True, text=True, timeout=120)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0 and "OK" in r.stdout
