@@ -6,7 +6,7 @@ PKG  := paper_2605_08523_b200
 LIB  := $(PKG)/lib/libfermiforge_b200.so
 SRCS := $(PKG)/csrc/ffg_capi.cu
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fermiforge/ffg.h
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(PKG)/csrc \
+NVFLAGS := $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(PKG)/csrc \
            -Xptxas -v --expt-relaxed-constexpr
 
 all: lib oracle

@@ -148,11 +148,19 @@ int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, cons
 /* Number of kernels ffg_density_matrices_dev launches for one call (for accounting). */
 int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, int32_t mode);
 
-/* Measurement hooks (bench.py): when enabled, every layer-kernel (K2) launch is
+/* Measurement hooks (bench.py): when enabled, every recursion-kernel (K2) launch is
  * bracketed by CUDA events on its stream; ffg_profile_read() synchronises them and
  * returns the summed device time and launch count since the last read. */
 int ffg_profile_layers(int enable);
 int ffg_profile_read(double* total_ms, int64_t* launches);
+/* The same, plus the algorithmic flops (L * c * N^2 (N+1) per matrix) of
+ * the profiled launches. */
+int ffg_profile_read_ex(double* total_ms, int64_t* launches, double* algorithmic_flops);
+/* Introspection of the K2 work decomposition (pure host): the pair table for an nb x nb
+ * grid of 128-blocks, entries A0 | A1 << 10 | S << 20 | dummy << 30 (blocks (A0,S) and
+ * (A1,S) share B panel S).  Writes min(count, capacity) entries; returns count, -1 on a
+ * bad nb. */
+int32_t ffg_pair_table(int32_t nb, uint32_t* out, int32_t capacity);
 
 /* Release cached device workspaces of the calling process. */
 void ffg_release_workspaces(void);

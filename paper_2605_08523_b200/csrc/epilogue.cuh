@@ -1,0 +1,265 @@
+// K2 epilogue arithmetic for one thread's row segment of a 128x128 block:
+//   X' = a Y + b X (+ c on the diagonal),  A' = A + d' X',  binary16 hi/lo split of X'
+// (scalar_models.cpp:243-252 per element: `acc += d*x` for the next layer, then
+// `x = a*x2 + b*x + c`).  The fp64 coefficients enter as hi/lo fp32 pairs and the products /
+// sums use error-free transformations (FMA product errors, TwoSum), so every result is the
+// fp32 rounding of an approximation accurate to ~2^-46 relative -- the same result as
+// evaluating in fp64 and rounding once, up to rare last-bit ties -- without fp64 or
+// conversion instructions.  Padded rows/columns (>= n) hold zeros in X and Y, so they stay
+// zero (the identity term is only added for rows < n).
+#pragma once
+#include "kernels.cuh"
+
+namespace ffg {
+
+struct EpiCoef {
+    float a_hi, a_lo, b_hi, b_lo, c_hi, c_lo, d_hi, d_lo;
+};
+
+__device__ __forceinline__ void split_f64(double v, float& hi, float& lo) {
+    hi = (float)v;
+    lo = (float)(v - (double)hi);
+}
+
+__device__ __forceinline__ EpiCoef load_coef(const double* coef, int l, bool last) {
+    EpiCoef k;
+    split_f64(__ldg(coef + 4 * l + 0), k.a_hi, k.a_lo);
+    split_f64(__ldg(coef + 4 * l + 1), k.b_hi, k.b_lo);
+    split_f64(__ldg(coef + 4 * l + 2), k.c_hi, k.c_lo);
+    split_f64(last ? 0.0 : __ldg(coef + 4 * (l + 1) + 3), k.d_hi, k.d_lo);
+    return k;
+}
+
+#ifndef FFG_EPI_EFT
+#define FFG_EPI_EFT 1  // 1: error-free transformations (~correctly rounded); 0: fused FMAs
+#endif
+
+// a Y + b X (+ c when with_c), nearly correctly rounded
+template <bool WITH_C>
+__device__ __forceinline__ float poly_step(float y, float x, const EpiCoef& k) {
+#if !FFG_EPI_EFT
+    // fp32 FMAs on hi/lo coefficients: no systematic coefficient rounding, <= ~1 ulp
+    float t = fmaf(k.a_lo, y, k.b_lo * x);
+    if constexpr (WITH_C) t += k.c_hi + k.c_lo;
+    return fmaf(k.a_hi, y, fmaf(k.b_hi, x, t));
+#else
+    const float p = k.a_hi * y;
+    const float ep = fmaf(k.a_hi, y, -p);
+    const float q = k.b_hi * x;
+    const float eq = fmaf(k.b_hi, x, -q);
+    float s = p + q;
+    float z = s - p;
+    float t = (p - (s - z)) + (q - z);
+    t += ep + eq;
+    t = fmaf(k.a_lo, y, fmaf(k.b_lo, x, t));
+    if constexpr (WITH_C) {
+        const float s2 = s + k.c_hi;
+        const float z2 = s2 - s;
+        t += ((s - (s2 - z2)) + (k.c_hi - z2)) + k.c_lo;
+        s = s2;
+    }
+    return s + t;
+#endif
+}
+
+// A + d x, nearly correctly rounded
+__device__ __forceinline__ float acc_step(float a, float x, const EpiCoef& k) {
+#if !FFG_EPI_EFT
+    return fmaf(k.d_hi, x, fmaf(k.d_lo, x, a));
+#else
+    const float m = k.d_hi * x;
+    const float em = fmaf(k.d_hi, x, -m);
+    const float s = a + m;
+    const float z = s - a;
+    const float t = ((a - (s - z)) + (m - z)) + fmaf(k.d_lo, x, em);
+    return s + t;
+#endif
+}
+
+// packed binary16 split of two values: hi = rn(x * 2^14), lo = rn(x * 2^14 - hi)
+// (bf16 mode: hi = rn_bf16(x), lo = 0)
+template <int MODE>
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    if constexpr (MODE == kModeBF16) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+        hi = *reinterpret_cast<const uint32_t*>(&h);
+        lo = 0u;
+    } else {
+        const float s0 = x0 * kHalfScale, s1 = x1 * kHalfScale;
+        const __half2 h = __floats2half2_rn(s0, s1);
+        hi = *reinterpret_cast<const uint32_t*>(&h);
+        if constexpr (MODE == kModeF32E) {
+            const float2 f = __half22float2(h);
+            const __half2 r = __floats2half2_rn(s0 - f.x, s1 - f.y);
+            lo = *reinterpret_cast<const uint32_t*>(&r);
+        } else {
+            lo = 0u;
+        }
+    }
+}
+
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint16_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                              uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ void stsm_x4(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r0),
+                 "r"(r1), "r"(r2), "r"(r3)
+                 : "memory");
+}
+// Transpose a 32x32 binary16 piece (64-byte rows, SW64) from `src` into `dst` with the warp:
+// per 8-row strip rs, ldmatrix.trans reads the four 8x8 matrices (rs, cb) transposed and
+// stmatrix writes them as matrices (cb, rs) of dst.
+__device__ __forceinline__ void transpose_piece(uint32_t src, uint32_t dst, int lane) {
+    const uint32_t j = lane >> 3, rr = lane & 7;
+#pragma unroll
+    for (uint32_t rs = 0; rs < 4; ++rs) {
+        uint32_t r0, r1, r2, r3;
+        ldsm_x4_trans(src + sw64(rs * 8 + rr, j), r0, r1, r2, r3);
+        stsm_x4(dst + sw64(j * 8 + rr, rs), r0, r1, r2, r3);
+    }
+}
+
+// Per-thread health of the values it produced: z accumulates x*0 (NaN iff any x is
+// non-finite), mx the largest |x| (binary16 split range: |x| 2^14 < 65504).
+struct EpiHealth {
+    float z = 0.0f, mx = 0.0f;
+    __device__ __forceinline__ void add(float x) {
+        z = fmaf(x, 0.0f, z);
+        mx = fmaxf(mx, fabsf(x));
+    }
+    __device__ __forceinline__ bool nonfinite() const { return z != z; }
+    template <int MODE>
+    __device__ __forceinline__ bool half_range() const {
+        return MODE != kModeBF16 && !(mx * kHalfScale < kHalfMax);
+    }
+};
+
+// One 16-column sub-block (columns c0..c0+15 of the 128x128 block) of this thread's row r,
+// mid-recursion layer: X/A in place, hi/lo into the warp's 32x32 direct staging piece
+// (`stg_d`: hi at +0, lo at +kPieceBytes; row = lane).  The mirrored piece is produced
+// afterwards by the warp (transpose_piece).  DIAG: the block is on the matrix diagonal; only
+// columns >= r are owned (the rest is the mirror of owned values) and the identity term is
+// added at column r.  dblk: the 32x32 piece itself is on the diagonal and is completed
+// symmetrically in place.
+template <int MODE, bool DIAG>
+__device__ __forceinline__ void epi_sub_mid(const uint32_t (&v)[16], float* Xt, float* At, int r,
+                                            int c0, int lane, int sub, bool c_on, const EpiCoef& k,
+                                            uint32_t stg_d, bool dblk, EpiHealth& hl,
+                                            bool nomem = false) {
+    using Tr = ModeTraits<MODE>;
+    float4 xq[4], aq[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (nomem) {  // measurement only
+            xq[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            aq[j] = xq[j];
+            continue;
+        }
+        xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
+        aq[j] = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
+    }
+    uint32_t hp[8], lp[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
+        float as[4] = {aq[j].x, aq[j].y, aq[j].z, aq[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float y = __uint_as_float(v[4 * j + e]);
+            float xn;
+            if constexpr (DIAG) {
+                const int cl = c0 + 4 * j + e;
+                xn = (cl == r && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
+                if (cl >= r) hl.add(xn);
+            } else {
+                xn = poly_step<false>(y, xs[e], k);
+                hl.add(xn);
+            }
+            as[e] = acc_step(as[e], xn, k);
+            xs[e] = xn;
+        }
+        if (!nomem) {
+            __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
+            __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
+        }
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
+    }
+    if (!dblk) {
+        sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
+        sts_v4(stg_d + sw64(lane, 2 * sub + 1), hp[4], hp[5], hp[6], hp[7]);
+        if (Tr::kHasLo) {
+            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 0), lp[0], lp[1], lp[2], lp[3]);
+            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 1), lp[4], lp[5], lp[6], lp[7]);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const uint32_t col = 16 * sub + e;
+            if ((int)col < lane) continue;
+            const uint16_t hb = (uint16_t)(hp[e >> 1] >> (16 * (e & 1)));
+            const uint16_t lb = (uint16_t)(lp[e >> 1] >> (16 * (e & 1)));
+            const uint32_t off = sw64(col, lane >> 3) + (lane & 7) * 2;
+            const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
+            sts_u16(stg_d + off, hb);
+            sts_u16(stg_d + doff, hb);
+            if (Tr::kHasLo) {
+                sts_u16(stg_d + kPieceBytes + off, lb);
+                sts_u16(stg_d + kPieceBytes + doff, lb);
+            }
+        }
+    }
+}
+
+// Last layer: D = A + X_L (fp64, full symmetric storage) and the statistics of the owned
+// elements (Tr D, sum D^2 with off-diagonal elements counted twice); sixteen columns.
+template <bool DIAG>
+__device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const float* Xt, const float* At,
+                                             int r, int c0, int gi, int gj0, int n, bool c_on,
+                                             const EpiCoef& k, double* Dm, EpiHealth& hl, double& tr,
+                                             double& sq) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float4 xq = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
+        const float4 aq = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
+        const float xs[4] = {xq.x, xq.y, xq.z, xq.w};
+        const float as[4] = {aq.x, aq.y, aq.z, aq.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int cl = c0 + 4 * j + e;
+            const int gj = gj0 + cl;
+            const float y = __uint_as_float(v[4 * j + e]);
+            const bool dg = DIAG && cl == r;
+            const float xn = (dg && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
+            const bool own = !DIAG || cl >= r;
+            if (own) hl.add(xn);
+            if (own && gi < n && gj < n) {
+                const double dv = (double)as[e] + (double)xn;
+                if (Dm) {
+                    Dm[(size_t)gi * n + gj] = dv;
+                    if (!dg) Dm[(size_t)gj * n + gi] = dv;
+                }
+                if (dg) {
+                    tr += dv;
+                    sq += dv * dv;
+                } else {
+                    sq += 2.0 * dv * dv;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace ffg

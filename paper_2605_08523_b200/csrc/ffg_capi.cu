@@ -19,7 +19,7 @@
 #include <vector>
 
 #include "fermiforge/ffg.h"
-#include "kernels.cuh"
+#include "k2_pair.cuh"
 
 using namespace ffg;
 
@@ -160,6 +160,22 @@ struct Workspace {
     // (SW128), [4..7] 32x32 epilogue pieces (SW64)
     int tm_B = -1, tm_np = -1;
     CUtensorMap tm[8];
+    // pair kernel (k2_pair.cuh): panel counters, pair table, per-layer coefficients, maps
+    uint32_t* counters = nullptr;
+    size_t cap_cnt = 0;
+    uint32_t* pairs = nullptr;
+    int pairs_nb = -1, PT = 0;
+    size_t cap_pairs = 0;
+    double* coef = nullptr;
+    size_t cap_coef = 0;
+    int pm_B = -1, pm_np = -1;
+    PairMaps pmaps;
+    // pinned upload ring for small per-call host data (params, coefficients)
+    static constexpr int kRing = 8;
+    static constexpr size_t kSlot = 64 * 1024;
+    uint8_t* ring = nullptr;
+    cudaEvent_t ring_ev[kRing] = {};
+    int ring_next = 0;
     std::mutex mu;
 };
 
@@ -192,6 +208,12 @@ void free_ws(Workspace* w) {
     cudaFree(w->bounds_out);
     cudaFree(w->status);
     cudaFreeHost(w->host_small);
+    cudaFree(w->counters);
+    cudaFree(w->pairs);
+    cudaFree(w->coef);
+    cudaFreeHost(w->ring);
+    for (auto& e : w->ring_ev)
+        if (e) cudaEventDestroy(e);
     if (w->ev0) cudaEventDestroy(w->ev0);
     if (w->ev1) cudaEventDestroy(w->ev1);
 }
@@ -255,9 +277,75 @@ int ensure_staging(Workspace& w, size_t elems) {
     return FFG_OK;
 }
 
+// Copy a small host array to the device asynchronously on `st` through a pinned ring slot;
+// the slot is reused only after its previous copy has executed (event), so the caller's
+// array may change right after the call.
+int upload_small(Workspace& w, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes > Workspace::kSlot) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));  // pageable: staged
+        return FFG_OK;
+    }
+    if (!w.ring) {
+        CK(cudaMallocHost(&w.ring, Workspace::kRing * Workspace::kSlot));
+        for (auto& e : w.ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int k = w.ring_next;
+    w.ring_next = (k + 1) % Workspace::kRing;
+    CK(cudaEventSynchronize(w.ring_ev[k]));
+    uint8_t* slot = w.ring + (size_t)k * Workspace::kSlot;
+    memcpy(slot, src, bytes);
+    CK(cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(w.ring_ev[k], st));
+    return FFG_OK;
+}
+
+// Pair table of the K2 pair kernel (k2_pair.cuh): every block {R, C} (R <= C) of an nb x nb
+// block grid exactly once, as pairs of blocks sharing their B panel S.  Column J pairs its
+// upper blocks (I, J) over panel J; an odd leftover (the diagonal) takes block {J, J+1} from
+// column J+1 in the lower orientation (J+1, J); the last column's leftover gets a dummy
+// partner (so at most one dummy per matrix).  Pairs are then ordered row-major by the
+// upper-triangle rows of their blocks so that panels complete early in a layer.
+std::vector<uint32_t> pair_table(int nb) {
+    struct P { int a0, a1, s, d; };
+    std::vector<P> v;
+    int skip = -1;
+    for (int J = 0; J < nb; ++J) {
+        std::vector<int> U;
+        for (int I = 0; I <= J; ++I)
+            if (I != skip) U.push_back(I);
+        skip = -1;
+        if (U.size() % 2) {
+            U.pop_back();  // the diagonal block (J, J)
+            if (J + 1 < nb) {
+                v.push_back({J, J + 1, J, 0});
+                skip = J;
+            } else {
+                v.push_back({J, J, J, 1});
+            }
+        }
+        for (size_t k = 0; k + 1 < U.size(); k += 2) v.push_back({U[k], U[k + 1], J, 0});
+    }
+    auto key = [](const P& t) {
+        int r = std::min(t.a0, t.s), c = std::max(t.a0, t.s);
+        if (!t.d) {
+            r = std::max(r, std::min(t.a1, t.s));
+            c = std::max(c, std::max(t.a1, t.s));
+        }
+        return std::make_pair(r, c);
+    };
+    std::stable_sort(v.begin(), v.end(), [&](const P& x, const P& y) { return key(x) < key(y); });
+    std::vector<uint32_t> out;
+    for (const P& t : v)
+        out.push_back((uint32_t)t.a0 | ((uint32_t)t.a1 << 10) | ((uint32_t)t.s << 20) |
+                      ((uint32_t)t.d << 30));
+    return out;
+}
+
 // --------------------------------------------------------------------- small kernels
-__global__ void reset_kernel(unsigned long long* bounds, int* flags, int B) {
+__global__ void reset_kernel(unsigned long long* bounds, int* flags, int B,
+                             uint32_t* counters = nullptr, int n_counters = 0) {
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < n_counters) counters[m] = 0u;
     if (m < B) {
         bounds[2 * m + 0] = ~0ull;
         bounds[2 * m + 1] = 0ull;
@@ -302,6 +390,24 @@ int debug_flags() {
     return v;
 }
 
+// Host-mapped watchdog record (ptx.cuh watchdog_fire): [0] fired count, [1] block,
+// [2] thread, [3] site tag, [4..5] site data.  Survives a trapped context.
+unsigned long long* g_watch_host = nullptr;
+int install_watchdog() {
+    static int rc = [] {
+        void* h = nullptr;
+        if (cudaHostAlloc(&h, 16 * sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess)
+            return (int)FFG_ERR_CUDA;
+        memset(h, 0, 16 * sizeof(unsigned long long));
+        void* d = nullptr;
+        if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return (int)FFG_ERR_CUDA;
+        if (cudaMemcpyToSymbol(ffg_watch_buf, &d, sizeof(d)) != cudaSuccess) return (int)FFG_ERR_CUDA;
+        g_watch_host = static_cast<unsigned long long*>(h);
+        return (int)FFG_OK;
+    }();
+    return rc;
+}
+
 int num_sms() {
     static int v = [] {
         int dev = 0, n = 148;
@@ -326,15 +432,16 @@ int launch_layer(const LayerMaps& maps, const LayerParams& p, int tiles, cudaStr
     return FFG_OK;
 }
 
-// Optional CUDA-event timing of every K2 (layer) launch, for the roofline figure.
+// Optional CUDA-event timing of every K2 launch, for the roofline figure.
 struct LayerProfile {
     bool on = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
     size_t used = 0;
+    double flops = 0.0;  // algorithmic flops of the profiled launches
     std::mutex mu;
 } g_prof;
 
-int prof_begin(cudaStream_t st, cudaEvent_t* stop) {
+int prof_begin(cudaStream_t st, cudaEvent_t* stop, double flops) {
     *stop = nullptr;
     if (!g_prof.on) return FFG_OK;
     std::lock_guard<std::mutex> lk(g_prof.mu);
@@ -347,6 +454,67 @@ int prof_begin(cudaStream_t st, cudaEvent_t* stop) {
     auto& pr = g_prof.ev[g_prof.used++];
     CK(cudaEventRecord(pr.first, st));
     *stop = pr.second;
+    g_prof.flops += flops;
+    return FFG_OK;
+}
+
+unsigned long long* g_prof_buf = nullptr;  // FFG_DEBUG_K2 & 8: per-CTA role wait cycles
+
+// K2 implementation: 1 = per-layer single-CTA persistent kernel (kernels.cuh, kept for A/B
+// measurement), default = CTA-pair multi-layer kernel (k2_pair.cuh).
+int k2_impl() {
+    static int v = [] {
+        const char* e = getenv("FFG_K2");
+        return e ? atoi(e) : 2;
+    }();
+    return v;
+}
+
+// Matrices per L2-resident group of the pair kernel.  Enough pair items per layer
+// (G * PT >= 2 * resident pairs) that a layer's first items find their panels complete while
+// the rest of the group's layer is still in flight (static round-robin schedule; see the
+// schedule simulation in DESIGN.md), and otherwise as many as fit `FFG_GROUP_MB` (default
+// 80 MiB of the 126 MB L2) of per-matrix working set (X, A blocks + two hi/lo parities).
+int group_size(int B, int64_t np, int PT, int resident_pairs, int mode) {
+    const char* e = getenv("FFG_GROUP");
+    if (e) return std::max(1, std::min(B, atoi(e)));
+    const char* mb = getenv("FFG_GROUP_MB");
+    const double budget = (mb ? atof(mb) : 80.0) * 1048576.0;
+    const double per = (double)np * np * (8.0 * 0.5625 + (mode == kModeF32E ? 8.0 : 4.0));
+    const int fit = (int)(budget / per);
+    const int fill = (2 * resident_pairs + PT - 1) / PT;
+    return std::max(1, std::min(B, std::max(fit, fill)));
+}
+
+// Co-resident CTA pairs of the pair kernel (all pairs must be resident: the layer
+// dependencies are waited for inside the kernel).
+template <int MODE>
+int pair_capacity(int* out) {
+    static int max_pairs = -1;
+    if (max_pairs < 0) {
+        CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                PairCfg<MODE>::kSmem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * (num_sms() / 2));
+        cfg.blockDim = dim3(kPairThreads);
+        cfg.dynamicSmemBytes = PairCfg<MODE>::kSmem;
+        int nc = 0;
+        CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_pair_kernel<MODE>, &cfg));
+        if (nc < 1) return set_err(FFG_ERR_CUDA, "pair kernel: no co-resident CTA pair fits");
+        max_pairs = nc;
+    }
+    *out = max_pairs;
+    return FFG_OK;
+}
+
+template <int MODE>
+int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
+    int cap, rc;
+    if ((rc = pair_capacity<MODE>(&cap))) return rc;
+    if ((rc = install_watchdog())) return set_err(FFG_ERR_CUDA, "watchdog buffer");
+    const int pairs = (int)std::min<int64_t>(cap, items);
+    mlsp2_pair_kernel<MODE><<<2 * pairs, kPairThreads, PairCfg<MODE>::kSmem, st>>>(maps, pp);
+    CK(cudaGetLastError());
     return FFG_OK;
 }
 
@@ -366,17 +534,67 @@ struct Job {
     double* bounds_dev = nullptr;       // [B][4] or null (-> workspace)
 };
 
-// Enqueue the full pipeline for one batch on `st`.  Host-synchronous only for
-// the tiny per-matrix parameter upload (pinned, async).
+int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L) {
+    size_t dummy = 0;
+    int rc;
+    if ((size_t)B * nb > w.cap_cnt) {
+        if ((rc = grow(&w.counters, dummy, (size_t)B * nb))) return rc;
+        w.cap_cnt = (size_t)B * nb;
+    }
+    if (w.pairs_nb != nb) {
+        const std::vector<uint32_t> t = pair_table(nb);
+        if (t.size() > w.cap_pairs) {
+            if ((rc = grow(&w.pairs, dummy, t.size()))) return rc;
+            w.cap_pairs = t.size();
+        }
+        CK(cudaMemcpy(w.pairs, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+        w.pairs_nb = nb;
+        w.PT = (int)t.size();
+    }
+    if ((size_t)4 * L > w.cap_coef) {
+        if ((rc = grow(&w.coef, dummy, (size_t)4 * L))) return rc;
+        w.cap_coef = (size_t)4 * L;
+    }
+    if (w.pm_B != B || w.pm_np != (int)np) {
+        for (int par = 0; par < 2; ++par) {
+            uint16_t* hi = w.op[2 * par + 0];
+            uint16_t* lo = w.op[2 * par + 1];
+            const int64_t rows = (int64_t)B * np;
+            if ((rc = make_map(&w.pmaps.a_hi[par], hi, rows, np, 2, 64, 128))) return rc;
+            if ((rc = make_map(&w.pmaps.a_lo[par], lo, rows, np, 2, 64, 128))) return rc;
+            if ((rc = make_map(&w.pmaps.b_hi[par], hi, rows, np, 2, 64, kPairHalf))) return rc;
+            if ((rc = make_map(&w.pmaps.b_lo[par], lo, rows, np, 2, 64, kPairHalf))) return rc;
+            if ((rc = make_map(&w.pmaps.p_hi[par], hi, rows, np, 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
+                return rc;
+            if ((rc = make_map(&w.pmaps.p_lo[par], lo, rows, np, 2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
+                return rc;
+        }
+        w.pm_B = B;
+        w.pm_np = (int)np;
+    }
+    return FFG_OK;
+}
+
+// Enqueue the full pipeline for one batch on `st` (asynchronous; the small per-call host
+// arrays go through the pinned upload ring).
 int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     const int B = j.B;
     const int64_t n = j.n;
     const int64_t np = (n + kBM - 1) / kBM * kBM;
     const int nb = (int)(np / kBM);
     const int64_t T = (int64_t)nb * (nb + 1) / 2;
+    const ffg_model& md = *j.model;
+    const bool pair = k2_impl() != 1;
     int rc;
-    if ((rc = ensure(w, B, np, T, true))) return rc;
-    if (w.tm_B != B || w.tm_np != (int)np) {
+    if ((rc = ensure(w, B, np, pair ? 0 : T, true))) return rc;
+    if (pair && (rc = ensure_pair(w, B, np, nb, md.n_layers))) return rc;
+    const int64_t Tpart = pair ? 2 * (int64_t)w.PT : T;  // statistics partials per matrix
+    if ((size_t)B * Tpart > w.cap_T) {
+        size_t dummy = 0;
+        if ((rc = grow(&w.partials, dummy, (size_t)B * Tpart))) return rc;
+        w.cap_T = (size_t)B * Tpart;
+    }
+    if (!pair && (w.tm_B != B || w.tm_np != (int)np)) {
         for (int k = 0; k < 4; ++k) {
             if ((rc = make_map(&w.tm[k], w.op[k], (int64_t)B * np, np, 2, 64, 128))) return rc;
             if ((rc = make_map(&w.tm[4 + k], w.op[k], (int64_t)B * np, np, 2, 32, 32,
@@ -387,18 +605,20 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         w.tm_np = (int)np;
     }
     // per-matrix parameters
-    double* ph = w.params_host;
+    std::vector<double> ph((size_t)4 * B);
     for (int m = 0; m < B; ++m) {
         ph[0 * B + m] = j.alpha[m];
         ph[1 * B + m] = j.gamma[m];
         ph[2 * B + m] = j.scale ? j.scale[m] : 0.0;
         ph[3 * B + m] = j.mu ? j.mu[m] : 0.0;
     }
-    CK(cudaMemcpyAsync(w.params, ph, sizeof(double) * 4 * B, cudaMemcpyHostToDevice, st));
-    reset_kernel<<<(B + 127) / 128, 128, 0, st>>>(w.bounds, w.flags, B);
+    if ((rc = upload_small(w, w.params, ph.data(), sizeof(double) * 4 * B, st))) return rc;
+    if (pair && (rc = upload_small(w, w.coef, md.abcd, sizeof(double) * 4 * md.n_layers, st)))
+        return rc;
+    const int ncnt = pair ? B * nb : 0;
+    reset_kernel<<<(std::max(B, ncnt) + 127) / 128, 128, 0, st>>>(w.bounds, w.flags, B, w.counters, ncnt);
     CK(cudaGetLastError());
 
-    const ffg_model& md = *j.model;
     RescaleParams rp{};
     rp.H = j.H_dev;
     rp.alpha = w.params;
@@ -417,45 +637,92 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     rescale_gershgorin_kernel<<<dim3((unsigned)(np / 8), (unsigned)B), 256, 0, st>>>(rp);
     CK(cudaGetLastError());
 
-    for (int l = 0; l < md.n_layers; ++l) {
-        const int par = l & 1;
-        LayerParams lp{};
-        lp.X = w.X;
-        lp.A = w.A;
-        lp.hi_dst = w.op[2 * (par ^ 1) + 0];
-        lp.lo_dst = w.op[2 * (par ^ 1) + 1];
-        lp.D = j.D_dev;
-        lp.partials = w.partials;
-        lp.flags = w.flags;
-        lp.a = md.abcd[4 * l + 0];
-        lp.b = md.abcd[4 * l + 1];
-        lp.c = md.abcd[4 * l + 2];
-        lp.last = (l == md.n_layers - 1);
-        lp.d_next = lp.last ? 0.0 : md.abcd[4 * (l + 1) + 3];
-        lp.n = (int)n;
-        lp.np = (int)np;
-        lp.nb = nb;
-        lp.T = (int)T;
-        lp.layer = l;
-        lp.n_layers = md.n_layers;
-        lp.exact_layers = exact_drain_layers();
-        lp.B = B;
-        lp.dbg = debug_flags();
-        LayerMaps maps;
-        maps.hi = w.tm[2 * par + 0];
-        maps.lo = w.tm[2 * par + 1];
-        maps.hip = w.tm[4 + 2 * (par ^ 1) + 0];
-        maps.lop = w.tm[4 + 2 * (par ^ 1) + 1];
-        const int tiles = (int)(B * T);
-        cudaEvent_t stop;
-        if ((rc = prof_begin(st, &stop))) return rc;
+    const double layer_flops = (double)B * ((j.mode == kModeF32E) ? 3.0 : 1.0) * (double)n * n * (n + 1);
+    if (pair) {
+        PairParams pp{};
+        pp.X = w.X;
+        pp.A = w.A;
+        pp.D = j.D_dev;
+        pp.partials = w.partials;
+        pp.flags = w.flags;
+        pp.counters = w.counters;
+        pp.pairs = w.pairs;
+        pp.coef = w.coef;
+        pp.n = (int)n;
+        pp.np = (int)np;
+        pp.nb = nb;
+        pp.PT = w.PT;
+        pp.B = B;
+        int cap = 0;
         switch (j.mode) {
-            case kModeF32E: rc = launch_layer<kModeF32E>(maps, lp, tiles, st); break;
-            case kModeF16: rc = launch_layer<kModeF16>(maps, lp, tiles, st); break;
-            default: rc = launch_layer<kModeBF16>(maps, lp, tiles, st); break;
+            case kModeF32E: rc = pair_capacity<kModeF32E>(&cap); break;
+            case kModeF16: rc = pair_capacity<kModeF16>(&cap); break;
+            default: rc = pair_capacity<kModeBF16>(&cap); break;
+        }
+        if (rc) return rc;
+        pp.G = group_size(B, np, w.PT, cap, j.mode);
+        pp.l0 = 0;
+        pp.l1 = md.n_layers;
+        pp.n_layers = md.n_layers;
+        pp.exact_layers = exact_drain_layers();
+        pp.dbg = debug_flags();
+        if (pp.dbg & 8) {
+            static unsigned long long* prof = nullptr;
+            if (!prof) CK(cudaMallocManaged(&prof, sizeof(unsigned long long) * 16 * 2 * 512));
+            pp.prof = prof;
+            g_prof_buf = prof;
+        }
+        const int64_t items = (int64_t)md.n_layers * B * w.PT;
+        cudaEvent_t stop;
+        if ((rc = prof_begin(st, &stop, layer_flops * md.n_layers))) return rc;
+        switch (j.mode) {
+            case kModeF32E: rc = launch_pair<kModeF32E>(w.pmaps, pp, items, st); break;
+            case kModeF16: rc = launch_pair<kModeF16>(w.pmaps, pp, items, st); break;
+            default: rc = launch_pair<kModeBF16>(w.pmaps, pp, items, st); break;
         }
         if (rc) return rc;
         if (stop) CK(cudaEventRecord(stop, st));
+    } else {
+        for (int l = 0; l < md.n_layers; ++l) {
+            const int par = l & 1;
+            LayerParams lp{};
+            lp.X = w.X;
+            lp.A = w.A;
+            lp.hi_dst = w.op[2 * (par ^ 1) + 0];
+            lp.lo_dst = w.op[2 * (par ^ 1) + 1];
+            lp.D = j.D_dev;
+            lp.partials = w.partials;
+            lp.flags = w.flags;
+            lp.a = md.abcd[4 * l + 0];
+            lp.b = md.abcd[4 * l + 1];
+            lp.c = md.abcd[4 * l + 2];
+            lp.last = (l == md.n_layers - 1);
+            lp.d_next = lp.last ? 0.0 : md.abcd[4 * (l + 1) + 3];
+            lp.n = (int)n;
+            lp.np = (int)np;
+            lp.nb = nb;
+            lp.T = (int)T;
+            lp.layer = l;
+            lp.n_layers = md.n_layers;
+            lp.exact_layers = exact_drain_layers();
+            lp.B = B;
+            lp.dbg = debug_flags();
+            LayerMaps maps;
+            maps.hi = w.tm[2 * par + 0];
+            maps.lo = w.tm[2 * par + 1];
+            maps.hip = w.tm[4 + 2 * (par ^ 1) + 0];
+            maps.lop = w.tm[4 + 2 * (par ^ 1) + 1];
+            const int tiles = (int)(B * T);
+            cudaEvent_t stop;
+            if ((rc = prof_begin(st, &stop, layer_flops))) return rc;
+            switch (j.mode) {
+                case kModeF32E: rc = launch_layer<kModeF32E>(maps, lp, tiles, st); break;
+                case kModeF16: rc = launch_layer<kModeF16>(maps, lp, tiles, st); break;
+                default: rc = launch_layer<kModeBF16>(maps, lp, tiles, st); break;
+            }
+            if (rc) return rc;
+            if (stop) CK(cudaEventRecord(stop, st));
+        }
     }
     FinalizeParams fp{};
     fp.partials = w.partials;
@@ -464,7 +731,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     fp.scale = j.scale ? w.params + 2 * B : nullptr;
     fp.mu = w.params + 3 * B;
     fp.mu0 = md.mu0;
-    fp.T = (int)T;
+    fp.T = (int)Tpart;
     fp.B = B;
     fp.stats = j.stats_dev ? j.stats_dev : w.stats;
     fp.bounds_out = j.bounds_dev ? j.bounds_dev : w.bounds_out;
@@ -795,17 +1062,19 @@ int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, in
     (void)n;
     (void)mode;
     if (!model) return 0;
-    return 3 + (int64_t)model->n_layers;  // reset + K1 + L x K2 + K3
+    if (k2_impl() != 1) return 4;            // reset + K1 + K2 (all layers) + K3
+    return 3 + (int64_t)model->n_layers;    // reset + K1 + L x K2 + K3
 }
 
 int ffg_profile_layers(int enable) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.on = enable != 0;
     g_prof.used = 0;
+    g_prof.flops = 0.0;
     return FFG_OK;
 }
 
-int ffg_profile_read(double* total_ms, int64_t* launches) {
+int ffg_profile_read_ex(double* total_ms, int64_t* launches, double* algorithmic_flops) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     double t = 0.0;
     for (size_t i = 0; i < g_prof.used; ++i) {
@@ -816,8 +1085,37 @@ int ffg_profile_read(double* total_ms, int64_t* launches) {
     }
     if (total_ms) *total_ms = t;
     if (launches) *launches = (int64_t)g_prof.used;
+    if (algorithmic_flops) *algorithmic_flops = g_prof.flops;
     g_prof.used = 0;
+    g_prof.flops = 0.0;
     return FFG_OK;
+}
+
+int ffg_profile_read(double* total_ms, int64_t* launches) {
+    return ffg_profile_read_ex(total_ms, launches, nullptr);
+}
+
+// Measurement only (FFG_DEBUG_K2 & 8): per-CTA role wait cycles of the last pair launch.
+int ffg_debug_role_cycles(uint64_t* out, int32_t ctas) {
+    if (!g_prof_buf) return set_err(FFG_ERR_VALIDATION, "no profile (set FFG_DEBUG_K2 & 8)");
+    CK(cudaDeviceSynchronize());
+    memcpy(out, g_prof_buf, sizeof(uint64_t) * 16 * ctas);
+    return FFG_OK;
+}
+
+// Measurement/debug: the watchdog record (see install_watchdog); returns fired count.
+int64_t ffg_debug_watchdog(uint64_t* out6) {
+    if (!g_watch_host) return 0;
+    for (int i = 0; i < 6; ++i) out6[i] = g_watch_host[i];
+    return (int64_t)g_watch_host[0];
+}
+
+int32_t ffg_pair_table(int32_t nb, uint32_t* out, int32_t capacity) {
+    if (nb < 1 || nb > 1023) return -1;
+    const std::vector<uint32_t> t = pair_table(nb);
+    if (out)
+        for (int32_t i = 0; i < (int32_t)t.size() && i < capacity; ++i) out[i] = t[i];
+    return (int32_t)t.size();
 }
 
 void ffg_release_workspaces(void) {

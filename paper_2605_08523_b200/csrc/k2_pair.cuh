@@ -1,0 +1,556 @@
+// K2 (pair form): the MLSP2 recursion layers on CTA pairs (tcgen05 cta_group::2).
+//
+// One launch runs layers [l0, l1) of a whole batch.  The unit of work is a PAIR ITEM: two
+// 128x128 blocks of Y = X^2 that share their B panel S, computed by one M=256 x N=128 MMA
+// over a CTA pair -- CTA rank c computes block (A_c, S) = panel A_c . panel S^T (X is
+// symmetric, so every block is a product of two ROW panels and both UMMA operands are
+// K-major row panels of the binary16 hi/lo split; no transpose pass).  The pair table
+// (host: pair_table()) covers every block {R, C} of the upper triangle exactly once, in the
+// orientation (A_c, S) chosen there; at most one dummy block per matrix.
+//
+// Items are ordered  group -> layer -> matrix in group -> pair  and dealt round-robin to the
+// persistent CTA pairs.  A group of G matrices runs all its layers before the next group
+// starts, so the group's working set (X, A, two hi/lo parities) stays resident in L2.  A
+// layer-(l+1) item waits (producer thread, ld.acquire.gpu) until panels A_c and S of its
+// matrix are complete at layer l: every block {P, *} increments counter[m][P] once per layer
+// after its hi/lo stores have landed (cp.async.bulk.wait_group 0 + release).  Panel counts
+// also order the WAR hazard on the hi/lo parity a layer overwrites: every reader of panels
+// A_c and S at layer l-1 is one of the blocks those counters wait for.
+//
+// Per CTA (640 threads, warp-specialised, setmaxnreg 32/104/120):
+//   warp 0        TMA producer: A_hi, A_lo (128 x 64) of panel A_c and this CTA's half
+//                 (64 x 64) of B_hi, B_lo of panel S; complete_tx on the LEADER's full barrier
+//   warp 1        TMEM allocator (both CTAs) / UMMA issuer (leader only)
+//   warps 4-11    drain the hi*hi TMEM ring (round-to-nearest register sums) -> Y in TMEM
+//   warps 12-19   epilogue (unchanged arithmetic, kernels.cuh): X' = aY + bX + cI,
+//                 A += d'X', binary16 split, direct + mirrored 32x32 pieces by TMA store;
+//                 last layer: D = A + X_L and the per-block statistics.
+// Accumulation precision: hi*hi is drained after every MMA for the first
+// `exact_layers` layers and after every K-block afterwards; hi*lo + lo*hi accumulate apart.
+#pragma once
+#include "epilogue.cuh"
+
+namespace ffg {
+
+constexpr int kPairThreads = 640;
+// setmaxnreg budgets per warpgroup (control / drain / epilogue); they only redistribute the
+// launch allocation of 640 x 96 registers
+constexpr int kPRegsCtl = 48, kPRegsDrain = 96, kPRegsEpi = 120;
+static_assert(128 * kPRegsCtl + 256 * kPRegsDrain + 256 * kPRegsEpi <= 640 * 96, "setmaxnreg budget");
+constexpr int kPairHalf = kBN / 2;                  // B rows supplied by each CTA
+constexpr int kPairOpA = kBM * kBK * 2;             // 16 KB
+constexpr int kPairOpB = kPairHalf * kBK * 2;       // 8 KB
+constexpr int kPairStagingBytes = kEpiWarps2 * 4 * kPieceBytes;  // 64 KB
+
+template <int MODE>
+struct PairCfg {
+    static constexpr int kStageBytes = ModeTraits<MODE>::kHasLo ? 2 * (kPairOpA + kPairOpB)
+                                                                : (kPairOpA + kPairOpB);
+    static constexpr int kStages = ModeTraits<MODE>::kHasLo ? 3 : 6;
+    static constexpr int kStagingOff = kStages * kStageBytes;
+    static constexpr int kBarOff = kStagingOff + kPairStagingBytes;
+    static constexpr int kSmem = kBarOff + 1024 + 1024;  // barriers/scratch + alignment slack
+};
+static_assert(PairCfg<kModeF32E>::kSmem <= 227 * 1024, "pair kernel smem");
+static_assert(PairCfg<kModeBF16>::kSmem <= 227 * 1024, "pair kernel smem");
+static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue warps alike");
+
+// TMEM: 4 slots x 128 columns.  A CHUNK is accumulated into the next slot of the ring:
+// FP32-emulated: one K16 step (exact-drain layers) or one K-block, issued cross terms first
+// (hi*lo with accumulate=0, lo*hi) and hi*hi last, so hi*hi sees exactly one truncating
+// accumulate per K16 step into a chunk-sized partial (accumulation precision);
+// single-product modes: the whole K extent.  The drain warps sum chunks in registers with
+// round-to-nearest adds and write Y into the item's LAST slot, which the epilogue frees.
+#ifndef FFG_DRAIN_SPIN
+#define FFG_DRAIN_SPIN 0  // drain warps spin on slot_full instead of sleeping in try_wait
+#endif
+#ifndef FFG_EXACT_K16
+#define FFG_EXACT_K16 1  // K16 steps per chunk in exact-drain layers (1 or 2)
+#endif
+__host__ __device__ constexpr int pair_chunks(int mode, int nk, bool exact) {
+    return mode == kModeF32E ? (exact ? nk * (kBK / kUK) / FFG_EXACT_K16 : nk) : 1;
+}
+
+struct PairMaps {
+    CUtensorMap a_hi[2], a_lo[2];     // operand A boxes 64 x 128 (SW128), per hi/lo parity
+    CUtensorMap b_hi[2], b_lo[2];     // operand B half boxes 64 x 64 (SW128)
+    CUtensorMap p_hi[2], p_lo[2];     // epilogue store pieces 32 x 32 (SW64)
+};
+
+struct PairParams {
+    float* X;                 // [B][nb][nb] tile-interleaved blocks (all orientations written by K1)
+    float* A;
+    double* D;                // last layer: [B][n][n] fp64 (full storage) or null
+    double2* partials;        // last layer: [B][2*PT] per block (sum diag, sum sq)
+    int* flags;               // [B][2]
+    uint32_t* counters;       // [B][nb] panel completion counts (zero at launch)
+    const uint32_t* pairs;    // [PT]  A0 | A1 << 10 | S << 20 | dummy << 30
+    const double* coef;       // [n_layers][4] a, b, c, d
+    int n, np, nb, PT;
+    int B, G;                 // matrices, group size
+    int l0, l1, n_layers;     // layers of this launch, model depth
+    int exact_layers;
+    int dbg;                  // measurement only: 1 skip epilogue math, 2 skip loads/MMAs,
+                              // 4 skip dependency waits, 8 per-role wait cycles -> prof,
+                              // 16 skip operand loads, 32 skip hi/lo stores, 64 skip X/A
+                              // global traffic (all measurement only: results are wrong)
+    unsigned long long* prof; // [gridDim][16] (dbg & 8)
+};
+
+__device__ __forceinline__ void pair_decode(const PairParams& p, int item, int& m, int& l, int& pi) {
+    const int L = p.l1 - p.l0;
+    const int per_group = L * p.G * p.PT;
+    const int g = item / per_group;
+    const int base = g * p.G;
+    const int Gg = min(p.G, p.B - base);
+    int r = item - g * per_group;
+    const int per_layer = Gg * p.PT;
+    const int dl = r / per_layer;
+    r -= dl * per_layer;
+    const int mi = r / p.PT;
+    pi = r - mi * p.PT;
+    m = base + mi;
+    l = p.l0 + dl;
+}
+
+// dbg & 8: accumulate the cycles a role spends in a wait into a register counter
+#define FFG_TIMED(acc, stmt)                                     \
+    do {                                                         \
+        if (p.dbg & 8) {                                         \
+            const long long t_ = clock64();                      \
+            stmt;                                                \
+            acc += (unsigned long long)(clock64() - t_);         \
+        } else {                                                 \
+            stmt;                                                \
+        }                                                        \
+    } while (0)
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
+    mlsp2_pair_kernel(const __grid_constant__ PairMaps tm, const __grid_constant__ PairParams p) {
+    using Tr = ModeTraits<MODE>;
+    using Cfg = PairCfg<MODE>;
+    constexpr bool kDrain = Tr::kProducts == 3;
+    constexpr int S = Cfg::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
+    uint64_t* full = bars;                 // [S]  leader: TMA bytes of both CTAs
+    uint64_t* empty = bars + S;            // [S]  both: stage consumed (multicast commit)
+    uint64_t* slot_full = bars + 2 * S;    // [4]  both: chunk accumulated in TMEM slot
+    uint64_t* slot_empty = bars + 2 * S + 4;  // [4] leader: slot read by both CTAs
+    uint64_t* y_full = bars + 2 * S + 8;   // [4]  local: Y formed in this slot (last chunk)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 12);
+    double* red = reinterpret_cast<double*>(bars + 2 * S + 14);  // [8][2]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair_id = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int total = (p.l1 - p.l0) * p.B * p.PT;
+    const int nk = p.np / kBK;
+    const int nb = p.nb;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], (p.dbg & 16) ? 2 : 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&slot_full[i], 1);
+            mbar_init(&slot_empty[i], 2 * kEpiWarps);  // drain warps, or epilogue warps (last chunk)
+        }
+        for (int i = 0; i < 4; ++i) mbar_init(&y_full[i], kEpiWarps);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kPRegsCtl) : "memory");
+        if (warp == 0 && lane == 0) {
+            // ================================================= TMA producer (both CTAs)
+            for (int i = 0; i < 2; ++i) {
+                tma_prefetch_desc(&tm.a_hi[i]);
+                tma_prefetch_desc(&tm.b_hi[i]);
+                if (Tr::kHasLo) {
+                    tma_prefetch_desc(&tm.a_lo[i]);
+                    tma_prefetch_desc(&tm.b_lo[i]);
+                }
+            }
+            const uint32_t bytes = 2u * Cfg::kStageBytes;  // both CTAs land on the leader's barrier
+            int it = 0;
+            unsigned long long w_dep = 0, w_empty = 0;
+            const long long t_start = clock64();
+            for (int item = pair_id; item < total; item += n_pairs) {
+                int m, l, pi;
+                pair_decode(p, item, m, l, pi);
+                const uint32_t pr = __ldg(p.pairs + pi);
+                const int a0 = pr & 1023, a1 = (pr >> 10) & 1023, sp = (pr >> 20) & 1023;
+                const bool dummy = (pr >> 30) & 1;
+                const int ap = rank ? a1 : a0;
+                if (l > p.l0 && !(p.dbg & 4)) {
+                    const uint32_t need = (uint32_t)(nb * (l - p.l0));
+                    const uint32_t* cm = p.counters + (size_t)m * nb;
+                    const long long t0 = clock64();
+                    while (ld_acquire_gpu(cm + ap) < need)
+                        watchdog_check(t0, 3, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + ap),
+                                       ((unsigned long long)need << 32) | ld_acquire_gpu(cm + ap));
+                    while (ld_acquire_gpu(cm + sp) < need)
+                        watchdog_check(t0, 4, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + sp),
+                                       ((unsigned long long)need << 32) | ld_acquire_gpu(cm + sp));
+                    if (p.dbg & 8) w_dep += (unsigned long long)(clock64() - t0);
+                    fence_proxy_async_global();
+                }
+                if (!(p.dbg & 1) && !(dummy && rank)) {
+                    const size_t tb = xa_tile_base(m, ap, sp, nb);
+                    tma_prefetch_l2_bulk(p.X + tb, kBM * kBN * 4);
+                    tma_prefetch_l2_bulk(p.A + tb, kBM * kBN * 4);
+                }
+                const int par = l & 1;
+                const int rowA = m * p.np + ap * kBM;
+                const int rowB = m * p.np + sp * kBN + (int)rank * kPairHalf;
+                for (int kb = 0; kb < ((p.dbg & 2) ? 0 : nk); ++kb, ++it) {
+                    const int s = it % S;
+                    FFG_TIMED(w_empty, mbar_wait(&empty[s], ((it / S) & 1) ^ 1));
+                    const uint32_t fbar = mapa_shared(smem_u32(&full[s]), 0);
+                    if (p.dbg & 16) {  // measurement: no operand traffic (MMAs on stale smem);
+                        mbar_arrive_cluster(fbar);  // both CTAs arrive, keeping them in step
+                        continue;
+                    }
+                    if (leader) mbar_expect_tx(&full[s], bytes);
+                    uint8_t* st = smem + s * Cfg::kStageBytes;
+                    tma_load_2d_pair(st, &tm.a_hi[par], fbar, kb * kBK, rowA);
+                    if (Tr::kHasLo) {
+                        tma_load_2d_pair(st + kPairOpA, &tm.a_lo[par], fbar, kb * kBK, rowA);
+                        tma_load_2d_pair(st + 2 * kPairOpA, &tm.b_hi[par], fbar, kb * kBK, rowB);
+                        tma_load_2d_pair(st + 2 * kPairOpA + kPairOpB, &tm.b_lo[par], fbar, kb * kBK, rowB);
+                    } else {
+                        tma_load_2d_pair(st + kPairOpA, &tm.b_hi[par], fbar, kb * kBK, rowB);
+                    }
+                }
+            }
+            if (p.dbg & 8) {
+                unsigned long long* o = p.prof + (size_t)blockIdx.x * 16;
+                o[0] = (unsigned long long)(clock64() - t_start);
+                o[1] = w_dep;
+                o[2] = w_empty;
+            }
+        } else if (warp == 1 && leader) {
+            // ================================================= UMMA issuer (leader CTA, whole
+            // warp: descriptors are warp-uniform; one elected lane issues each instruction)
+            constexpr uint32_t idesc = umma_idesc_f16(Tr::kFmt, 2 * kBM, kBN);
+            constexpr uint32_t offAlo = kPairOpA;
+            constexpr uint32_t offBhi = Tr::kHasLo ? 2 * kPairOpA : kPairOpA;
+            constexpr uint32_t offBlo = 2 * kPairOpA + kPairOpB;
+            const uint64_t desc0 = umma_desc_sw128(smem_u32(smem));  // stage 0, offset 0
+            int it = 0, g = 0;
+            unsigned long long w_full = 0, w_slot = 0;
+            for (int item = pair_id; item < total; item += n_pairs) {
+                int m, l, pi;
+                pair_decode(p, item, m, l, pi);
+                const bool exact = l < p.exact_layers;
+                uint32_t t_slot = 0;
+                auto open_slot = [&]() {
+                    const int sl = g & 3;
+                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[sl], ((g >> 2) & 1) ^ 1));
+                    tc_fence_after();
+                    t_slot = tmem + sl * 128;
+                };
+                auto close_slot = [&]() {
+                    if (elect_one_sync()) umma_commit_pair(&slot_full[g & 3]);
+                    __syncwarp();
+                    ++g;
+                };
+                // descriptor of (stage base + byte offset): the start address field is addr>>4
+                auto D = [&](uint64_t sbase, uint32_t off) { return sbase + (off >> 4); };
+                if (!kDrain) open_slot();
+                for (int kb = 0; kb < ((p.dbg & 2) ? 0 : nk); ++kb, ++it) {
+                    const int s = it % S;
+                    FFG_TIMED(w_full, mbar_wait(&full[s], (it / S) & 1));
+                    tc_fence_after();
+                    const uint64_t sb = desc0 + (uint64_t)((s * Cfg::kStageBytes) >> 4);
+                    if (!kDrain) {
+#pragma unroll
+                        for (int kk = 0; kk < kBK / kUK; ++kk) {
+                            const uint32_t koff = kk * kUK * 2;
+                            if (elect_one_sync())
+                                umma_f16_pair(t_slot, D(sb, koff), D(sb, offBhi + koff), idesc, (kb | kk) != 0);
+                            __syncwarp();
+                        }
+                    } else if (exact) {
+#pragma unroll
+                        for (int k0 = 0; k0 < kBK / kUK; k0 += FFG_EXACT_K16) {
+                            open_slot();
+                            if (elect_one_sync()) {
+#pragma unroll
+                                for (int kk = k0; kk < k0 + FFG_EXACT_K16; ++kk) {
+                                    const uint32_t koff = kk * kUK * 2;
+                                    umma_f16_pair(t_slot, D(sb, koff), D(sb, offBlo + koff), idesc, kk != k0);
+                                    umma_f16_pair(t_slot, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
+                                }
+#pragma unroll
+                                for (int kk = k0; kk < k0 + FFG_EXACT_K16; ++kk) {
+                                    const uint32_t koff = kk * kUK * 2;
+                                    umma_f16_pair(t_slot, D(sb, koff), D(sb, offBhi + koff), idesc, 1u);
+                                }
+                            }
+                            __syncwarp();
+                            close_slot();
+                        }
+                    } else {
+                        open_slot();
+                        if (elect_one_sync()) {
+#pragma unroll
+                            for (int kk = 0; kk < kBK / kUK; ++kk) {
+                                const uint32_t koff = kk * kUK * 2;
+                                umma_f16_pair(t_slot, D(sb, koff), D(sb, offBlo + koff), idesc, kk != 0);
+                                umma_f16_pair(t_slot, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
+                            }
+#pragma unroll
+                            for (int kk = 0; kk < kBK / kUK; ++kk) {
+                                const uint32_t koff = kk * kUK * 2;
+                                umma_f16_pair(t_slot, D(sb, koff), D(sb, offBhi + koff), idesc, 1u);
+                            }
+                        }
+                        __syncwarp();
+                        close_slot();
+                    }
+                    if (elect_one_sync()) umma_commit_pair(&empty[s]);
+                    __syncwarp();
+                }
+                if (!kDrain || (p.dbg & 2)) {
+                    if (kDrain) open_slot();
+                    close_slot();
+                }
+            }
+            if ((p.dbg & 8) && lane == 0) {
+                unsigned long long* o = p.prof + (size_t)blockIdx.x * 16;
+                o[3] = w_full;
+                o[4] = w_slot;
+            }
+        }
+        __syncwarp();
+    } else if (warp < 4 + kEpiWarps) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsDrain) : "memory");
+        // ===================================================== chunk drain -> Y (both CTAs)
+        const int q = warp & 3;
+        const int hc = (warp - 4) >> 2;
+        const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + hc * kEpiCols;
+        const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
+        const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
+        int g = 0, u = 0;
+        unsigned long long w_sf = 0;
+        for (int item = pair_id; item < total; item += n_pairs, ++u) {
+            int m, l, pi;
+            pair_decode(p, item, m, l, pi);
+            const int chunks = (p.dbg & 2) ? 1 : pair_chunks(MODE, nk, l < p.exact_layers);
+            float yacc[kEpiCols];
+#pragma unroll
+            for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
+#pragma unroll 1
+            for (int f = 0; f < chunks; ++f, ++g) {
+                const int sl = g & 3;
+                #if FFG_DRAIN_SPIN
+                FFG_TIMED(w_sf, mbar_wait(&slot_full[sl], (g >> 2) & 1));
+#else
+                FFG_TIMED(w_sf, mbar_wait_sleep(&slot_full[sl], (g >> 2) & 1));
+#endif
+                tc_fence_after();
+                const bool lastc = f == chunks - 1;
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tlane + sl * 128 + ch * 16, v);
+                    tmem_ld_wait();
+                    if (ch == 3 && !lastc) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 16; e += 2) {
+                        const float2 acc = add_f32x2(
+                            make_float2(yacc[16 * ch + e], yacc[16 * ch + e + 1]),
+                            make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+                        yacc[16 * ch + e] = acc.x;
+                        yacc[16 * ch + e + 1] = acc.y;
+                    }
+                }
+                if (lastc) {  // Y into this slot for the epilogue (which frees the slot)
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t v[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * ch + e] * inv_s2);
+                        tmem_st_32x32b_x16(tlane + sl * 128 + ch * 16, v);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&y_full[sl]);
+                }
+            }
+        }
+        if ((p.dbg & 8) && warp == 4 && lane == 0) p.prof[(size_t)blockIdx.x * 16 + 5] = w_sf;
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsEpi) : "memory");
+        // ===================================================== epilogue (both CTAs)
+        const int q = warp & 3;            // TMEM lane quarter = 32-row slice of the block
+        const int s = (warp - 12) >> 2;    // column quarters s and s + 2
+        const int ew = warp - 12;
+        const int r = q * 32 + lane;       // block row of this thread
+        const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
+        const int np = p.np, n = p.n;
+        uint8_t* stg = smem + Cfg::kStagingOff + ew * 4 * kPieceBytes;
+        const uint32_t stg_a = smem_u32(stg);
+        const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
+        int g = 0;
+        uint32_t yph = 0;  // per-slot phase bits of y_full (a slot holds Y until freed here)
+        unsigned long long w_y = 0, w_pub = 0, w_st = 0;
+        for (int item = pair_id; item < total; item += n_pairs) {
+            int m, l, pi;
+            pair_decode(p, item, m, l, pi);
+            const uint32_t pr = __ldg(p.pairs + pi);
+            const int R = rank ? (pr >> 10) & 1023 : pr & 1023;  // block rows (A panel)
+            const int C = (pr >> 20) & 1023;                     // block cols (B panel)
+            const bool dummy = rank && ((pr >> 30) & 1);
+            const bool last = (l == p.n_layers - 1);
+            const EpiCoef k = load_coef(p.coef, l, last);
+            const int nxt = (l + 1) & 1;   // hi/lo parity written by this layer
+            g += (p.dbg & 2) ? 1 : pair_chunks(MODE, nk, l < p.exact_layers);
+            const int ysl = (g - 1) & 3;   // slot holding this item's Y
+            const bool diag = R == C;
+            const int gi = R * kBM + r;
+            const bool c_on = gi < n;      // identity term only on real rows
+            const uint32_t tacc = tlane + ysl * 128;
+            float* Xt = p.X + xa_tile_base(m, R, C, nb);
+            float* At = p.A + xa_tile_base(m, R, C, nb);
+            EpiHealth hl;
+            double tr = 0.0, sq = 0.0;
+            FFG_TIMED(w_y, mbar_wait_sleep(&y_full[ysl], (yph >> ysl) & 1));
+            yph ^= 1u << ysl;
+            tc_fence_after();
+#pragma unroll 1
+            for (int qi = 0; qi < 2; ++qi) {
+                const int qc = s + 2 * qi;  // column quarter (32 columns)
+                if (dummy || (p.dbg & 1)) continue;
+                if (diag && qc < q) continue;  // lower half of a diagonal block: mirrored
+                if (!last) {
+                    if (lane == 0) FFG_TIMED(w_st, tma_store_wait_read());  // staging free again
+                    __syncwarp();
+                }
+                const bool dblk = diag && qc == q;  // 32x32 piece on the matrix diagonal
+#pragma unroll
+                for (int sub = 0; sub < 2; ++sub) {
+                    const int c0 = 32 * qc + 16 * sub;
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tacc + c0, v);
+                    tmem_ld_wait();
+                    if (!last) {
+                        const bool nomem = p.dbg & 64;
+                        if (diag)
+                            epi_sub_mid<MODE, true>(v, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl, nomem);
+                        else
+                            epi_sub_mid<MODE, false>(v, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl, nomem);
+                    } else {
+                        double* Dm = p.D ? p.D + (size_t)m * n * n : nullptr;
+                        if (diag)
+                            epi_sub_last<true>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                        else
+                            epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                    }
+                }
+                if (!last) {
+                    if (!dblk) {  // mirrored pieces: warp transpose of the direct pieces
+                        __syncwarp();
+                        transpose_piece(stg_a, stg_a + 2 * kPieceBytes, lane);
+                        if (Tr::kHasLo) transpose_piece(stg_a + kPieceBytes, stg_a + 3 * kPieceBytes, lane);
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && !(p.dbg & 32)) {
+                        const int prow = m * np + R * kBM + 32 * q;   // direct piece origin
+                        const int pcol = C * kBN + 32 * qc;
+                        tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
+                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
+                        if (!dblk) {
+                            const int mrow = m * np + C * kBN + 32 * qc;
+                            const int mcol = R * kBM + 32 * q;
+                            tma_store_2d(&tm.p_hi[nxt], stg + 2 * kPieceBytes, mcol, mrow);
+                            if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + 3 * kPieceBytes, mcol, mrow);
+                        }
+                        tma_store_commit();
+                    }
+                }
+            }
+            // this warp's Y reads are done: release the pair's TMEM slot
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * ysl);
+            if (!dummy) {
+                const bool any_nf = __any_sync(0xffffffffu, hl.nonfinite());
+                const bool any_hr = !last && __any_sync(0xffffffffu, hl.template half_range<MODE>());
+                if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], l + 1);
+                if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], l + 1);
+            }
+            if (last) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    tr += __shfl_xor_sync(0xffffffffu, tr, o);
+                    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                }
+                named_bar_sync(3, kEpiWarps2 * 32);  // previous block's partial consumed
+                if (lane == 0) {
+                    red[2 * ew + 0] = tr;
+                    red[2 * ew + 1] = sq;
+                }
+                named_bar_sync(3, kEpiWarps2 * 32);
+                if (ew == 0 && lane == 0) {
+                    double T0 = 0.0, T1 = 0.0;
+                    for (int w = 0; w < kEpiWarps2; ++w) {  // fixed order
+                        T0 += red[2 * w + 0];
+                        T1 += red[2 * w + 1];
+                    }
+                    p.partials[(size_t)m * 2 * p.PT + 2 * pi + rank] = make_double2(T0, T1);
+                }
+            } else if (!dummy && l + 1 < p.l1) {
+                // publish the block: hi/lo stores landed, X/A stores visible -> panel counters
+                const long long tp = clock64();
+                if (lane == 0) {
+                    tma_store_wait_all();
+                    fence_proxy_async_global();
+                }
+                __syncwarp();
+                named_bar_sync(4, kEpiWarps2 * 32);
+                if (p.dbg & 8) w_pub += (unsigned long long)(clock64() - tp);
+                if (ew == 0 && lane == 0) {
+                    __threadfence();
+                    uint32_t* cm = p.counters + (size_t)m * nb;
+                    red_release_gpu_add(cm + R, 1u);
+                    if (C != R) red_release_gpu_add(cm + C, 1u);
+                }
+            }
+        }
+        if (lane == 0) tma_store_wait_all();
+        if ((p.dbg & 8) && warp == 12 && lane == 0) {
+            unsigned long long* o = p.prof + (size_t)blockIdx.x * 16;
+            o[6] = w_y;
+            o[7] = w_pub;
+            o[8] = w_st;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair(tmem, 512);
+    }
+}
+
+}  // namespace ffg

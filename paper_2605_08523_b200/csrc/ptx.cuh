@@ -37,10 +37,55 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Watchdog: a wait that has not completed after ~FFG_WATCHDOG_CYCLES SM cycles traps (the
+// launch fails with an error) instead of hanging the device.  0 disables it.
+#ifndef FFG_WATCHDOG_CYCLES
+#define FFG_WATCHDOG_CYCLES 4000000000ull
+#endif
+// On expiry the waiting thread records who/where in host-mapped memory (readable after the
+// trap has killed the context) before trapping.
+__device__ unsigned long long* ffg_watch_buf = nullptr;  // [16], host-mapped (ffg_capi.cu)
+__device__ __noinline__ void watchdog_fire(unsigned long long tag, unsigned long long a,
+                                           unsigned long long b) {
+    unsigned long long* w = ffg_watch_buf;
+    if (w && atomicAdd(w, 1ull) == 0ull) {
+        w[1] = blockIdx.x;
+        w[2] = threadIdx.x;
+        w[3] = tag;
+        w[4] = a;
+        w[5] = b;
+        __threadfence_system();
+    }
+    __trap();
+}
+__device__ __forceinline__ void watchdog_check(long long t0, unsigned long long tag = 0,
+                                               unsigned long long a = 0, unsigned long long b = 0) {
+    if (FFG_WATCHDOG_CYCLES && (unsigned long long)(clock64() - t0) > FFG_WATCHDOG_CYCLES)
+        watchdog_fire(tag, a, b);
+}
+// try_wait with a suspend-time hint: a waiting warp sleeps (until the phase completes or the
+// hint expires) instead of spinning on issue slots the working warps of its SM need.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    if (mbar_try_wait_sleep(a, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait_sleep(a, parity)) watchdog_check(t0, 1, a, parity);
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    while (!mbar_try_wait(a, parity)) {
-    }
+    if (mbar_try_wait(a, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(a, parity)) watchdog_check(t0, 2, a, parity);
 }
 
 // ------------------------------------------------------------------ TMA
@@ -184,11 +229,107 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
         "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0],"
+        " {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+
+// ------------------------------------------------------------------ clusters / CTA pairs
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem variable in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t cta_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(cta_addr), "r"(rank));
+    return r;
+}
+// arrive on an mbarrier given by its shared::cluster address (possibly the peer CTA's)
+// (default .release.cta semantics: the tcgen05.fence::before_thread_sync issued before it
+// orders the TMEM reads; a .release.cluster arrive would cost a GPU-scope MEMBAR per call)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-CTA tiled load: box lands in this CTA's smem, complete_tx goes to the barrier at
+// `bar_cluster` (the leader CTA's full barrier).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, uint32_t bar_cluster,
+                                                 int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(slot_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+                 : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T over the CTA pair (M = 256: 128 rows of A from each CTA,
+// N/2 rows of B from each CTA; each CTA's TMEM receives its 128 rows x N).  Leader only.
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Arrive (once each) on the mbarrier at this smem offset in both CTAs of the pair when all
+// previously issued tcgen05 ops of this thread complete.
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n .reg .b16 m;\n mov.b16 m, 3;\n"
+        " tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], m;\n}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+// ------------------------------------------------------------------ cross-CTA flags (gpu scope)
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// order generic-proxy global accesses with async-proxy (TMA) global accesses
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// One lane of the (fully active) warp; operands computed warp-uniformly outside the elected
+// region stay in uniform registers (no per-instruction R2UR / ELECT loops).
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, %1;\n @px mov.s32 %0, 1;\n}"
+        : "+r"(pred)
+        : "r"(0xffffffffu));
+    return pred != 0;
 }
 
 // ------------------------------------------------------------------ misc

@@ -110,7 +110,7 @@ SYMBOLS = ("ffg_abi_version", "ffg_last_error", "ffg_device_available", "ffg_in_
            "ffg_spectral_bounds", "ffg_apply_model", "ffg_mixed_square", "ffg_density_statistics",
            "ffg_density_matrix", "ffg_density_matrices", "ffg_density_matrices_dev",
            "ffg_kernel_launches", "ffg_profile_layers", "ffg_profile_read",
-           "ffg_release_workspaces")
+           "ffg_profile_read_ex", "ffg_pair_table", "ffg_release_workspaces")
 
 
 @lru_cache(maxsize=None)
@@ -144,6 +144,9 @@ def lib() -> ctypes.CDLL:
                                       ctypes.c_int32]
     L.ffg_profile_layers.argtypes = [ctypes.c_int]
     L.ffg_profile_read.argtypes = [_D, ctypes.POINTER(ctypes.c_int64)]
+    L.ffg_profile_read_ex.argtypes = [_D, ctypes.POINTER(ctypes.c_int64), _D]
+    L.ffg_pair_table.restype = ctypes.c_int32
+    L.ffg_pair_table.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32]
     L.ffg_release_workspaces.restype = None
     assert L.ffg_abi_version() == 1
     return L
@@ -376,11 +379,29 @@ def profile_layers(enable: bool) -> None:
 
 
 def profile_read() -> tuple[float, int]:
-    """(summed layer-kernel device ms, launches) since the last read."""
+    """(summed K2 device ms, K2 launches) since the last read (CUDA events on the stream)."""
+    t, n, _ = profile_read_ex()
+    return t, n
+
+
+def profile_read_ex() -> tuple[float, int, float]:
+    """(summed K2 device ms, K2 launches, algorithmic flops of those launches)."""
     t = ctypes.c_double()
     n = ctypes.c_int64()
-    _check(lib().ffg_profile_read(ctypes.byref(t), ctypes.byref(n)))
-    return t.value, n.value
+    f = ctypes.c_double()
+    _check(lib().ffg_profile_read_ex(ctypes.byref(t), ctypes.byref(n), ctypes.byref(f)))
+    return t.value, n.value, f.value
+
+
+def pair_table(nb: int) -> np.ndarray:
+    """K2 work decomposition for an nb x nb grid of 128-blocks: rows (A0, A1, S, dummy);
+    the CTA pair computes blocks (A0, S) and (A1, S) sharing B panel S."""
+    cnt = lib().ffg_pair_table(nb, None, 0)
+    if cnt < 0:
+        raise DimensionError(f"bad block count {nb}")
+    buf = np.zeros(cnt, dtype=np.uint32)
+    lib().ffg_pair_table(nb, buf.ctypes.data, cnt)
+    return np.stack([buf & 1023, (buf >> 10) & 1023, (buf >> 20) & 1023, (buf >> 30) & 1], axis=1)
 
 
 def algorithmic_flops(n: int, layers: int, mode: PrecisionMode) -> float:

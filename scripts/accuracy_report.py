@@ -16,9 +16,10 @@ for tag in ("tb16", "tb64", "tb64_m40"):
     f = np.load(f"{O.GOLDEN}/matrix_{tag}.npz")
     cases.append((tag, f["H"], float(f["mu"]), float(f["kT"]), str(f["model"]), f["D_recursion"]))
 mu, kT = batch_params(512)
-for n, seed, m_, k_ in [(256, 1234, 0.0, 0.01), (1024, 1234, 0.0, 0.01)] + [(512, 10000 + k, mu[k], kT[k]) for k in (0, 5, 11, 23)]:
+for n, seed, m_, k_ in [(256, 1234, 0.0, 0.01), (1024, 1234, 0.0, 0.01)] + [(512, 10000 + k, mu[k], kT[k]) for k in (0, 5, 11, 23, 100, 200, 300, 400)]:
     cases.append((f"tb{n}_s{seed}", tight_binding(n, seed=seed), m_, k_, "M1500", None))
 worst = {}
+worst_big = {}
 for tag, H, mu_, kT_, mname, Dref in cases:
     model = E.load_model(mname)
     if Dref is None:
@@ -26,9 +27,13 @@ for tag, H, mu_, kT_, mname, Dref in cases:
     for mode in modes:
         D, st, pv = E.compute_density_matrix(H, mu_, kT_, model, mode)
         e = err(D, Dref)
-        w = worst.setdefault(mode.name, [0, 0, 0])
-        for i in range(3):
-            w[i] = max(w[i], e[i])
+        for dct in ([worst, worst_big] if H.shape[0] >= 256 else [worst]):
+            w = dct.setdefault(mode.name, [0, 0, 0])
+            for i in range(3):
+                w[i] = max(w[i], e[i])
         print(f"{tag:16s} {mode.name:15s} max {e[0]:.2e} fro {e[1]:.2e} tr {e[2]:.2e}", flush=True)
+tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("FFG_"))
 for k, w in worst.items():
-    print(f"WORST {k:15s} max {w[0]:.2e} fro {w[1]:.2e} tr {w[2]:.2e}  drain={os.environ.get('FFG_DRAIN_K16', '1')}")
+    print(f"WORST     {k:15s} max {w[0]:.2e} fro {w[1]:.2e} tr {w[2]:.2e}  [{tag}]")
+for k, w in worst_big.items():
+    print(f"WORST_BIG {k:15s} max {w[0]:.2e} fro {w[1]:.2e} tr {w[2]:.2e}  [{tag}]")

@@ -17,7 +17,7 @@ def declared_symbols():
     import os
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     txt = open(os.path.join(root, HEADER)).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(ffg_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|void|const char\*)\s+(ffg_\w+)\(", txt, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -85,6 +85,24 @@ def test_no_cpu_fallback_without_device():
 
 def test_kernel_launch_accounting():
     m = E.load_model("M1500")
-    assert E.kernel_launches(1, 1024, m) == 3 + 30
+    assert E.kernel_launches(1, 1024, m) == 4  # reset, K1, K2 (all 30 layers), K3
     assert E.algorithmic_flops(4096, 30, E.PrecisionMode.MIXED_EMULATED) == pytest.approx(6.19e12, rel=1e-3)
     assert E.algorithmic_flops(1024, 30, E.PrecisionMode.BF16) == pytest.approx(3.22e10, rel=1e-2)
+
+
+@pytest.mark.parametrize("nb", list(range(1, 41)) + [64, 127, 128])
+def test_pair_table_covers_upper_triangle_once(nb):
+    """K2 decomposition (k2_pair.cuh): every block {R, C} exactly once, each pair shares its
+    B panel, at most one dummy (only when the block count is odd)."""
+    t = E.pair_table(nb)
+    seen = {}
+    for a0, a1, s, d in t.tolist():
+        assert max(a0, a1, s) < nb
+        for a in ([a0] if d else [a0, a1]):
+            key = (min(a, s), max(a, s))
+            seen[key] = seen.get(key, 0) + 1
+        if not d:
+            assert a0 != a1
+    want = {(i, j) for i in range(nb) for j in range(i, nb)}
+    assert set(seen) == want and set(seen.values()) == {1}
+    assert int(t[:, 3].sum()) == (nb * (nb + 1) // 2) % 2

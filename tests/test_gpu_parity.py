@@ -267,7 +267,8 @@ def _write_mm(path, M):
     # (the format of write_matrix_market, symmetric_matrix.cpp:120-138)
     n = M.shape[0]
     with open(path, "w") as f:
-        f.write("%%MatrixMarket matrix array real symmetric\n%d %d\n" % (n, n))
+        f.write("%%MatrixMarket matrix array real symmetric\n")
+        f.write("%d %d\n" % (n, n))
         for j in range(n):
             for i in range(j, n):
                 f.write("%.17g\n" % M[i, j])
