@@ -131,6 +131,18 @@ __device__ __forceinline__ void transpose_piece(uint32_t src, uint32_t dst, int 
     }
 }
 
+// In-place transpose of a 32x32 binary16 piece (64-byte rows, SW64): the warp reads all sixteen
+// 8x8 matrices transposed into registers, then stores matrix (rs, cb)^T at position (cb, rs).
+__device__ __forceinline__ void transpose_piece_inplace(uint32_t buf, int lane) {
+    const uint32_t j = lane >> 3, rr = lane & 7;
+    uint32_t t[4][4];
+#pragma unroll
+    for (uint32_t rs = 0; rs < 4; ++rs) ldsm_x4_trans(buf + sw64(rs * 8 + rr, j), t[rs][0], t[rs][1], t[rs][2], t[rs][3]);
+    __syncwarp();
+#pragma unroll
+    for (uint32_t rs = 0; rs < 4; ++rs) stsm_x4(buf + sw64(j * 8 + rr, rs), t[rs][0], t[rs][1], t[rs][2], t[rs][3]);
+}
+
 // Per-thread health of the values it produced: z accumulates x*0 (NaN iff any x is
 // non-finite), mx the largest |x| (binary16 split range: |x| 2^14 < 65504).
 struct EpiHealth {

@@ -488,18 +488,18 @@ int group_size(int B, int64_t np, int PT, int resident_pairs, int mode) {
 
 // Co-resident CTA pairs of the pair kernel (all pairs must be resident: the layer
 // dependencies are waited for inside the kernel).
-template <int MODE>
+template <int MODE, bool RES>
 int pair_capacity(int* out) {
     static int max_pairs = -1;
     if (max_pairs < 0) {
-        CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PairCfg<MODE>::kSmem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * (num_sms() / 2));
         cfg.blockDim = dim3(kPairThreads);
         cfg.dynamicSmemBytes = PairCfg<MODE>::kSmem;
         int nc = 0;
-        CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_pair_kernel<MODE>, &cfg));
+        CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_pair_kernel<MODE, RES>, &cfg));
         if (nc < 1) return set_err(FFG_ERR_CUDA, "pair kernel: no co-resident CTA pair fits");
         max_pairs = nc;
     }
@@ -507,15 +507,45 @@ int pair_capacity(int* out) {
     return FFG_OK;
 }
 
-template <int MODE>
+template <int MODE, bool RES>
 int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
     int cap, rc;
-    if ((rc = pair_capacity<MODE>(&cap))) return rc;
+    if ((rc = pair_capacity<MODE, RES>(&cap))) return rc;
     if ((rc = install_watchdog())) return set_err(FFG_ERR_CUDA, "watchdog buffer");
+    // streaming: persistent pairs walk all items round-robin; resident: exactly one CTA pair per
+    // pair item of a layer (each keeps its block for all layers), `items` = pairs per layer
+    if (RES && items > cap) return set_err(FFG_ERR_CUDA, "resident K2: %lld pairs > %d resident", (long long)items, cap);
     const int pairs = (int)std::min<int64_t>(cap, items);
-    mlsp2_pair_kernel<MODE><<<2 * pairs, kPairThreads, PairCfg<MODE>::kSmem, st>>>(maps, pp);
+    mlsp2_pair_kernel<MODE, RES><<<2 * pairs, kPairThreads, PairCfg<MODE>::kSmem, st>>>(maps, pp);
     CK(cudaGetLastError());
     return FFG_OK;
+}
+
+template <bool RES>
+int pair_capacity_mode(int mode, int* cap) {
+    switch (mode) {
+        case kModeF32E: return pair_capacity<kModeF32E, RES>(cap);
+        case kModeF16: return pair_capacity<kModeF16, RES>(cap);
+        default: return pair_capacity<kModeBF16, RES>(cap);
+    }
+}
+template <bool RES>
+int launch_pair_mode(int mode, const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
+    switch (mode) {
+        case kModeF32E: return launch_pair<kModeF32E, RES>(maps, pp, items, st);
+        case kModeF16: return launch_pair<kModeF16, RES>(maps, pp, items, st);
+        default: return launch_pair<kModeBF16, RES>(maps, pp, items, st);
+    }
+}
+
+// Resident K2 (one block per CTA for the whole recursion, k2_pair.cuh resident_workers) when
+// a matrix's pair table fits the co-resident CTA pairs and FFG_RESIDENT=1.
+bool use_resident(int PT, int cap) {
+    static int v = [] {
+        const char* e = getenv("FFG_RESIDENT");
+        return e ? atoi(e) : 0;  // measured slower than streaming; opt-in
+    }();
+    return v != 0 && PT <= cap;
 }
 
 struct Job {
@@ -653,14 +683,10 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         pp.nb = nb;
         pp.PT = w.PT;
         pp.B = B;
-        int cap = 0;
-        switch (j.mode) {
-            case kModeF32E: rc = pair_capacity<kModeF32E>(&cap); break;
-            case kModeF16: rc = pair_capacity<kModeF16>(&cap); break;
-            default: rc = pair_capacity<kModeBF16>(&cap); break;
-        }
-        if (rc) return rc;
-        pp.G = group_size(B, np, w.PT, cap, j.mode);
+        pp.hi[0] = w.op[0];
+        pp.lo[0] = w.op[1];
+        pp.hi[1] = w.op[2];
+        pp.lo[1] = w.op[3];
         pp.l0 = 0;
         pp.l1 = md.n_layers;
         pp.n_layers = md.n_layers;
@@ -672,15 +698,26 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
             pp.prof = prof;
             g_prof_buf = prof;
         }
-        const int64_t items = (int64_t)md.n_layers * B * w.PT;
+        int cap_res = 0, cap = 0;
+        if ((rc = pair_capacity_mode<true>(j.mode, &cap_res))) return rc;
         cudaEvent_t stop;
         if ((rc = prof_begin(st, &stop, layer_flops * md.n_layers))) return rc;
-        switch (j.mode) {
-            case kModeF32E: rc = launch_pair<kModeF32E>(w.pmaps, pp, items, st); break;
-            case kModeF16: rc = launch_pair<kModeF16>(w.pmaps, pp, items, st); break;
-            default: rc = launch_pair<kModeBF16>(w.pmaps, pp, items, st); break;
+        if (use_resident(w.PT, cap_res)) {
+            // resident: groups of G matrices, one CTA pair per pair item for all layers
+            const int G = std::max(1, cap_res / w.PT);
+            for (int m0 = 0; m0 < B; m0 += G) {
+                PairParams gp = pp;
+                gp.m0 = m0;
+                gp.B = std::min(G, B - m0);
+                gp.G = gp.B;
+                if ((rc = launch_pair_mode<true>(j.mode, w.pmaps, gp, (int64_t)gp.B * w.PT, st))) return rc;
+            }
+        } else {
+            if ((rc = pair_capacity_mode<false>(j.mode, &cap))) return rc;
+            pp.G = group_size(B, np, w.PT, cap, j.mode);
+            const int64_t items = (int64_t)md.n_layers * B * w.PT;
+            if ((rc = launch_pair_mode<false>(j.mode, w.pmaps, pp, items, st))) return rc;
         }
-        if (rc) return rc;
         if (stop) CK(cudaEventRecord(stop, st));
     } else {
         for (int l = 0; l < md.n_layers; ++l) {

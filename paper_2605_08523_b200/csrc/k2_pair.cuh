@@ -37,6 +37,10 @@ constexpr int kPairThreads = 640;
 // launch allocation of 640 x 96 registers
 constexpr int kPRegsCtl = 48, kPRegsDrain = 96, kPRegsEpi = 120;
 static_assert(128 * kPRegsCtl + 256 * kPRegsDrain + 256 * kPRegsEpi <= 640 * 96, "setmaxnreg budget");
+// resident variant: 16 worker warps (drain + epilogue) own 32 columns each of the CTA's block
+constexpr int kResWorkers = 16;
+constexpr int kRRegsCtl = 40, kRRegsWork = 104;
+static_assert(128 * kRRegsCtl + 512 * kRRegsWork <= 640 * 96, "setmaxnreg budget (resident)");
 constexpr int kPairHalf = kBN / 2;                  // B rows supplied by each CTA
 constexpr int kPairOpA = kBM * kBK * 2;             // 16 KB
 constexpr int kPairOpB = kPairHalf * kBK * 2;       // 8 KB
@@ -95,6 +99,9 @@ struct PairParams {
                               // 16 skip operand loads, 32 skip hi/lo stores, 64 skip X/A
                               // global traffic (all measurement only: results are wrong)
     unsigned long long* prof; // [gridDim][16] (dbg & 8)
+    int m0;                   // first matrix of this launch (resident groups)
+    uint16_t* hi[2];          // hi/lo parity buffers [B][np][np] (resident epilogue stores)
+    uint16_t* lo[2];
 };
 
 __device__ __forceinline__ void pair_decode(const PairParams& p, int item, int& m, int& l, int& pi) {
@@ -109,8 +116,261 @@ __device__ __forceinline__ void pair_decode(const PairParams& p, int item, int& 
     r -= dl * per_layer;
     const int mi = r / p.PT;
     pi = r - mi * p.PT;
-    m = base + mi;
+    m = p.m0 + base + mi;
     l = p.l0 + dl;
+}
+
+
+__device__ __forceinline__ void stg_v4(uint16_t* gp, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    *reinterpret_cast<uint4*>(gp) = make_uint4(a, b, c, d);
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr) : "memory");
+    return v;
+}
+
+// Resident K2 workers (RES): warps 4-19 of each CTA own its block (R, C) of one matrix for
+// the whole recursion.  Warp w: TMEM lane quarter q = w & 3 (rows 32q..32q+31), column quarter
+// c = (w - 4) >> 2 (32 columns); thread = one row.  X_l lives in TMEM slot 3, A_l and the
+// per-layer Y in registers; per layer the only global traffic is the hi/lo pieces of X_{l+1}
+// (direct row segments straight from registers, the mirrored piece through an in-place
+// ldmatrix.trans / stmatrix transpose in a 2 KB per-warp staging piece).
+template <int MODE>
+__device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t tmem, int warp, int lane,
+                                                 uint32_t rank, int pair_id, int n_pairs, int total,
+                                                 int nk, uint64_t* slot_full, uint64_t* slot_empty,
+                                                 uint8_t* staging, double* red) {
+    using Tr = ModeTraits<MODE>;
+    const int q = warp & 3, c = (warp - 4) >> 2, wk = warp - 4;
+    const int r = q * 32 + lane;
+    const int nb = p.nb, n = p.n, np = p.np;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + 32 * c;  // + slot * 128
+    const uint32_t tX = tl + 3 * 128;
+    const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
+    const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
+    const uint32_t stg = smem_u32(staging) + wk * 2 * kPieceBytes;  // hi piece, lo piece
+    int m, l_first, pi;
+    pair_decode(p, pair_id, m, l_first, pi);
+    const uint32_t pr = __ldg(p.pairs + pi);
+    const int R = rank ? (pr >> 10) & 1023 : pr & 1023;
+    const int C = (pr >> 20) & 1023;
+    const bool dummy = rank && ((pr >> 30) & 1);
+    const bool diag = R == C;
+    const bool skip = dummy || (diag && c < q);  // lower half of a diagonal block: mirrored
+    const bool dblk = diag && c == q;            // this warp's 32x32 piece is on the diagonal
+    const int gi = R * kBM + r;
+    const bool c_on = gi < n;
+    float areg[32];
+    // X_0 -> TMEM slot 3, A_1 -> registers (K1 wrote both in the tile-interleaved layout)
+    if (!skip) {
+        const float* Xt = p.X + xa_tile_base(m, R, C, nb);
+        const float* At = p.A + xa_tile_base(m, R, C, nb);
+        uint32_t xv[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 x = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, 8 * c + j)));
+            const float4 a = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, 8 * c + j)));
+            xv[4 * j + 0] = __float_as_uint(x.x); xv[4 * j + 1] = __float_as_uint(x.y);
+            xv[4 * j + 2] = __float_as_uint(x.z); xv[4 * j + 3] = __float_as_uint(x.w);
+            areg[4 * j + 0] = a.x; areg[4 * j + 1] = a.y; areg[4 * j + 2] = a.z; areg[4 * j + 3] = a.w;
+        }
+        tmem_st_32x32b_x32(tX, xv);
+        tmem_st_wait();
+    } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) areg[e] = 0.0f;
+    }
+    int g = 0;
+    for (int item = pair_id; item < total; item += n_pairs) {
+        const int l = l_first + (item - pair_id) / n_pairs;
+        const bool last = (l == p.n_layers - 1);
+        const int chunks = (p.dbg & 2) ? 1 : pair_chunks(MODE, nk, l < p.exact_layers);
+        int ysl = 0;
+        {
+            float yacc[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) yacc[e] = 0.0f;
+#pragma unroll 1
+            for (int f = 0; f < chunks; ++f, ++g) {
+                const int sl = g % 3;
+                mbar_wait_sleep(&slot_full[sl], (g / 3) & 1);
+                tc_fence_after();
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tl + sl * 128, v);
+                tmem_ld_wait();
+                const bool lastc = f == chunks - 1;
+                if (!lastc) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
+                }
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    const float2 acc = add_f32x2(make_float2(yacc[e], yacc[e + 1]),
+                                                 make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+                    yacc[e] = acc.x;
+                    yacc[e + 1] = acc.y;
+                }
+                if (lastc) {  // Y of the layer into this slot; the epilogue below frees it
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(yacc[e] * inv_s2);
+                    tmem_st_32x32b_x32(tl + sl * 128, v);
+                    tmem_st_wait();
+                    ysl = sl;
+                }
+            }
+        }
+        // ------------------------------------------------------------- epilogue of layer l
+        const EpiCoef k = load_coef(p.coef, l, last);
+        EpiHealth hl;
+        double tr = 0.0, sq = 0.0;
+        const bool work = !skip && !(p.dbg & 1);
+        const int nxt = (l + 1) & 1;
+        uint16_t* const hbase = p.hi[nxt] + (size_t)m * np * np;
+        uint16_t* const lbase = p.lo[nxt] + (size_t)m * np * np;
+        double* Dm = (last && p.D) ? p.D + (size_t)m * n * n : nullptr;
+#pragma unroll
+        for (int h = 0; h < 2 && work; ++h) {
+            uint32_t yv[16], xv[16];
+            tmem_ld_32x32b_x16(tl + ysl * 128 + 16 * h, yv);
+            tmem_ld_32x32b_x16(tX + 16 * h, xv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int cl = 32 * c + 16 * h + e;
+                const float y = __uint_as_float(yv[e]);
+                const float x = __uint_as_float(xv[e]);
+                const bool dg = diag && cl == r;
+                const float xn = (dg && c_on) ? poly_step<true>(y, x, k) : poly_step<false>(y, x, k);
+                const bool own = !dblk || cl >= r;
+                if (own) hl.add(xn);
+                if (!last) {
+                    areg[16 * h + e] = acc_step(areg[16 * h + e], xn, k);
+                    xv[e] = __float_as_uint(xn);
+                } else {
+                    const int gj = C * kBN + cl;
+                    if (own && gi < n && gj < n) {
+                        const double dv = (double)areg[16 * h + e] + (double)xn;
+                        if (Dm) {
+                            Dm[(size_t)gi * n + gj] = dv;
+                            if (!dg) Dm[(size_t)gj * n + gi] = dv;
+                        }
+                        if (dg) {
+                            tr += dv;
+                            sq += dv * dv;
+                        } else {
+                            sq += 2.0 * dv * dv;
+                        }
+                    }
+                }
+            }
+            if (!last) {
+                tmem_st_32x32b_x16(tX + 16 * h, xv);
+                uint32_t hp[8], lp[8];
+#pragma unroll
+                for (int e = 0; e < 16; e += 2)
+                    split2<MODE>(__uint_as_float(xv[e]), __uint_as_float(xv[e + 1]), hp[e >> 1], lp[e >> 1]);
+                // row segment into the staging pieces (hi at +0, lo at +2 KB; row = lane)
+                sts_v4(stg + sw64(lane, 2 * h + 0), hp[0], hp[1], hp[2], hp[3]);
+                sts_v4(stg + sw64(lane, 2 * h + 1), hp[4], hp[5], hp[6], hp[7]);
+                if (Tr::kHasLo) {
+                    sts_v4(stg + kPieceBytes + sw64(lane, 2 * h + 0), lp[0], lp[1], lp[2], lp[3]);
+                    sts_v4(stg + kPieceBytes + sw64(lane, 2 * h + 1), lp[4], lp[5], lp[6], lp[7]);
+                }
+                tmem_st_wait();
+            }
+        }
+        // Y slot read by this warp: release it (every warp arrives, working or not)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * ysl);
+        if (!last && work) {
+            __syncwarp();
+#pragma unroll
+            for (int hl2 = 0; hl2 < (Tr::kHasLo ? 2 : 1); ++hl2) {
+                const uint32_t pc = stg + hl2 * kPieceBytes;
+                uint16_t* base = hl2 ? lbase : hbase;
+                if (!dblk) {
+                    // direct: row gi, columns C*128 + 32c .. +31 (64 contiguous bytes)
+                    uint16_t* gd = base + (size_t)gi * np + C * kBN + 32 * c;
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        const uint4 t = lds_v4(pc + sw64(lane, ch));
+                        stg_v4(gd + 8 * ch, t.x, t.y, t.z, t.w);
+                    }
+                    __syncwarp();
+                    transpose_piece_inplace(pc, lane);
+                    __syncwarp();
+                    // mirrored: rows C*128 + 32c + lane, columns R*128 + 32q .. +31
+                    uint16_t* gm = base + (size_t)(C * kBN + 32 * c + lane) * np + R * kBM + 32 * q;
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        const uint4 t = lds_v4(pc + sw64(lane, ch));
+                        stg_v4(gm + 8 * ch, t.x, t.y, t.z, t.w);
+                    }
+                } else {
+                    // diagonal piece: owned (col >= row) values mirrored into the lower triangle
+                    uint16_t own16[32];
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        const uint4 t = lds_v4(pc + sw64(lane, ch));
+                        const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) own16[8 * ch + e] = (uint16_t)(w4[e >> 1] >> (16 * (e & 1)));
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (e > lane) sts_u16(pc + sw64(e, lane >> 3) + (lane & 7) * 2, own16[e]);
+                    __syncwarp();
+                    uint16_t* gd = base + (size_t)gi * np + C * kBN + 32 * c;
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        const uint4 t = lds_v4(pc + sw64(lane, ch));
+                        stg_v4(gd + 8 * ch, t.x, t.y, t.z, t.w);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (!dummy) {
+            const bool any_nf = __any_sync(0xffffffffu, hl.nonfinite());
+            const bool any_hr = !last && __any_sync(0xffffffffu, hl.template half_range<MODE>());
+            if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], l + 1);
+            if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], l + 1);
+        }
+        if (last) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                tr += __shfl_xor_sync(0xffffffffu, tr, o);
+                sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            }
+            if (lane == 0) {
+                red[2 * wk + 0] = tr;
+                red[2 * wk + 1] = sq;
+            }
+            named_bar_sync(3, kResWorkers * 32);
+            if (wk == 0 && lane == 0) {
+                double T0 = 0.0, T1 = 0.0;
+                for (int w2 = 0; w2 < kResWorkers; ++w2) {  // fixed order
+                    T0 += red[2 * w2 + 0];
+                    T1 += red[2 * w2 + 1];
+                }
+                p.partials[(size_t)m * 2 * p.PT + 2 * pi + rank] = make_double2(T0, T1);
+            }
+        } else if (!dummy && l + 1 < p.l1) {
+            // publish the block: every worker's hi/lo stores -> (bar) -> release the counters
+            named_bar_sync(4, kResWorkers * 32);
+            if (wk == 0 && lane == 0) {
+                __threadfence();
+                uint32_t* cm = p.counters + (size_t)m * nb;
+                red_release_gpu_add(cm + R, 1u);
+                if (C != R) red_release_gpu_add(cm + C, 1u);
+            }
+        }
+    }
 }
 
 // dbg & 8: accumulate the cycles a role spends in a wait into a register counter
@@ -125,9 +385,10 @@ __device__ __forceinline__ void pair_decode(const PairParams& p, int item, int& 
         }                                                        \
     } while (0)
 
-template <int MODE>
+template <int MODE, bool RES = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     mlsp2_pair_kernel(const __grid_constant__ PairMaps tm, const __grid_constant__ PairParams p) {
+    constexpr int kSlots = RES ? 3 : 4;  // TMEM chunk ring (resident: slot 3 holds the X block)
     using Tr = ModeTraits<MODE>;
     using Cfg = PairCfg<MODE>;
     constexpr bool kDrain = Tr::kProducts == 3;
@@ -159,7 +420,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
         for (int i = 0; i < 4; ++i) {
             mbar_init(&slot_full[i], 1);
-            mbar_init(&slot_empty[i], 2 * kEpiWarps);  // drain warps, or epilogue warps (last chunk)
+            // streaming: drain warps, or epilogue warps (Y slot); resident: the 16 worker warps
+            mbar_init(&slot_empty[i], RES ? 2 * kResWorkers : 2 * kEpiWarps);
         }
         for (int i = 0; i < 4; ++i) mbar_init(&y_full[i], kEpiWarps);
         fence_barrier_init();
@@ -171,7 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kPRegsCtl) : "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RES ? kRRegsCtl : kPRegsCtl) : "memory");
         if (warp == 0 && lane == 0) {
             // ================================================= TMA producer (both CTAs)
             for (int i = 0; i < 2; ++i) {
@@ -206,7 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     if (p.dbg & 8) w_dep += (unsigned long long)(clock64() - t0);
                     fence_proxy_async_global();
                 }
-                if (!(p.dbg & 1) && !(dummy && rank)) {
+                if (!RES && !(p.dbg & 1) && !(dummy && rank)) {
                     const size_t tb = xa_tile_base(m, ap, sp, nb);
                     tma_prefetch_l2_bulk(p.X + tb, kBM * kBN * 4);
                     tma_prefetch_l2_bulk(p.A + tb, kBM * kBN * 4);
@@ -256,13 +518,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 const bool exact = l < p.exact_layers;
                 uint32_t t_slot = 0;
                 auto open_slot = [&]() {
-                    const int sl = g & 3;
-                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[sl], ((g >> 2) & 1) ^ 1));
+                    const int sl = g % kSlots;
+                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[sl], ((g / kSlots) & 1) ^ 1));
                     tc_fence_after();
                     t_slot = tmem + sl * 128;
                 };
                 auto close_slot = [&]() {
-                    if (elect_one_sync()) umma_commit_pair(&slot_full[g & 3]);
+                    if (elect_one_sync()) umma_commit_pair(&slot_full[g % kSlots]);
                     __syncwarp();
                     ++g;
                 };
@@ -335,6 +597,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             }
         }
         __syncwarp();
+    } else if constexpr (RES) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRRegsWork) : "memory");
+        resident_workers<MODE>(p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk,
+                               slot_full, slot_empty, smem + Cfg::kStagingOff,
+                               reinterpret_cast<double*>(bars + 2 * S + 14));
     } else if (warp < 4 + kEpiWarps) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsDrain) : "memory");
         // ===================================================== chunk drain -> Y (both CTAs)
@@ -438,8 +705,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll 1
             for (int qi = 0; qi < 2; ++qi) {
                 const int qc = s + 2 * qi;  // column quarter (32 columns)
-                if (dummy || (p.dbg & 1)) continue;
-                if (diag && qc < q) continue;  // lower half of a diagonal block: mirrored
+                // lower half of a diagonal block is mirrored from the upper half
+                if (dummy || (p.dbg & 1) || (diag && qc < q)) {
+                    if (lane == 0) tma_store_commit();
+                    continue;
+                }
                 if (!last) {
                     if (lane == 0) FFG_TIMED(w_st, tma_store_wait_read());  // staging free again
                     __syncwarp();
@@ -484,9 +754,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                             tma_store_2d(&tm.p_hi[nxt], stg + 2 * kPieceBytes, mcol, mrow);
                             if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + 3 * kPieceBytes, mcol, mrow);
                         }
-                        tma_store_commit();
                     }
                 }
+                if (lane == 0) tma_store_commit();  // one bulk group per quarter, possibly empty
             }
             // this warp's Y reads are done: release the pair's TMEM slot
             tc_fence_before();

@@ -289,3 +289,36 @@ def test_cpp_drop_in_shim(tmp_path, model):
                        capture_output=True, text=True, timeout=120)
     print(r.stdout, r.stderr)
     assert r.returncode == 0 and "OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_resident_variant_parity(tmp_path):
+    """The opt-in resident K2 (FFG_RESIDENT=1: one CTA pair keeps its block for all layers)
+    against the fp64 recursion, batched, FP32-emulated and BF16 (subprocess: the switch is
+    read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2605_08523_b200 import engine as E
+from paper_2605_08523_b200.hamiltonians import tight_binding, batch_params
+from oracle import oracle as O
+m = E.load_model("M1500")
+mu, kT = batch_params(6)
+for n in (256, 512):
+    Hs = [tight_binding(n, seed=10000 + k) for k in range(6)]
+    for mode, tol, ttol in ((E.PrecisionMode.MIXED_EMULATED, 5e-6, 1e-6), (E.PrecisionMode.BF16, 1e-1, 1e-2)):
+        Ds, st, pv = E.compute_density_matrices(Hs, mu, kT, m, mode)
+        for k in range(6):
+            R = O.density_matrix_f64(Hs[k], mu[k], kT[k], m.abcd, m.beta0, m.mu0)
+            e = np.abs(Ds[k] - R).max(); t = abs(st[k].trace - np.trace(R)) / np.trace(R)
+            assert np.array_equal(Ds[k], Ds[k].T)
+            assert e <= tol and t <= ttol, (n, mode, k, e, t)
+print("RESIDENT_OK")
+""" % root
+    env = dict(os.environ, FFG_RESIDENT="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "RESIDENT_OK" in r.stdout, r.stdout + r.stderr
