@@ -145,6 +145,49 @@ int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, cons
                              double* D_dev, double* stats_dev, int32_t* status_dev,
                              double* bounds_dev, void* stream);
 
+/* ---------------------------------------------------------------- workflow
+ * Callers of the density-matrix path built on the same pipeline: every call below runs
+ * K1 -> K2 -> K3 only; the statistics (Tr D, Tr D^2) that K3 already produces supply the
+ * Newton derivative and the entropy trace, so none needs an extra matrix multiply. */
+
+/* An entropy model (Architecture::Entropy, scalar_models.hpp:150-156; evaluate_entropy
+ * scalar_models.cpp:320-326): inner MLSP2 rows evaluated at x0 = alpha (x - mu0) + mu0 with
+ * no spectrum flip, s = (4 ln 2) y (1 - y).  inner.beta0 / inner.mu0 are the trained_at of
+ * the Fermi model it pairs with (pairing by exact (beta0, mu0)). */
+typedef struct ffg_entropy_model {
+    ffg_model inner;
+    double alpha;       /* in (0, 1) */
+} ffg_entropy_model;
+
+/* SPEC thermodynamics: entropy_trace = Tr s(H) for the Fermi function at
+ * (mu, kT), computed as (4 ln 2)(Tr Y - Tr Y^2) with Y the inner recursion's output (the
+ * fused statistics of K3: no extra GEMM for the final (4 ln 2) Y (I - Y) layer). */
+int ffg_entropy_trace(const double* H, int64_t n, double mu, double kT, const ffg_entropy_model* em,
+                      int32_t mode, double* entropy_trace, ffg_provenance* prov);
+
+/* SPEC expectation (Eq. 9): <A> = Tr(D A) = sum_ij D_ij A_ij for symmetric
+ * D, A (fixed-order device reduction).  Band energy = expectation(D, H - mu I). */
+int ffg_expectation(const double* D, const double* A, int64_t n, double* out);
+
+/* SPEC solve_chemical_potential (Eqs. 42-45): Newton iteration on
+ * g(mu) = Tr D(mu) - n_occ with g'(mu) = beta (Tr D - Tr D^2) (Eq. 44, from the fused
+ * statistics), steps clamped to half the spectral width, safeguarded by a bracket of the
+ * model's region of validity; bisection when g' < 1e-14 beta n (flat derivative).  One
+ * K1 -> K2 -> K3 run per iteration on the device-resident H. */
+typedef struct ffg_mu_report {
+    double mu;            /* final chemical potential (energy units of H)            */
+    double residual;      /* Tr D(mu) - n_occ                                       */
+    int32_t iterations;   /* density-matrix evaluations                             */
+    int32_t converged;    /* |residual| <= tol                                      */
+    int32_t bisections;   /* steps taken by bisection instead of Newton             */
+} ffg_mu_report;
+/* D_out (n*n) and stats_out ({Tr D, Tr D^2}) are for the final mu and may be NULL;
+ * history (2*max_iter doubles: mu_k, residual_k) may be NULL. */
+int ffg_solve_chemical_potential(const double* H, int64_t n, double kT, double n_occ, double mu_guess,
+                                 const ffg_model* model, int32_t mode, double tol, int32_t max_iter,
+                                 double* D_out, double* stats_out, double* history,
+                                 ffg_mu_report* report);
+
 /* Number of kernels ffg_density_matrices_dev launches for one call (for accounting). */
 int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, int32_t mode);
 

@@ -15,6 +15,7 @@ Run here (where /root/reference exists):  python oracle/gen_fixtures.py [--skip-
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -25,6 +26,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 from oracle import oracle as O  # noqa: E402
 from paper_2605_08523_b200.hamiltonians import tight_binding, goe  # noqa: E402
+
+# entropy models (train_entropy, trainer.cpp:1274) on the Fermi fixtures above
+ENTROPY = {"E40": dict(base="M40", samples=6000, max_iter=1000, seed=42),
+           "E1500": dict(base="M1500", samples=20000, max_iter=400, seed=42)}
 
 CONFIGS = {
     "M1500": dict(beta0=1500.0, mu0=1.0 / 3.0, layers=30, samples=20000, max_iter=400, seed=42),
@@ -55,9 +60,34 @@ def train(name: str) -> dict:
     }
 
 
+def train_entropy(name: str) -> dict:
+    c = ENTROPY[name]
+    R = O.ref()
+    m = O.load_coefficients(c["base"])
+    L = m["abcd"].shape[0]
+    abcd = np.zeros((L, 4))
+    alpha = ctypes.c_double()
+    rep = np.zeros(5)
+    rc = R.ffr_train_entropy_mlsp2(O._dp(np.ascontiguousarray(m["abcd"])), L, float(m["beta0"]),
+                                   float(m["mu0"]), c["samples"], c["max_iter"], c["seed"], O._dp(abcd),
+                                   ctypes.byref(alpha), O._dp(rep))
+    if rc < 0:
+        raise RuntimeError(R.ffr_last_error().decode())
+    return {
+        "name": name, "architecture": "entropy", "base": c["base"], "beta0": g17(m["beta0"]),
+        "mu0": g17(m["mu0"]), "alpha": g17(alpha.value),
+        "training": {k: c[k] for k in ("samples", "max_iter", "seed")} | {"weighting": "derivative"},
+        "report": {"final_max_error": rep[0], "final_rms_error": rep[1], "iterations": int(rep[2]),
+                   "converged": bool(rep[3]), "initial_max_error": rep[4]},
+        "provenance": "train_entropy (proj/core/src/trainer.cpp:1274) compiled from /root/reference via oracle/Makefile",
+        "layers": [[g17(v) for v in row] for row in abcd],
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-train", action="store_true")
+    ap.add_argument("--only-fermi", action="store_true", help="skip the entropy models")
     args = ap.parse_args()
     R = O.ref()
     assert R is not None, "build oracle/_ref first (make -C oracle)"
@@ -84,6 +114,28 @@ def main():
         with open(os.path.join(O.GOLDEN, f"scalar_{name}.json"), "w") as f:
             json.dump({"x": [g17(v) for v in xs], "evaluate_model": [g17(v) for v in ys],
                        "provenance": "reference evaluate_model (scalar_models.cpp:330) via oracle/_ref"}, f)
+
+    # entropy models + scalar golden tables (reference evaluate_model, Architecture::Entropy,
+    # and the exact fermi_entropy) on the same x grid
+    for name in ENTROPY if not args.only_fermi else ():
+        path = os.path.join(O.GOLDEN, f"coefficients_{name}.json")
+        if not (args.skip_train and os.path.exists(path)):
+            d = train_entropy(name)
+            if os.path.exists(path):
+                with open(path) as f:
+                    old = json.load(f)
+                assert old["layers"] == d["layers"] and old["alpha"] == d["alpha"], \
+                    f"{name}: trainer no longer bit-identical"
+            with open(path, "w") as f:
+                json.dump(d, f, indent=1)
+            print(name, d["report"])
+        e = O.load_entropy_coefficients(name)
+        ys, ex = O.evaluate_entropy_ref(e["abcd"], e["alpha"], float(e["beta0"]), float(e["mu0"]), xs)
+        with open(os.path.join(O.GOLDEN, f"scalar_{name}.json"), "w") as f:
+            json.dump({"x": [g17(v) for v in xs], "evaluate_model": [g17(v) for v in ys],
+                       "fermi_entropy": [g17(v) for v in ex],
+                       "provenance": "reference evaluate_model (Entropy, scalar_models.cpp:320-347) and "
+                                     "fermi_entropy via oracle/_ref"}, f)
 
     # SP2 sign sequences embedded into MLSP2 (scalar_models.cpp:63-88, :554-607)
     sp2 = {}

@@ -119,6 +119,70 @@ def load_coefficients(name: str) -> dict:
     return d
 
 
+def load_entropy_coefficients(name: str) -> dict:
+    """tests/golden/coefficients_<E...>.json -> {'abcd', 'alpha', 'beta0', 'mu0', ...}."""
+    d = load_coefficients(name)
+    d["alpha"] = float(d["alpha"])
+    return d
+
+
+def evaluate_entropy_ref(abcd: np.ndarray, alpha: float, beta0: float, mu0: float, x: np.ndarray):
+    """Reference evaluate_model for an Entropy model and fermi_entropy(x; beta0, mu0)."""
+    R = ref()
+    if R is None:
+        raise RuntimeError("oracle/_ref not built")
+    R.ffr_evaluate_entropy_model.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_double, ctypes.c_void_p, ctypes.c_int64,
+                                             ctypes.c_void_p, ctypes.c_void_p]
+    abcd = np.ascontiguousarray(abcd, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(x)
+    ex = np.zeros_like(x)
+    rc = R.ffr_evaluate_entropy_model(abcd.ctypes.data, abcd.shape[0], float(alpha), float(beta0), float(mu0),
+                                      x.ctypes.data, x.size, y.ctypes.data, ex.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(R.ffr_last_error().decode())
+    return y, ex
+
+
+def entropy_scalar(abcd: np.ndarray, alpha: float, mu0: float, x: np.ndarray) -> np.ndarray:
+    """evaluate_entropy (scalar_models.cpp:320-326) restated: x0 = alpha (x - mu0) + mu0 (no flip),
+    y = evaluate_mlsp2(x0) (acc += d x before the square; acc + x at the end), (4 ln 2) y (1 - y)."""
+    x0 = alpha * (np.asarray(x, dtype=np.float64) - mu0) + mu0
+    acc = np.zeros_like(x0)
+    xx = x0.copy()
+    for a, b, c, d in abcd:
+        acc = acc + d * xx
+        xx = a * xx * xx + b * xx + c
+    y = acc + xx
+    return 4.0 * np.log(2.0) * y * (1.0 - y)
+
+
+def entropy_trace_f64(H: np.ndarray, mu: float, kT: float, abcd: np.ndarray, alpha: float, beta0: float,
+                      mu0: float) -> float:
+    """Tr s(H) by the fp64 matrix recursion: X0 = alpha (beta/beta0)(H - mu I) + mu0 I, Y = MLSP2(X0),
+    Tr S = (4 ln 2)(Tr Y - Tr Y^2) (S = (4 ln 2) Y (I - Y), Y symmetric)."""
+    n = H.shape[0]
+    s = (1.0 / kT) / beta0
+    X = alpha * s * (H - mu * np.eye(n)) + mu0 * np.eye(n)
+    A = np.zeros_like(X)
+    for a, b, c, d in abcd:
+        A = A + d * X
+        X = a * (X @ X) + b * X + c * np.eye(n)
+    Y = A + X
+    return float(4.0 * np.log(2.0) * (np.trace(Y) - np.sum(Y * Y)))
+
+
+def entropy_trace_exact(H: np.ndarray, mu: float, kT: float) -> float:
+    """sum_i s(f(lambda_i)) with s(y) = -y ln y - (1-y) ln(1-y) (exact electronic entropy)."""
+    lam = np.linalg.eigvalsh(H)
+    z = (lam - mu) / kT
+    f = 1.0 / (1.0 + np.exp(np.clip(z, -700, 700)))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        s = -np.where(f > 0, f * np.log(f), 0.0) - np.where(f < 1, (1 - f) * np.log1p(-f), 0.0)
+    return float(np.sum(s))
+
+
 # ----------------------------------------------------------------------------- scalar
 
 def evaluate_model_c(abcd: np.ndarray, x: np.ndarray) -> np.ndarray:

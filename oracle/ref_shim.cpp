@@ -127,6 +127,66 @@ int ffr_train_fermi_mlsp2(double beta0, double mu0, int layers, int samples, int
     }
 }
 
+
+// train_entropy (trainer.cpp:1274) on an MLSP2 Fermi base; out: inner abcd rows, alpha;
+// report = [final_max, final_rms, iterations, converged, initial_max].
+int ffr_train_entropy_mlsp2(const double* base_abcd, int L, double beta0, double mu0, int samples,
+                            int max_iter, uint64_t seed, double* abcd_out, double* alpha_out,
+                            double* report) {
+    try {
+        const ModelCoefficients base = mlsp2_model(base_abcd, L, beta0, mu0);
+        TrainingConfig cfg;
+        cfg.beta0 = beta0;
+        cfg.mu0 = mu0;
+        cfg.architecture = Architecture::Mlsp2;
+        cfg.layers = L;
+        cfg.sample_count = samples;
+        cfg.max_iterations = max_iter;
+        cfg.seed = seed;
+        cfg.weighting = Weighting::Derivative;
+        auto [m, rep] = train_entropy(cfg, base);
+        const auto& e = std::get<EntropyModelCoefficients>(m.payload);
+        for (std::size_t i = 0; i < e.inner.layers.size(); ++i) {
+            abcd_out[4 * i + 0] = e.inner.layers[i].a;
+            abcd_out[4 * i + 1] = e.inner.layers[i].b;
+            abcd_out[4 * i + 2] = e.inner.layers[i].c;
+            abcd_out[4 * i + 3] = e.inner.layers[i].d;
+        }
+        *alpha_out = e.alpha;
+        report[0] = rep.final_max_error;
+        report[1] = rep.final_rms_error;
+        report[2] = rep.iterations;
+        report[3] = rep.converged ? 1.0 : 0.0;
+        report[4] = rep.initial_max_error;
+        return static_cast<int>(e.inner.layers.size());
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// evaluate_model (scalar_models.cpp:330, Architecture::Entropy) and the exact
+// fermi_entropy (scalar_models.hpp:56) on a grid of model-frame x.
+int ffr_evaluate_entropy_model(const double* abcd, int L, double alpha, double beta0, double mu0,
+                               const double* xs, int64_t n, double* out, double* exact) {
+    try {
+        EntropyModelCoefficients e;
+        e.inner = std::get<Mlsp2Coefficients>(mlsp2_model(abcd, L, beta0, mu0).payload);
+        e.alpha = alpha;
+        e.mu0 = mu0;
+        ModelCoefficients m;
+        m.architecture = Architecture::Entropy;
+        m.payload = std::move(e);
+        m.trained_at = FermiParams{beta0, mu0};
+        for (int64_t i = 0; i < n; ++i) {
+            out[i] = evaluate_model(m, xs[i]);
+            if (exact) exact[i] = fermi_entropy(xs[i], FermiParams{beta0, mu0});
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 double ffr_pairwise_sum(const double* v, int64_t n) {
     return pairwise_sum(std::span<const double>(v, static_cast<std::size_t>(n)));
 }

@@ -382,6 +382,17 @@ __global__ void row_stats_kernel(const double* D, int n, double2* partials) {
     if (lane == 0) partials[i] = make_double2(dg, sq);
 }
 
+// Per-row (sum_j D_ij A_ij, 0) partials, one warp per row (ffg_expectation).
+__global__ void row_dot_kernel(const double* D, const double* A, int n, double2* partials) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * 8 + warp;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s += D[(size_t)i * n + j] * A[(size_t)i * n + j];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) partials[i] = make_double2(s, 0.0);
+}
+
 // Layers 0..exact-1 drain the hi*hi accumulator after every MMA, later layers once per
 // K-block (their rounding is amplified far less by the remaining recursion).
 int exact_drain_layers() {
@@ -972,6 +983,45 @@ void rescale_coeffs(int B, const double* mu, const double* kT, const ffg_model* 
     }
 }
 
+// One K1 -> K2 -> K3 run of a single device-resident matrix (workspace staging) and its
+// per-matrix records: stats {Tr D, Tr D^2}, widened bounds {eps_min, eps_max, x_min, x_max},
+// status, flags.  D goes to w.Ds when want_D.
+int eval_single(Workspace& w, cudaStream_t st, int64_t n, double alpha, double gamma, double scale,
+                double mu, const ffg_model* md, int mode, bool want_D, double stats[2], double bounds[4],
+                int* status, int flags[2]) {
+    Job j;
+    j.B = 1;
+    j.n = n;
+    j.H_dev = w.Hs;
+    j.alpha = &alpha;
+    j.gamma = &gamma;
+    j.scale = &scale;
+    j.mu = &mu;
+    j.model = md;
+    j.mode = mode;
+    j.D_dev = want_D ? w.Ds : nullptr;
+    int rc;
+    if ((rc = enqueue(w, j, st))) return rc;
+    uint8_t* hs = static_cast<uint8_t*>(w.host_small);
+    CK(cudaMemcpyAsync(hs, w.stats, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs + 16, w.bounds_out, 32, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs + 48, w.status, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs + 52, w.flags, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    memcpy(stats, hs, 16);
+    memcpy(bounds, hs + 16, 32);
+    memcpy(status, hs + 48, 4);
+    memcpy(flags, hs + 52, 8);
+    return FFG_OK;
+}
+
+int status_error(int code, const double* b, const int* f) {
+    if (code == FFG_ERR_OUT_OF_REGION)
+        return set_err(code, "out of region of validity: x in [%.17g, %.17g] (eps=[%.17g, %.17g])", b[2], b[3],
+                       b[0], b[1]);
+    return set_err(code, "%s at layer %d", status_text(code), code == FFG_ERR_DIVERGED ? f[0] : f[1]);
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -1055,6 +1105,166 @@ int ffg_mixed_square(const float* X, int64_t n, float* Y_out) {
                   FFG_MODE_MIXED_EMULATED, Dp, nullptr, nullptr);
     if (rc) return rc;
     for (size_t e = 0; e < nn; ++e) Y_out[e] = (float)Yd[e];
+    return FFG_OK;
+}
+
+int ffg_expectation(const double* D, const double* A, int64_t n, double* out) {
+    int rc, dev;
+    if ((rc = validate_n(n))) return rc;
+    if (!D || !A || !out) return set_err(FFG_ERR_VALIDATION, "null argument");
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    const size_t nn = (size_t)n * n;
+    if ((rc = ensure_staging(w, nn))) return rc;
+    if ((rc = ensure(w, 1, 128, n, false))) return rc;
+    CK(cudaMemcpyAsync(w.Hs, A, nn * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.Ds, D, nn * 8, cudaMemcpyHostToDevice, st));
+    row_dot_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(w.Ds, w.Hs, (int)n, w.partials);
+    reset_kernel<<<1, 32, 0, st>>>(w.bounds, w.flags, 1);
+    FinalizeParams fp{};
+    fp.partials = w.partials;
+    fp.bounds = w.bounds;
+    fp.flags = w.flags;
+    fp.T = (int)n;
+    fp.B = 1;
+    fp.stats = w.stats;
+    fp.bounds_out = w.bounds_out;
+    fp.status = w.status;
+    finalize_stats_kernel<<<1, 256, 0, st>>>(fp);
+    CK(cudaGetLastError());
+    double r[2];
+    CK(cudaMemcpyAsync(r, w.stats, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *out = r[0];
+    return FFG_OK;
+}
+
+int ffg_entropy_trace(const double* H, int64_t n, double mu, double kT, const ffg_entropy_model* em,
+                      int32_t mode_api, double* entropy_trace, ffg_provenance* prov) {
+    int rc, dev, mode;
+    if (!em) return set_err(FFG_ERR_VALIDATION, "entropy model is null");
+    if ((rc = validate_model(&em->inner))) return rc;
+    if (!(em->alpha > 0.0 && em->alpha < 1.0) || !std::isfinite(em->alpha))
+        return set_err(FFG_ERR_VALIDATION, "EntropyModelCoefficients: alpha must lie in (0,1)");
+    if ((rc = mode_to_internal(mode_api, &mode))) return rc;
+    if ((rc = validate_n(n))) return rc;
+    if ((rc = check_mu_kT(1, &mu, &kT))) return rc;
+    if (!H || !entropy_trace) return set_err(FFG_ERR_VALIDATION, "null argument");
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    const size_t nn = (size_t)n * n;
+    if ((rc = ensure_staging(w, nn))) return rc;
+    CK(cudaMemcpyAsync(w.Hs, H, nn * 8, cudaMemcpyHostToDevice, st));
+    // model frame x = mu0 + s (H - mu), x0 = alpha (x - mu0) + mu0 = alpha s (H - mu) + mu0
+    const double s = (1.0 / kT) / em->inner.beta0;
+    const double a = em->alpha * s, g = em->inner.mu0 - em->alpha * s * mu;
+    double stats[2], bounds[4];
+    int status, flags[2];
+    if ((rc = eval_single(w, st, n, a, g, s, mu, &em->inner, mode, false, stats, bounds, &status, flags)))
+        return rc;
+    if (prov) fill_prov(prov, bounds, &kT, mu, status, flags, &em->inner, mode_api, (int)n, 0.0);
+    if (status != FFG_OK) return status_error(status, bounds, flags);
+    *entropy_trace = 4.0 * std::log(2.0) * (stats[0] - stats[1]);
+    return FFG_OK;
+}
+
+int ffg_solve_chemical_potential(const double* H, int64_t n, double kT, double n_occ, double mu_guess,
+                                 const ffg_model* md, int32_t mode_api, double tol, int32_t max_iter,
+                                 double* D_out, double* stats_out, double* history, ffg_mu_report* report) {
+    int rc, dev, mode;
+    if ((rc = validate_model(md))) return rc;
+    if ((rc = mode_to_internal(mode_api, &mode))) return rc;
+    if ((rc = validate_n(n))) return rc;
+    if (!H) return set_err(FFG_ERR_VALIDATION, "H is null");
+    if (!(kT > 0.0) || !std::isfinite(kT)) return set_err(FFG_ERR_VALIDATION, "kT must be positive and finite");
+    if (!(n_occ > 0.0 && n_occ < (double)n))
+        return set_err(FFG_ERR_VALIDATION, "n_occ must lie in (0, N) (got %.17g)", n_occ);
+    if (!std::isfinite(mu_guess)) return set_err(FFG_ERR_VALIDATION, "mu_guess must be finite");
+    if (!(tol > 0.0) || max_iter < 1) return set_err(FFG_ERR_VALIDATION, "tol > 0 and max_iter >= 1 required");
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    const size_t nn = (size_t)n * n;
+    if ((rc = ensure_staging(w, nn))) return rc;
+    CK(cudaMemcpyAsync(w.Hs, H, nn * 8, cudaMemcpyHostToDevice, st));
+    const double beta = 1.0 / kT, s = beta / md->beta0;
+    auto eval = [&](double mu, double* stats, double* bounds, int* status, int* flags) {
+        return eval_single(w, st, n, -s, (1.0 - md->mu0) + s * mu, s, mu, md, mode, true, stats, bounds, status,
+                           flags);
+    };
+    double mu = mu_guess, stats[2], bounds[4];
+    int status, flags[2];
+    if ((rc = eval(mu, stats, bounds, &status, flags))) return rc;
+    // bracket: mu for which the model's region of validity holds (x_min >= 0, x_max <= 1) and
+    // Tr D is monotone in mu (Eq. 43: dTr D / dmu = beta Tr D(I - D) >= 0)
+    const double W = bounds[1] - bounds[0];
+    double lo = std::max(bounds[0], bounds[1] - (1.0 - md->mu0) / s);
+    double hi = std::min(bounds[1], bounds[0] + md->mu0 / s);
+    if (!(lo < hi))
+        return set_err(FFG_ERR_OUT_OF_REGION, "no chemical potential keeps beta'=%.6g inside the model's region "
+                       "of validity (beta0=%.6g)", beta * W, md->beta0);
+    if (status == FFG_ERR_OUT_OF_REGION) {  // cold start outside the region: restart mid-bracket
+        mu = 0.5 * (lo + hi);
+        if ((rc = eval(mu, stats, bounds, &status, flags))) return rc;
+    }
+    if (status != FFG_OK) return status_error(status, bounds, flags);
+    int it = 1, bis = 0;
+    bool conv = false;
+    double g = stats[0] - n_occ;
+    for (;;) {
+        if (history) {
+            history[2 * (it - 1) + 0] = mu;
+            history[2 * (it - 1) + 1] = g;
+        }
+        if (std::fabs(g) <= tol) {
+            conv = true;
+            break;
+        }
+        if (it >= max_iter) break;
+        if (g > 0.0) hi = std::min(hi, mu); else lo = std::max(lo, mu);
+        const double gp = beta * (stats[0] - stats[1]);   // Eq. 44
+        double next;
+        if (gp > 1e-14 * beta * (double)n) {
+            double dmu = -g / gp;                             // Eq. 45
+            dmu = std::max(-0.5 * W, std::min(0.5 * W, dmu)); // clamp: half the spectral width
+            next = mu + dmu;
+            if (!(next > lo && next < hi)) {                  // safeguard: leave the bracket -> bisect
+                next = 0.5 * (lo + hi);
+                ++bis;
+            }
+        } else {                                              // flat derivative: bisection fallback
+            next = 0.5 * (lo + hi);
+            ++bis;
+        }
+        mu = next;
+        if ((rc = eval(mu, stats, bounds, &status, flags))) return rc;
+        if (status != FFG_OK) return status_error(status, bounds, flags);
+        g = stats[0] - n_occ;
+        ++it;
+    }
+    if (D_out) {
+        CK(cudaMemcpyAsync(D_out, w.Ds, nn * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    if (stats_out) {
+        stats_out[0] = stats[0];
+        stats_out[1] = stats[1];
+    }
+    if (report) {
+        report->mu = mu;
+        report->residual = g;
+        report->iterations = it;
+        report->converged = conv ? 1 : 0;
+        report->bisections = bis;
+    }
+    if (!conv)
+        return set_err(FFG_ERR_DIVERGED, "chemical potential not converged after %d evaluations "
+                       "(|Tr D - n_occ| = %.3g > tol %.3g)", it, std::fabs(g), tol);
     return FFG_OK;
 }
 

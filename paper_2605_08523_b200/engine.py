@@ -96,6 +96,15 @@ class _Model(ctypes.Structure):
                 ("mu0", ctypes.c_double)]
 
 
+class _EntropyModel(ctypes.Structure):
+    _fields_ = [("inner", _Model), ("alpha", ctypes.c_double)]
+
+
+class _MuReport(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_double), ("residual", ctypes.c_double), ("iterations", ctypes.c_int32),
+                ("converged", ctypes.c_int32), ("bisections", ctypes.c_int32)]
+
+
 class _Prov(ctypes.Structure):
     _fields_ = [("eps_min", ctypes.c_double), ("eps_max", ctypes.c_double),
                 ("beta_prime", ctypes.c_double), ("mu_prime", ctypes.c_double),
@@ -110,7 +119,8 @@ SYMBOLS = ("ffg_abi_version", "ffg_last_error", "ffg_device_available", "ffg_in_
            "ffg_spectral_bounds", "ffg_apply_model", "ffg_mixed_square", "ffg_density_statistics",
            "ffg_density_matrix", "ffg_density_matrices", "ffg_density_matrices_dev",
            "ffg_kernel_launches", "ffg_profile_layers", "ffg_profile_read",
-           "ffg_profile_read_ex", "ffg_pair_table", "ffg_release_workspaces")
+           "ffg_profile_read_ex", "ffg_pair_table", "ffg_release_workspaces",
+           "ffg_entropy_trace", "ffg_expectation", "ffg_solve_chemical_potential")
 
 
 @lru_cache(maxsize=None)
@@ -145,6 +155,13 @@ def lib() -> ctypes.CDLL:
     L.ffg_profile_layers.argtypes = [ctypes.c_int]
     L.ffg_profile_read.argtypes = [_D, ctypes.POINTER(ctypes.c_int64)]
     L.ffg_profile_read_ex.argtypes = [_D, ctypes.POINTER(ctypes.c_int64), _D]
+    L.ffg_entropy_trace.argtypes = [_D, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                    ctypes.POINTER(_EntropyModel), ctypes.c_int32, _D, ctypes.POINTER(_Prov)]
+    L.ffg_expectation.argtypes = [_D, _D, ctypes.c_int64, _D]
+    L.ffg_solve_chemical_potential.argtypes = [_D, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                               ctypes.c_double, ctypes.POINTER(_Model), ctypes.c_int32,
+                                               ctypes.c_double, ctypes.c_int32, _D, _D, _D,
+                                               ctypes.POINTER(_MuReport)]
     L.ffg_pair_table.restype = ctypes.c_int32
     L.ffg_pair_table.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32]
     L.ffg_release_workspaces.restype = None
