@@ -14,6 +14,10 @@
 //   density_statistics(D)
 //   compute_density_matrix(H, mu, kT, m, mode, prov) SPEC.md:458-462 (model selected by the caller)
 //   compute_density_matrices(Hs, mu, kT, m, mode)    batched
+//   solve_chemical_potential(H, beta, n_occ, guess, m) SPEC.md:468-476 (Eqs. 42-45)
+//   entropy_trace(H, mu, kT, entropy model)          SPEC.md:478-486 (Tr S, no extra GEMM)
+//   thermodynamics(H, beta, mu, m, entropy model)
+//   expectation(D, A)                                SPEC.md:488-495 (Eq. 9)
 //
 // Errors are rethrown as the reference's exception types: ValidationError
 // (scalar_models.hpp:21-24), DivergedEvaluationError{layer} (trainer.hpp:20-25),
@@ -192,6 +196,88 @@ inline std::vector<DensityStatistics> compute_density_matrices(
         for (auto& d : Dbuf) D_out->push_back(unchecked_from_buffer(n, std::move(d)));
     }
     return out;
+}
+
+// ---------------------------------------------------------------- workflow
+
+/// SPEC MuSolveReport.
+struct MuSolveReport {
+    double mu_final = 0.0;
+    int iterations = 0;
+    std::vector<std::pair<double, double>> residual_history;  // (mu, Tr D - n_occ)
+    bool converged = false;
+    int bisections = 0;
+};
+
+/// SPEC solve_chemical_potential: Newton on Tr D(mu) - n_occ with g'(mu) = beta (Tr D - Tr D^2)
+/// from the fused statistics (Eq. 44), clamped steps, bisection fallback; returns the density
+/// matrix at the converged mu.  Non-convergence throws DivergedEvaluationError.
+inline std::pair<SymmetricMatrix, MuSolveReport> solve_chemical_potential(
+    const SymmetricMatrix& H, double beta, double n_occ, double mu_guess, const ModelCoefficients& m,
+    double tol = 1e-6, int max_iter = 30, PrecisionMode mode = PrecisionMode::MixedEmulated) {
+    detail::FlatModel fm(m);
+    std::vector<double> D(static_cast<std::size_t>(H.dim()) * H.dim());
+    std::vector<double> hist(2 * static_cast<std::size_t>(max_iter));
+    double s[2];
+    ffg_mu_report r{};
+    const int rc = ffg_solve_chemical_potential(H.data().data(), H.dim(), 1.0 / beta, n_occ, mu_guess, &fm.c,
+                                                static_cast<int32_t>(mode), tol, max_iter, D.data(), s,
+                                                hist.data(), &r);
+    detail::check(rc);
+    MuSolveReport rep;
+    rep.mu_final = r.mu;
+    rep.iterations = r.iterations;
+    rep.converged = r.converged != 0;
+    rep.bisections = r.bisections;
+    for (int k = 0; k < r.iterations; ++k) rep.residual_history.emplace_back(hist[2 * k], hist[2 * k + 1]);
+    return {unchecked_from_buffer(H.dim(), std::move(D)), std::move(rep)};
+}
+
+/// SPEC thermodynamics' entropy term: Tr s(H) at (mu, kT) through an entropy model
+/// (EntropyModelCoefficients, scalar_models.hpp:150-156) trained at the Fermi model's (beta0, mu0).
+inline double entropy_trace(const SymmetricMatrix& H, double mu, double kT, const ModelCoefficients& em,
+                            PrecisionMode mode = PrecisionMode::MixedEmulated) {
+    em.validate();
+    if (em.architecture != Architecture::Entropy)
+        throw ValidationError("entropy_trace: an Entropy-architecture model is required");
+    const auto& e = std::get<EntropyModelCoefficients>(em.payload);
+    ModelCoefficients inner;
+    inner.architecture = Architecture::Mlsp2;
+    inner.payload = e.inner;
+    inner.trained_at = em.trained_at;
+    detail::FlatModel fm(inner);
+    ffg_entropy_model c{fm.c, e.alpha};
+    double out = 0.0;
+    ffg_provenance prov{};
+    detail::check(ffg_entropy_trace(H.data().data(), H.dim(), mu, kT, &c, static_cast<int32_t>(mode), &out, &prov));
+    return out;
+}
+
+/// SPEC expectation: Tr(D A) = sum_ij D_ij A_ij.
+inline double expectation(const SymmetricMatrix& D, const SymmetricMatrix& A) {
+    if (D.dim() != A.dim()) throw std::invalid_argument("expectation: dimension mismatch");
+    double out = 0.0;
+    detail::check(ffg_expectation(D.data().data(), A.data().data(), D.dim(), &out));
+    return out;
+}
+
+/// SPEC ThermodynamicResult.
+struct ThermodynamicResult {
+    SymmetricMatrix density;
+    double entropy_trace = 0.0, band_energy = 0.0, free_energy = 0.0;
+};
+
+/// SPEC thermodynamics with the models chosen by the caller (entropy model paired by exact
+/// (beta0, mu0)).
+inline ThermodynamicResult thermodynamics(const SymmetricMatrix& H, double beta, double mu,
+                                          const ModelCoefficients& m, const ModelCoefficients& em,
+                                          PrecisionMode mode = PrecisionMode::MixedEmulated) {
+    if (m.trained_at.beta != em.trained_at.beta || m.trained_at.mu != em.trained_at.mu)
+        throw ValidationError("thermodynamics: entropy model must share (beta0, mu0) with the Fermi model");
+    auto [D, st] = compute_density_matrix(H, mu, 1.0 / beta, m, mode);
+    const double ts = entropy_trace(H, mu, 1.0 / beta, em, mode);
+    const double band = expectation(D, H) - mu * st.trace;
+    return ThermodynamicResult{std::move(D), ts, band, band - ts / beta};
 }
 
 }  // namespace fermiforge

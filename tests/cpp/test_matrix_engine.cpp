@@ -89,6 +89,21 @@ int main(int argc, char** argv) {
     }
     const auto b = spectral_bounds(H);
     fails += !(b.eps_min < b.eps_max);
+
+    // workflow: mu solve restores n_occ; entropy / thermodynamics with a reference-typed
+    // EntropyModelCoefficients built from the Fermi set's own layers (structure test only)
+    const double n_occ = st.trace;
+    auto [Dm, rep] = solve_chemical_potential(H, 1.0 / kT, n_occ, mu + 0.03, m, 1e-3);
+    fails += !(rep.converged && std::abs(rep.mu_final - mu) <= 1e-3 && std::abs(Dm.trace() - n_occ) <= 2e-3);
+    std::printf("mu-solve: mu=%.6f (target %.6f) in %d evaluations\n", rep.mu_final, mu, rep.iterations);
+    ModelCoefficients em;
+    em.architecture = Architecture::Entropy;
+    em.payload = EntropyModelCoefficients{std::get<Mlsp2Coefficients>(m.payload), 0.85, m.trained_at.mu};
+    em.trained_at = m.trained_at;
+    const auto th = thermodynamics(H, 1.0 / kT, mu, m, em);
+    fails += !(std::isfinite(th.entropy_trace) &&
+               std::abs(th.free_energy - (th.band_energy - th.entropy_trace * kT)) <= 1e-9 * (1 + std::abs(th.free_energy)));
+    fails += !(std::abs(expectation(D, D) - st.trace_square) <= 1e-8 * st.trace_square);
     std::printf("%s\n", fails ? "FAIL" : "OK");
     return fails ? 1 : 0;
 }
