@@ -35,7 +35,14 @@ namespace ffg {
 constexpr int kPairThreads = 640;
 // setmaxnreg budgets per warpgroup (control / drain / epilogue); they only redistribute the
 // launch allocation of 640 x 96 registers
+#ifndef FFG_DRAIN_BATCH
+#define FFG_DRAIN_BATCH 2  // x16 TMEM loads in flight per drain wait (1 or 2; measured: 2)
+#endif
+#if FFG_DRAIN_BATCH > 1
+constexpr int kPRegsCtl = 48, kPRegsDrain = 104, kPRegsEpi = 112;
+#else
 constexpr int kPRegsCtl = 48, kPRegsDrain = 96, kPRegsEpi = 120;
+#endif
 static_assert(128 * kPRegsCtl + 256 * kPRegsDrain + 256 * kPRegsEpi <= 640 * 96, "setmaxnreg budget");
 // resident variant: 16 worker warps (drain + epilogue) own 32 columns each of the CTA's block
 constexpr int kResWorkers = 16;
@@ -65,8 +72,11 @@ static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue war
 // accumulate per K16 step into a chunk-sized partial (accumulation precision);
 // single-product modes: the whole K extent.  The drain warps sum chunks in registers with
 // round-to-nearest adds and write Y into the item's LAST slot, which the epilogue frees.
+#ifndef FFG_XA_AHEAD
+#define FFG_XA_AHEAD 0  // items ahead the producer prefetches the epilogue's X/A block into L2
+#endif
 #ifndef FFG_DRAIN_SPIN
-#define FFG_DRAIN_SPIN 0  // drain warps spin on slot_full instead of sleeping in try_wait
+#define FFG_DRAIN_SPIN 1  // drain warps spin on slot_full (measured faster than sleeping)
 #endif
 #ifndef FFG_EXACT_K16
 #define FFG_EXACT_K16 1  // K16 steps per chunk in exact-drain layers (1 or 2)
@@ -468,10 +478,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     if (p.dbg & 8) w_dep += (unsigned long long)(clock64() - t0);
                     fence_proxy_async_global();
                 }
-                if (!RES && !(p.dbg & 1) && !(dummy && rank)) {
-                    const size_t tb = xa_tile_base(m, ap, sp, nb);
-                    tma_prefetch_l2_bulk(p.X + tb, kBM * kBN * 4);
-                    tma_prefetch_l2_bulk(p.A + tb, kBM * kBN * 4);
+                // warm L2 with the X/A block the epilogue of a LATER item of this CTA will read
+                // (FFG_XA_AHEAD items ahead; L2 is the coherence point, so an early prefetch
+                // cannot serve stale data)
+                if (!RES && !(p.dbg & 1)) {
+                    const int ia = item + FFG_XA_AHEAD * n_pairs;
+                    if (ia < total) {
+                        int m2, l2, pi2;
+                        pair_decode(p, ia, m2, l2, pi2);
+                        const uint32_t pr2 = __ldg(p.pairs + pi2);
+                        if (!(rank && ((pr2 >> 30) & 1))) {
+                            const int ap2 = rank ? (pr2 >> 10) & 1023 : pr2 & 1023;
+                            const size_t tb = xa_tile_base(m2, ap2, (pr2 >> 20) & 1023, nb);
+                            tma_prefetch_l2_bulk(p.X + tb, kBM * kBN * 4);
+                            tma_prefetch_l2_bulk(p.A + tb, kBM * kBN * 4);
+                        }
+                    }
                 }
                 const int par = l & 1;
                 const int rowA = m * p.np + ap * kBM;
@@ -630,17 +652,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 tc_fence_after();
                 const bool lastc = f == chunks - 1;
 #pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t v[16];
-                    tmem_ld_32x32b_x16(tlane + sl * 128 + ch * 16, v);
+                for (int ch = 0; ch < 4; ch += FFG_DRAIN_BATCH) {
+                    uint32_t v[16 * FFG_DRAIN_BATCH];
+#pragma unroll
+                    for (int b = 0; b < FFG_DRAIN_BATCH; ++b)
+                        tmem_ld_32x32b_x16(tlane + sl * 128 + (ch + b) * 16,
+                                           *reinterpret_cast<uint32_t(*)[16]>(&v[16 * b]));
                     tmem_ld_wait();
-                    if (ch == 3 && !lastc) {
+                    if (ch + FFG_DRAIN_BATCH == 4 && !lastc) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
                     }
 #pragma unroll
-                    for (int e = 0; e < 16; e += 2) {
+                    for (int e = 0; e < 16 * FFG_DRAIN_BATCH; e += 2) {
                         const float2 acc = add_f32x2(
                             make_float2(yacc[16 * ch + e], yacc[16 * ch + e + 1]),
                             make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
@@ -678,8 +703,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
         int g = 0;
         uint32_t yph = 0;  // per-slot phase bits of y_full (a slot holds Y until freed here)
-        unsigned long long w_y = 0, w_pub = 0, w_st = 0;
+        unsigned long long w_y = 0, w_pub = 0, w_st = 0, w_cmp = 0, w_pc = 0, w_tail = 0, w_item = 0;
         for (int item = pair_id; item < total; item += n_pairs) {
+            const long long t_item = (p.dbg & 8) ? clock64() : 0;
             int m, l, pi;
             pair_decode(p, item, m, l, pi);
             const uint32_t pr = __ldg(p.pairs + pi);
@@ -715,6 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     __syncwarp();
                 }
                 const bool dblk = diag && qc == q;  // 32x32 piece on the matrix diagonal
+                const long long t_c0 = (p.dbg & 8) ? clock64() : 0;
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     const int c0 = 32 * qc + 16 * sub;
@@ -735,6 +762,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                             epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
                     }
                 }
+                const long long t_c1 = (p.dbg & 8) ? clock64() : 0;
+                if (p.dbg & 8) w_cmp += (unsigned long long)(t_c1 - t_c0);
                 if (!last) {
                     if (!dblk) {  // mirrored pieces: warp transpose of the direct pieces
                         __syncwarp();
@@ -757,7 +786,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     }
                 }
                 if (lane == 0) tma_store_commit();  // one bulk group per quarter, possibly empty
+                if (p.dbg & 8) w_pc += (unsigned long long)(clock64() - t_c1);
             }
+            const long long t_tail = (p.dbg & 8) ? clock64() : 0;
             // this warp's Y reads are done: release the pair's TMEM slot
             tc_fence_before();
             __syncwarp();
@@ -805,6 +836,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     if (C != R) red_release_gpu_add(cm + C, 1u);
                 }
             }
+            if (p.dbg & 8) {
+                const long long te = clock64();
+                w_tail += (unsigned long long)(te - t_tail);
+                w_item += (unsigned long long)(te - t_item);
+            }
         }
         if (lane == 0) tma_store_wait_all();
         if ((p.dbg & 8) && warp == 12 && lane == 0) {
@@ -812,6 +848,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             o[6] = w_y;
             o[7] = w_pub;
             o[8] = w_st;
+            o[9] = w_cmp;
+            o[10] = w_pc;
+            o[11] = w_tail;
+            o[12] = w_item;
         }
     }
     tc_fence_before();

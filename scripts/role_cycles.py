@@ -6,7 +6,8 @@ import numpy as np, torch
 from paper_2605_08523_b200 import engine as E
 from paper_2605_08523_b200.hamiltonians import tight_binding, batch_params
 m = E.load_model("M1500")
-names = ["total", "prod_dep", "prod_empty", "mma_full", "mma_slot", "drain_slotfull", "epi_y", "epi_publish", "epi_stwait"]
+names = ["total", "prod_dep", "prod_empty", "mma_full", "mma_slot", "drain_slotfull", "epi_y", "epi_publish",
+         "epi_stwait", "epi_compute", "epi_pieces", "epi_tail", "epi_item"]
 for spec in (sys.argv[1:] or ["1024x16", "4096x1", "512x64"]):
     n, B = (int(x) for x in spec.split("x"))
     for mode in (E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16):
@@ -24,5 +25,6 @@ for spec in (sys.argv[1:] or ["1024x16", "4096x1", "512x64"]):
         row = {k: a[:, i].mean() / tot for i, k in enumerate(names)}
         row["mma_full"] = lead[:, 3].mean() / tot
         row["mma_slot"] = lead[:, 4].mean() / tot
+        items = (p_items := None)
         print(f"n={n} B={B} {mode.name:15s} total {tot/1e6:8.2f} Mcyc  " +
               "  ".join(f"{k}={v:.2f}" for k, v in row.items() if k != "total"), flush=True)
