@@ -1,11 +1,12 @@
 // K2 epilogue arithmetic for one thread's row segment of a 128x128 block:
 //   X' = a Y + b X (+ c on the diagonal),  A' = A + d' X',  binary16 hi/lo split of X'
 // (scalar_models.cpp:243-252 per element: `acc += d*x` for the next layer, then
-// `x = a*x2 + b*x + c`).  The fp64 coefficients enter as hi/lo fp32 pairs and the products /
-// sums use error-free transformations (FMA product errors, TwoSum), so every result is the
-// fp32 rounding of an approximation accurate to ~2^-46 relative -- the same result as
-// evaluating in fp64 and rounding once, up to rare last-bit ties -- without fp64 or
-// conversion instructions.  Padded rows/columns (>= n) hold zeros in X and Y, so they stay
+// `x = a*x2 + b*x + c`).  The fp64 coefficients enter as hi/lo fp32 pairs, so no layer sees a
+// systematically rounded coefficient.  Default: fused FMAs, x' = fma(a_hi, y, fma(b_hi, x,
+// a_lo y + b_lo x)) (<= ~1 ulp); FFG_EPI_EFT=1 selects error-free transformations (FMA product
+// errors, TwoSum: the fp32 rounding of a ~2^-46-accurate value, as evaluating in fp64 and
+// rounding once).  Both measure the same accuracy on the parity sample; neither
+// uses fp64 or conversion instructions.  Padded rows/columns (>= n) hold zeros in X and Y, so they stay
 // zero (the identity term is only added for rows < n).
 #pragma once
 #include "kernels.cuh"
@@ -31,7 +32,8 @@ __device__ __forceinline__ EpiCoef load_coef(const double* coef, int l, bool las
 }
 
 #ifndef FFG_EPI_EFT
-#define FFG_EPI_EFT 1  // 1: error-free transformations (~correctly rounded); 0: fused FMAs
+#define FFG_EPI_EFT 0  // 1: error-free transformations (~correctly rounded); 0: fused FMAs on hi/lo
+                       // coefficients (default: same measured accuracy, 4-7% faster K2)
 #endif
 
 // a Y + b X (+ c when with_c), nearly correctly rounded
@@ -206,6 +208,74 @@ __device__ __forceinline__ void epi_sub_mid(const uint32_t (&v)[16], float* Xt, 
             __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
             __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
         }
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
+    }
+    if (!dblk) {
+        sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
+        sts_v4(stg_d + sw64(lane, 2 * sub + 1), hp[4], hp[5], hp[6], hp[7]);
+        if (Tr::kHasLo) {
+            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 0), lp[0], lp[1], lp[2], lp[3]);
+            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 1), lp[4], lp[5], lp[6], lp[7]);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const uint32_t col = 16 * sub + e;
+            if ((int)col < lane) continue;
+            const uint16_t hb = (uint16_t)(hp[e >> 1] >> (16 * (e & 1)));
+            const uint16_t lb = (uint16_t)(lp[e >> 1] >> (16 * (e & 1)));
+            const uint32_t off = sw64(col, lane >> 3) + (lane & 7) * 2;
+            const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
+            sts_u16(stg_d + off, hb);
+            sts_u16(stg_d + doff, hb);
+            if (Tr::kHasLo) {
+                sts_u16(stg_d + kPieceBytes + off, lb);
+                sts_u16(stg_d + kPieceBytes + doff, lb);
+            }
+        }
+    }
+}
+
+// X/A of 16 columns (c0 .. c0+15) of row r: four float4 each.
+__device__ __forceinline__ void epi_load16(const float* Xt, const float* At, int r, int c0, float4 (&xq)[4],
+                                           float4 (&aq)[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
+        aq[j] = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
+    }
+}
+
+// epi_sub_mid on X/A already in registers (the caller loads the next sub-block first)
+template <int MODE, bool DIAG>
+__device__ __forceinline__ void epi_sub_mid_pre(const uint32_t (&v)[16], const float4 (&xq)[4],
+                                                const float4 (&aq)[4], float* Xt, float* At, int r, int c0,
+                                                int lane, int sub, bool c_on, const EpiCoef& k, uint32_t stg_d,
+                                                bool dblk, EpiHealth& hl) {
+    using Tr = ModeTraits<MODE>;
+    uint32_t hp[8], lp[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
+        float as[4] = {aq[j].x, aq[j].y, aq[j].z, aq[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float y = __uint_as_float(v[4 * j + e]);
+            float xn;
+            if constexpr (DIAG) {
+                const int cl = c0 + 4 * j + e;
+                xn = (cl == r && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
+                if (cl >= r) hl.add(xn);
+            } else {
+                xn = poly_step<false>(y, xs[e], k);
+                hl.add(xn);
+            }
+            as[e] = acc_step(as[e], xn, k);
+            xs[e] = xn;
+        }
+        __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
+        __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
         split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
         split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
     }

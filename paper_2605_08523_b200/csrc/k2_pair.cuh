@@ -72,6 +72,15 @@ static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue war
 // accumulate per K16 step into a chunk-sized partial (accumulation precision);
 // single-product modes: the whole K extent.  The drain warps sum chunks in registers with
 // round-to-nearest adds and write Y into the item's LAST slot, which the epilogue frees.
+#ifndef FFG_EPI_PREFETCH
+#define FFG_EPI_PREFETCH 0  // epilogue loads sub-block 1's X/A before computing sub-block 0
+#endif
+#ifndef FFG_EPI_SPIN
+#define FFG_EPI_SPIN 0  // epilogue warps spin on y_full instead of sleeping
+#endif
+#ifndef FFG_DEP_BACKOFF
+#define FFG_DEP_BACKOFF 0  // ns of __nanosleep between panel-counter polls (0: tight poll)
+#endif
 #ifndef FFG_XA_AHEAD
 #define FFG_XA_AHEAD 0  // items ahead the producer prefetches the epilogue's X/A block into L2
 #endif
@@ -469,10 +478,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     const uint32_t need = (uint32_t)(nb * (l - p.l0));
                     const uint32_t* cm = p.counters + (size_t)m * nb;
                     const long long t0 = clock64();
-                    while (ld_acquire_gpu(cm + ap) < need)
+                    while (ld_acquire_gpu(cm + ap) < need && (FFG_DEP_BACKOFF ? (__nanosleep(FFG_DEP_BACKOFF), 1) : 1))
                         watchdog_check(t0, 3, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + ap),
                                        ((unsigned long long)need << 32) | ld_acquire_gpu(cm + ap));
-                    while (ld_acquire_gpu(cm + sp) < need)
+                    while (ld_acquire_gpu(cm + sp) < need && (FFG_DEP_BACKOFF ? (__nanosleep(FFG_DEP_BACKOFF), 1) : 1))
                         watchdog_check(t0, 4, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + sp),
                                        ((unsigned long long)need << 32) | ld_acquire_gpu(cm + sp));
                     if (p.dbg & 8) w_dep += (unsigned long long)(clock64() - t0);
@@ -725,7 +734,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             float* At = p.A + xa_tile_base(m, R, C, nb);
             EpiHealth hl;
             double tr = 0.0, sq = 0.0;
+#if FFG_EPI_SPIN
+            FFG_TIMED(w_y, mbar_wait(&y_full[ysl], (yph >> ysl) & 1));
+#else
             FFG_TIMED(w_y, mbar_wait_sleep(&y_full[ysl], (yph >> ysl) & 1));
+#endif
             yph ^= 1u << ysl;
             tc_fence_after();
 #pragma unroll 1
@@ -742,6 +755,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 }
                 const bool dblk = diag && qc == q;  // 32x32 piece on the matrix diagonal
                 const long long t_c0 = (p.dbg & 8) ? clock64() : 0;
+#if FFG_EPI_PREFETCH
+                float4 xq[4], aq[4];
+                if (!last) epi_load16(Xt, At, r, 32 * qc, xq, aq);
+#endif
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     const int c0 = 32 * qc + 16 * sub;
@@ -749,11 +766,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     tmem_ld_32x32b_x16(tacc + c0, v);
                     tmem_ld_wait();
                     if (!last) {
+#if FFG_EPI_PREFETCH
+                        // software pipeline: the next sub-block's X/A are in flight during this one
+                        float4 xn[4], an[4];
+                        if (sub == 0) epi_load16(Xt, At, r, c0 + 16, xn, an);
+                        if (diag)
+                            epi_sub_mid_pre<MODE, true>(v, xq, aq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl);
+                        else
+                            epi_sub_mid_pre<MODE, false>(v, xq, aq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl);
+                        if (sub == 0) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                xq[j] = xn[j];
+                                aq[j] = an[j];
+                            }
+                        }
+#else
                         const bool nomem = p.dbg & 64;
                         if (diag)
                             epi_sub_mid<MODE, true>(v, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl, nomem);
                         else
                             epi_sub_mid<MODE, false>(v, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl, nomem);
+#endif
                     } else {
                         double* Dm = p.D ? p.D + (size_t)m * n * n : nullptr;
                         if (diag)
