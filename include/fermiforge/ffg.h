@@ -135,6 +135,16 @@ int ffg_density_matrices(int32_t batch, const double* const* H, int64_t n, const
                          const double* kT, const ffg_model* model, int32_t mode,
                          double* const* D_out, double* stats_out, ffg_provenance* prov);
 
+/* Asynchronous form of ffg_density_matrices for pipelined callers (a serving loop): enqueues
+ * the chunked H2D / compute / D2H pipeline and returns a ticket at once; at most two calls may
+ * be in flight, so a caller overlaps step k's transfers with step k-1's compute.  H and D_out
+ * must stay valid (page-locked for overlap) until ffg_wait(ticket) returns; stats / prov /
+ * status are delivered by ffg_wait. */
+int ffg_density_matrices_async(int32_t batch, const double* const* H, int64_t n, const double* mu,
+                               const double* kT, const ffg_model* model, int32_t mode,
+                               double* const* D_out, int64_t* ticket);
+int ffg_wait(int64_t ticket, double* stats_out, ffg_provenance* prov);
+
 /* Device-resident batch, asynchronous on `stream` (cudaStream_t, NULL = default):
  * H_dev [batch][n][n] fp64; mu / kT host arrays (copied at call time);
  * D_dev [batch][n][n] fp64 or NULL; stats_dev [batch][2]; status_dev [batch] int32

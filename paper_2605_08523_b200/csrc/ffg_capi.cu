@@ -134,6 +134,27 @@ int make_map(CUtensorMap* tm, void* base, int64_t rows, int64_t np, int elem, in
 }
 
 // --------------------------------------------------------------------- workspace
+// One in-flight batch of the host-buffer path: device staging, pinned per-matrix records,
+// events, and the call parameters provenance needs at wait time.
+struct HostSlot {
+    static constexpr int kMaxChunks = 8;
+    double* Hs = nullptr;
+    double* Ds = nullptr;
+    size_t cap = 0;
+    void* host_small = nullptr;
+    size_t host_small_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_d2h = nullptr;
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
+    bool busy = false;
+    int64_t ticket = 0;
+    int B = 0;
+    int64_t n = 0;
+    int mode_api = 0;
+    ffg_model model{};
+    std::vector<double> mu, kT;
+    bool has_mu = false, has_kT = false;
+};
+
 struct Workspace {
     int device = -1;
     size_t cap_elems = 0;  // B * np * np
@@ -170,13 +191,17 @@ struct Workspace {
     size_t cap_coef = 0;
     int pm_B = -1, pm_np = -1;
     PairMaps pmaps;
-    // pipelined host path (run_host): copy streams and per-chunk events
-    static constexpr int kMaxChunks = 8;
+    // pipelined host path (submit_host / finish_host): copy streams and two in-flight slots
+    static constexpr int kMaxChunks = HostSlot::kMaxChunks;
+    static constexpr int kSlots = 2;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-    cudaEvent_t ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
+    HostSlot slot[kSlots];
+    int64_t next_ticket = 0;
     // pinned upload ring for small per-call host data (params, coefficients)
-    static constexpr int kRing = 8;
-    static constexpr size_t kSlot = 64 * 1024;
+    // (deep enough that the pipelined host path never blocks on a slot whose copy is pending:
+    // two uploads per chunk, up to kMaxChunks chunks per call, several calls in flight)
+    static constexpr int kRing = 64;
+    static constexpr size_t kSlot = 16 * 1024;
     uint8_t* ring = nullptr;
     cudaEvent_t ring_ev[kRing] = {};
     int ring_next = 0;
@@ -218,10 +243,17 @@ void free_ws(Workspace* w) {
     cudaFreeHost(w->ring);
     if (w->s_h2d) cudaStreamDestroy(w->s_h2d);
     if (w->s_d2h) cudaStreamDestroy(w->s_d2h);
-    for (auto& e : w->ev_in)
-        if (e) cudaEventDestroy(e);
-    for (auto& e : w->ev_done)
-        if (e) cudaEventDestroy(e);
+    for (auto& hsl : w->slot) {
+        cudaFree(hsl.Hs);
+        cudaFree(hsl.Ds);
+        cudaFreeHost(hsl.host_small);
+        for (cudaEvent_t e : {hsl.ev0, hsl.ev1, hsl.ev_d2h})
+            if (e) cudaEventDestroy(e);
+        for (auto& e : hsl.ev_in)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : hsl.ev_done)
+            if (e) cudaEventDestroy(e);
+    }
     for (auto& e : w->ring_ev)
         if (e) cudaEventDestroy(e);
     if (w->ev0) cudaEventDestroy(w->ev0);
@@ -834,55 +866,72 @@ const char* status_text(int st) {
     }
 }
 
-// Chunks of the pipelined host path: about 4 matrices each (measured at N=1024, B=16:
-// e2e 1915 / 2646 / 2883 matrices/s for 1 / 2 / 4 chunks), at most Workspace::kMaxChunks;
+// Chunks of the pipelined host path (smaller chunks overlap more transfer but shrink each K2
+// launch below its dependency slack).  Measured at N=1024, B=16: one synchronous call, 1 / 2 /
+// 4 chunks -> e2e 1990 / 2795 / 3041 matrices/s (default B/4); two async calls in flight ->
+// 3647 / 4507 / 3797 (default B/8: the neighbouring call already covers the edges).
 // FFG_E2E_CHUNKS overrides.
-int e2e_chunks(int B) {
+int e2e_chunks(int B, bool async) {
     const char* e = getenv("FFG_E2E_CHUNKS");
-    const int c = e ? atoi(e) : B / 4;
+    const int c = e ? atoi(e) : B / (async ? 8 : 4);
     return std::max(1, std::min({c, B, (int)Workspace::kMaxChunks}));
 }
 
 // Host-buffer driver shared by density_matrix(ces) / apply_model / mixed_square.
-int run_host(int B, const double* const* H, int64_t n, const double* alpha, const double* gamma,
-             const double* scale, const double* mu, const double* kT, const ffg_model* md,
-             int mode_api, double* const* D_out, double* stats_out, ffg_provenance* prov) {
-    int rc, dev, mode;
-    if ((rc = validate_model(md))) return rc;
-    if ((rc = mode_to_internal(mode_api, &mode))) return rc;
-    if ((rc = validate_n(n))) return rc;
-    if (B < 1) return set_err(FFG_ERR_DIMENSION, "batch must be >= 1");
-    for (int m = 0; m < B; ++m)
-        if (!H[m]) return set_err(FFG_ERR_VALIDATION, "H[%d] is null", m);
-    if ((rc = check_device(&dev))) return rc;
-    cudaStream_t st = lib_stream();
-    Workspace& w = *get_ws(dev, st);
-    std::lock_guard<std::mutex> lk(w.mu);
+// Submit the pipelined host path for one batch into a free pipeline slot (no host sync): the
+// batch runs in chunks; chunk k's H2D (copy stream) overlaps the compute of chunk k-1 and its
+// D2H (second copy stream) the compute of chunk k+1.  All kernels stay on the library stream
+// (K2 needs every CTA of its launch co-resident).  Two slots: a call may be submitted while
+// the previous one is still in flight; slot buffers (H/D staging, pinned records) are per slot,
+// the K2 workspace is shared in stream order.
+int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, int64_t n, const double* alpha,
+                const double* gamma, const double* scale, const double* mu, const double* kT,
+                const ffg_model* md, int mode_api, int mode, double* const* D_out, int* slot_out,
+                bool async = false) {
+    int rc;
+    int si = -1;
+    for (int k = 0; k < Workspace::kSlots; ++k)
+        if (!w.slot[k].busy && (si < 0 || w.slot[k].ticket < w.slot[si].ticket)) si = k;
+    if (si < 0) return set_err(FFG_ERR_VALIDATION, "two calls already in flight: ffg_wait one first");
+    HostSlot& hsl = w.slot[si];
     const size_t nn = (size_t)n * n;
-    if ((rc = ensure_staging(w, (size_t)B * nn))) return rc;
+    size_t dummy = 0;
+    if ((size_t)B * nn > hsl.cap) {
+        if ((rc = grow(&hsl.Hs, dummy, (size_t)B * nn))) return rc;
+        if ((rc = grow(&hsl.Ds, dummy, (size_t)B * nn))) return rc;
+        hsl.cap = (size_t)B * nn;
+    }
+    const size_t small = (size_t)B * (2 * 8 + 4 * 8 + 4 + 8);
+    if (small > hsl.host_small_bytes) {
+        cudaFreeHost(hsl.host_small);
+        CK(cudaMallocHost(&hsl.host_small, small));
+        hsl.host_small_bytes = small;
+    }
+    if (!hsl.ev0) {
+        CK(cudaEventCreate(&hsl.ev0));
+        CK(cudaEventCreate(&hsl.ev1));
+        CK(cudaEventCreateWithFlags(&hsl.ev_d2h, cudaEventDisableTiming));
+        for (int k = 0; k < Workspace::kMaxChunks; ++k) {
+            CK(cudaEventCreateWithFlags(&hsl.ev_in[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&hsl.ev_done[k], cudaEventDisableTiming));
+        }
+    }
+    if (!w.s_h2d) {
+        CK(cudaStreamCreateWithFlags(&w.s_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&w.s_d2h, cudaStreamNonBlocking));
+    }
     const int64_t np = (n + kBM - 1) / kBM * kBM;
     const int64_t T = (np / kBM) * (np / kBM + 1) / 2;
     if ((rc = ensure(w, B, np, T, true))) return rc;
     bool want_D = false;
     if (D_out)
         for (int m = 0; m < B; ++m) want_D |= D_out[m] != nullptr;
-    uint8_t* hs = static_cast<uint8_t*>(w.host_small);
+    uint8_t* hs = static_cast<uint8_t*>(hsl.host_small);
     double* h_stats = reinterpret_cast<double*>(hs);
     double* h_bounds = h_stats + 2 * B;
     int* h_status = reinterpret_cast<int*>(h_bounds + 4 * B);
     int* h_flags = h_status + B;
-    // Pipelined host path: the batch runs in chunks; chunk k's H2D (copy stream) overlaps the
-    // compute of chunk k-1 and its D2H (second copy stream) the compute of chunk k+1.  All
-    // kernels stay on the library stream (K2 needs every CTA of its launch co-resident).
-    const int nchunk = e2e_chunks(B);
-    if (!w.s_h2d) {
-        CK(cudaStreamCreateWithFlags(&w.s_h2d, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&w.s_d2h, cudaStreamNonBlocking));
-        for (int k = 0; k < Workspace::kMaxChunks; ++k) {
-            CK(cudaEventCreateWithFlags(&w.ev_in[k], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&w.ev_done[k], cudaEventDisableTiming));
-        }
-    }
+    const int nchunk = e2e_chunks(B, async);
     auto chunk_range = [&](int k, int& m0, int& mb) {
         m0 = (int)((int64_t)B * k / nchunk);
         mb = (int)((int64_t)B * (k + 1) / nchunk) - m0;
@@ -891,45 +940,70 @@ int run_host(int B, const double* const* H, int64_t n, const double* alpha, cons
         int m0, mb;
         chunk_range(k, m0, mb);
         for (int m = m0; m < m0 + mb; ++m)
-            CK(cudaMemcpyAsync(w.Hs + m * nn, H[m], nn * sizeof(double), cudaMemcpyHostToDevice, w.s_h2d));
-        CK(cudaEventRecord(w.ev_in[k], w.s_h2d));
+            CK(cudaMemcpyAsync(hsl.Hs + m * nn, H[m], nn * sizeof(double), cudaMemcpyHostToDevice, w.s_h2d));
+        CK(cudaEventRecord(hsl.ev_in[k], w.s_h2d));
     }
-    CK(cudaEventRecord(w.ev0, st));
+    CK(cudaEventRecord(hsl.ev0, st));
     for (int k = 0; k < nchunk; ++k) {
         int m0, mb;
         chunk_range(k, m0, mb);
-        CK(cudaStreamWaitEvent(st, w.ev_in[k], 0));
+        CK(cudaStreamWaitEvent(st, hsl.ev_in[k], 0));
         Job j;
         j.B = mb;
         j.n = n;
-        j.H_dev = w.Hs + m0 * nn;
+        j.H_dev = hsl.Hs + m0 * nn;
         j.alpha = alpha + m0;
         j.gamma = gamma + m0;
         j.scale = scale ? scale + m0 : nullptr;
         j.mu = mu ? mu + m0 : nullptr;
         j.model = md;
         j.mode = mode;
-        j.D_dev = want_D ? w.Ds + m0 * nn : nullptr;
+        j.D_dev = want_D ? hsl.Ds + m0 * nn : nullptr;
         if ((rc = enqueue(w, j, st))) return rc;
         // per-matrix records of this chunk (the next chunk's reset reuses the workspace)
         CK(cudaMemcpyAsync(h_stats + 2 * m0, w.stats, sizeof(double) * 2 * mb, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(h_bounds + 4 * m0, w.bounds_out, sizeof(double) * 4 * mb, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(h_status + m0, w.status, sizeof(int) * mb, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(h_flags + 2 * m0, w.flags, sizeof(int) * 2 * mb, cudaMemcpyDeviceToHost, st));
-        CK(cudaEventRecord(w.ev_done[k], st));
+        CK(cudaEventRecord(hsl.ev_done[k], st));
         if (want_D) {
-            CK(cudaStreamWaitEvent(w.s_d2h, w.ev_done[k], 0));
+            CK(cudaStreamWaitEvent(w.s_d2h, hsl.ev_done[k], 0));
             for (int m = m0; m < m0 + mb; ++m)
                 if (D_out[m])
-                    CK(cudaMemcpyAsync(D_out[m], w.Ds + m * nn, nn * sizeof(double), cudaMemcpyDeviceToHost,
+                    CK(cudaMemcpyAsync(D_out[m], hsl.Ds + m * nn, nn * sizeof(double), cudaMemcpyDeviceToHost,
                                        w.s_d2h));
         }
     }
-    CK(cudaEventRecord(w.ev1, st));
-    CK(cudaStreamSynchronize(st));
-    CK(cudaStreamSynchronize(w.s_d2h));
+    CK(cudaEventRecord(hsl.ev1, st));
+    CK(cudaEventRecord(hsl.ev_d2h, w.s_d2h));
+    hsl.busy = true;
+    hsl.ticket = ++w.next_ticket;
+    hsl.B = B;
+    hsl.n = n;
+    hsl.mode_api = mode_api;
+    hsl.model = *md;
+    hsl.mu.assign(mu ? mu : alpha, (mu ? mu : alpha) + B);
+    hsl.has_mu = mu != nullptr;
+    hsl.kT.assign(kT ? kT : alpha, (kT ? kT : alpha) + B);
+    hsl.has_kT = kT != nullptr;
+    *slot_out = si;
+    return FFG_OK;
+}
+
+// Wait for a submitted batch and deliver its statistics / provenance / status.
+int finish_host(Workspace& w, int si, double* stats_out, ffg_provenance* prov) {
+    HostSlot& hsl = w.slot[si];
+    hsl.busy = false;
+    CK(cudaEventSynchronize(hsl.ev1));
+    CK(cudaEventSynchronize(hsl.ev_d2h));
     float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, w.ev0, w.ev1));
+    CK(cudaEventElapsedTime(&ms, hsl.ev0, hsl.ev1));
+    const int B = hsl.B;
+    uint8_t* hs = static_cast<uint8_t*>(hsl.host_small);
+    double* h_stats = reinterpret_cast<double*>(hs);
+    double* h_bounds = h_stats + 2 * B;
+    int* h_status = reinterpret_cast<int*>(h_bounds + 4 * B);
+    int* h_flags = h_status + B;
     int first = FFG_OK, first_m = -1;
     for (int m = 0; m < B; ++m) {
         if (stats_out) {
@@ -937,8 +1011,9 @@ int run_host(int B, const double* const* H, int64_t n, const double* alpha, cons
             stats_out[2 * m + 1] = h_stats[2 * m + 1];
         }
         if (prov)
-            fill_prov(&prov[m], h_bounds + 4 * m, kT ? kT + m : nullptr, mu ? mu[m] : 0.0,
-                      h_status[m], h_flags + 2 * m, md, mode_api, (int)n, ms);
+            fill_prov(&prov[m], h_bounds + 4 * m, hsl.has_kT ? &hsl.kT[m] : nullptr,
+                      hsl.has_mu ? hsl.mu[m] : 0.0, h_status[m], h_flags + 2 * m, &hsl.model, hsl.mode_api,
+                      (int)hsl.n, ms);
         if (h_status[m] != FFG_OK && first == FFG_OK) {
             first = h_status[m];
             first_m = m;
@@ -957,6 +1032,33 @@ int run_host(int B, const double* const* H, int64_t n, const double* alpha, cons
                        first == FFG_ERR_DIVERGED ? f[0] : f[1]);
     }
     return FFG_OK;
+}
+
+int validate_host_call(int B, const double* const* H, int64_t n, const ffg_model* md, int mode_api, int* mode,
+                       int* dev) {
+    int rc;
+    if ((rc = validate_model(md))) return rc;
+    if ((rc = mode_to_internal(mode_api, mode))) return rc;
+    if ((rc = validate_n(n))) return rc;
+    if (B < 1) return set_err(FFG_ERR_DIMENSION, "batch must be >= 1");
+    for (int m = 0; m < B; ++m)
+        if (!H[m]) return set_err(FFG_ERR_VALIDATION, "H[%d] is null", m);
+    return check_device(dev);
+}
+
+// Host-buffer driver shared by density_matrix(ces) / apply_model / mixed_square: submit + wait.
+int run_host(int B, const double* const* H, int64_t n, const double* alpha, const double* gamma,
+             const double* scale, const double* mu, const double* kT, const ffg_model* md,
+             int mode_api, double* const* D_out, double* stats_out, ffg_provenance* prov) {
+    int rc, dev, mode;
+    if ((rc = validate_host_call(B, H, n, md, mode_api, &mode, &dev))) return rc;
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    int si;
+    if ((rc = submit_host(w, st, B, H, n, alpha, gamma, scale, mu, kT, md, mode_api, mode, D_out, &si)))
+        return rc;
+    return finish_host(w, si, stats_out, prov);
 }
 
 int check_mu_kT(int B, const double* mu, const double* kT) {
@@ -1318,6 +1420,37 @@ int ffg_density_matrices(int32_t batch, const double* const* H, int64_t n, const
     rescale_coeffs(batch, mu, kT, model, alpha, gamma, scale);
     return run_host(batch, H, n, alpha.data(), gamma.data(), scale.data(), mu, kT, model, mode,
                     D_out, stats_out, prov);
+}
+
+int ffg_density_matrices_async(int32_t batch, const double* const* H, int64_t n, const double* mu,
+                               const double* kT, const ffg_model* model, int32_t mode_api,
+                               double* const* D_out, int64_t* ticket) {
+    int rc, dev, mode;
+    if (!H || !ticket) return set_err(FFG_ERR_VALIDATION, "H / ticket is null");
+    if ((rc = validate_host_call(batch, H, n, model, mode_api, &mode, &dev))) return rc;
+    if ((rc = check_mu_kT(batch, mu, kT))) return rc;
+    std::vector<double> alpha, gamma, scale;
+    rescale_coeffs(batch, mu, kT, model, alpha, gamma, scale);
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    int si;
+    if ((rc = submit_host(w, st, batch, H, n, alpha.data(), gamma.data(), scale.data(), mu, kT, model, mode_api,
+                          mode, D_out, &si, true)))
+        return rc;
+    *ticket = w.slot[si].ticket;
+    return FFG_OK;
+}
+
+int ffg_wait(int64_t ticket, double* stats_out, ffg_provenance* prov) {
+    int rc, dev;
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = lib_stream();
+    Workspace& w = *get_ws(dev, st);
+    std::lock_guard<std::mutex> lk(w.mu);
+    for (int k = 0; k < Workspace::kSlots; ++k)
+        if (w.slot[k].busy && w.slot[k].ticket == ticket) return finish_host(w, k, stats_out, prov);
+    return set_err(FFG_ERR_VALIDATION, "ffg_wait: unknown or already completed ticket %lld", (long long)ticket);
 }
 
 int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, const double* mu,

@@ -120,7 +120,8 @@ SYMBOLS = ("ffg_abi_version", "ffg_last_error", "ffg_device_available", "ffg_in_
            "ffg_density_matrix", "ffg_density_matrices", "ffg_density_matrices_dev",
            "ffg_kernel_launches", "ffg_profile_layers", "ffg_profile_read",
            "ffg_profile_read_ex", "ffg_pair_table", "ffg_release_workspaces",
-           "ffg_entropy_trace", "ffg_expectation", "ffg_solve_chemical_potential")
+           "ffg_entropy_trace", "ffg_expectation", "ffg_solve_chemical_potential",
+           "ffg_density_matrices_async", "ffg_wait")
 
 
 @lru_cache(maxsize=None)
@@ -162,6 +163,10 @@ def lib() -> ctypes.CDLL:
                                                ctypes.c_double, ctypes.POINTER(_Model), ctypes.c_int32,
                                                ctypes.c_double, ctypes.c_int32, _D, _D, _D,
                                                ctypes.POINTER(_MuReport)]
+    L.ffg_density_matrices_async.argtypes = [ctypes.c_int32, ctypes.POINTER(_D), ctypes.c_int64, _D, _D,
+                                             ctypes.POINTER(_Model), ctypes.c_int32, ctypes.POINTER(_D),
+                                             ctypes.POINTER(ctypes.c_int64)]
+    L.ffg_wait.argtypes = [ctypes.c_int64, _D, ctypes.POINTER(_Prov)]
     L.ffg_pair_table.restype = ctypes.c_int32
     L.ffg_pair_table.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32]
     L.ffg_release_workspaces.restype = None
@@ -350,6 +355,37 @@ def compute_density_matrices(Hs: Sequence[np.ndarray], mu, kT, model: Mlsp2Model
     _check(lib().ffg_density_matrices(B, Hp, n, _dp(mu), _dp(kT), ctypes.byref(m), int(mode), Dp,
                                       _dp(stats), pv))
     return Ds, [DensityStatistics(*map(float, s)) for s in stats], [Provenance._from(p) for p in pv]
+
+
+class AsyncBatch:
+    """Handle of ffg_density_matrices_async: results land in the caller's D buffers; wait()
+    returns (stats, provenance) and raises the batch's first error."""
+
+    def __init__(self, ticket, B, keep):
+        self.ticket, self.B, self._keep = ticket, B, keep
+
+    def wait(self):
+        stats = np.zeros((self.B, 2))
+        pv = (_Prov * self.B)()
+        _check(lib().ffg_wait(self.ticket, _dp(stats), pv))
+        return [DensityStatistics(*map(float, st)) for st in stats], [Provenance._from(p) for p in pv]
+
+
+def compute_density_matrices_async(Hs, mu, kT, model: Mlsp2Model, Ds,
+                                   mode: PrecisionMode = PrecisionMode.MIXED_EMULATED) -> AsyncBatch:
+    """Asynchronous host-buffer batch (at most two in flight): Hs / Ds are lists of C-contiguous
+    float64 arrays (page-locked for transfer overlap) that must stay alive until wait()."""
+    B = len(Hs)
+    n = Hs[0].shape[0]
+    mu = np.ascontiguousarray(np.broadcast_to(np.asarray(mu, dtype=np.float64), (B,)))
+    kT = np.ascontiguousarray(np.broadcast_to(np.asarray(kT, dtype=np.float64), (B,)))
+    Hp = (_D * B)(*[_dp(H) for H in Hs])
+    Dp = (_D * B)(*[_dp(D) for D in Ds])
+    m = model._c()
+    t = ctypes.c_int64()
+    _check(lib().ffg_density_matrices_async(B, Hp, n, _dp(mu), _dp(kT), ctypes.byref(m), int(mode), Dp,
+                                            ctypes.byref(t)))
+    return AsyncBatch(t.value, B, (Hs, Ds, mu, kT, Hp, Dp, m, model))
 
 
 def compute_density_matrices_device(H_dev, mu, kT, model: Mlsp2Model,
