@@ -185,6 +185,8 @@ struct Workspace {
     uint32_t* counters = nullptr;
     size_t cap_cnt = 0;
     uint32_t* pairs = nullptr;
+    uint8_t* xa_used = nullptr;      // [nb][nb] blocks in the pair table's orientation
+    size_t cap_used = 0;
     int pairs_nb = -1, PT = 0;
     size_t cap_pairs = 0;
     double* coef = nullptr;
@@ -239,6 +241,7 @@ void free_ws(Workspace* w) {
     cudaFreeHost(w->host_small);
     cudaFree(w->counters);
     cudaFree(w->pairs);
+    cudaFree(w->xa_used);
     cudaFree(w->coef);
     cudaFreeHost(w->ring);
     if (w->s_h2d) cudaStreamDestroy(w->s_h2d);
@@ -631,6 +634,17 @@ int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L) {
             w.cap_pairs = t.size();
         }
         CK(cudaMemcpy(w.pairs, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+        std::vector<uint8_t> used((size_t)nb * nb, 0);
+        for (uint32_t e : t) {
+            const int a0 = e & 1023, a1 = (e >> 10) & 1023, sp = (e >> 20) & 1023;
+            used[(size_t)a0 * nb + sp] = 1;
+            if (!((e >> 30) & 1)) used[(size_t)a1 * nb + sp] = 1;
+        }
+        if (used.size() > w.cap_used) {
+            if ((rc = grow(&w.xa_used, dummy, used.size()))) return rc;
+            w.cap_used = used.size();
+        }
+        CK(cudaMemcpy(w.xa_used, used.data(), used.size(), cudaMemcpyHostToDevice));
         w.pairs_nb = nb;
         w.PT = (int)t.size();
     }
@@ -717,7 +731,8 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     rp.np = (int)np;
     rp.mode = j.mode;
     rp.write_operands = 1;
-    rescale_gershgorin_kernel<<<dim3((unsigned)(np / 8), (unsigned)B), 256, 0, st>>>(rp);
+    rp.xa_used = pair ? w.xa_used : nullptr;   // the per-layer kernel reads every upper block
+    rescale_tiles_kernel<<<dim3((unsigned)(np / kK1Rows), (unsigned)B), 256, 0, st>>>(rp);
     CK(cudaGetLastError());
 
     const double layer_flops = (double)B * ((j.mode == kModeF32E) ? 3.0 : 1.0) * (double)n * n * (n + 1);

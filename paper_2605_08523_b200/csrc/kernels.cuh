@@ -102,6 +102,16 @@ __device__ __forceinline__ bool half_range_bad(float x) {
     return fabsf(x * kHalfScale) >= kHalfMax;
 }
 
+// X and A live in a tile-interleaved layout: tile (I,J) of matrix m is a contiguous
+// 128x128 fp32 block stored as [32 column-quads][128 rows][4]; element (r, c) of the tile
+// at ((c/4)*128 + r)*4 + c%4.  A warp whose lanes own consecutive rows then reads/writes
+// 512 contiguous bytes per float4 access.
+__host__ __device__ __forceinline__ size_t xa_tile_base(int m, int I, int J, int nb) {
+    return (((size_t)m * nb + I) * nb + J) * (size_t)(kBM * kBN);
+}
+__host__ __device__ __forceinline__ uint32_t xa_off(int r, int c4) {  // float offset of quad c4, row r
+    return ((uint32_t)c4 * kBM + (uint32_t)r) * 4u;
+}
 // ===================================================================================== K1
 struct RescaleParams {
     const double* H;            // [B][n][n] row-major, exactly symmetric
@@ -115,6 +125,7 @@ struct RescaleParams {
     unsigned long long* bounds; // [B][2] ordered keys of (eps_min, eps_max) before widening
     int* flags;                 // [B][2] first bad X_k index: [0] non-finite, [1] half range
     int n, np, mode, write_operands;
+    const uint8_t* xa_used;     // [nb][nb] blocks whose X/A K2 reads (null: all blocks)
 };
 
 // One warp per row; 8 rows per CTA; grid (np/8, B).
@@ -225,6 +236,148 @@ __global__ void __launch_bounds__(256) rescale_gershgorin_kernel(const __grid_co
     }
 }
 
+// K1 (tiled): one CTA = 32 consecutive rows of one matrix (a quarter of block row I), all
+// columns, 128-column tiles.  Each warp streams 4 rows per tile (coalesced double2 loads, 1 KB
+// per row), writes the binary16 split row-major (256 B per row), and stages X0 / A1 in shared
+// memory so that the block-interleaved [c4][row][4] layout is written with 512-byte contiguous
+// runs (the row-per-lane K1 above stored 2 KB apart per lane).  Blocks K2 never reads
+// (xa_used) skip the X/A stores.  Gershgorin radii: fixed-order per-row warp trees.
+constexpr int kK1Rows = 32;
+constexpr int kK1Pad = 132;  // padded fp32 row stride of the staging tiles (conflict-free float4)
+__global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constant__ RescaleParams p) {
+    __shared__ __align__(16) float sX[kK1Rows * kK1Pad];
+    __shared__ __align__(16) float sA[kK1Rows * kK1Pad];
+    __shared__ double s_lo[8], s_hi[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = blockIdx.y;
+    const int n = p.n, np = p.np, nb = np / 128;
+    const int row0 = blockIdx.x * kK1Rows;          // first row of this CTA
+    const int I = row0 / 128, q = (row0 & 127) / kK1Rows;
+    const double alpha = p.alpha[m], gamma = p.gamma[m];
+    const float d0f = (float)p.d0;
+    (void)d0f;
+    double radius[4] = {0.0, 0.0, 0.0, 0.0}, hii[4] = {0.0, 0.0, 0.0, 0.0};
+    bool bad_nf = false, bad_hr = false;
+    for (int J = 0; J < nb; ++J) {
+        const int c0 = J * 128 + 4 * lane;           // this lane's 4 columns
+        double hk[4][4];                              // all four rows' loads in flight together
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = row0 + warp * 4 + k;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hk[k][e] = 0.0;
+            if (i < n) {
+                const double* hrow = p.H + ((size_t)m * n + i) * n;
+                if ((n & 3) == 0 && c0 + 3 < n) {
+                    const double2 v0 = __ldcs(reinterpret_cast<const double2*>(hrow + c0));
+                    const double2 v1 = __ldcs(reinterpret_cast<const double2*>(hrow + c0 + 2));
+                    hk[k][0] = v0.x; hk[k][1] = v0.y; hk[k][2] = v1.x; hk[k][3] = v1.y;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) hk[k][e] = (c0 + e < n) ? hrow[c0 + e] : 0.0;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int rl = warp * 4 + k;              // local row 0..31
+            const int i = row0 + rl;
+            const double* h = hk[k];
+            float x[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int j = c0 + e;
+                if (j == i) hii[k] = h[e]; else radius[k] += fabs(h[e]);
+                double v = alpha * h[e];
+                if (j == i && i < n) v += gamma;
+                x[e] = (float)v;
+                bad_nf |= !isfinite(x[e]);
+            }
+            if (p.write_operands) {
+                float a[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) a[e] = (float)(p.d0 * (double)x[e]);
+                *reinterpret_cast<float4*>(&sX[rl * kK1Pad + 4 * lane]) = make_float4(x[0], x[1], x[2], x[3]);
+                *reinterpret_cast<float4*>(&sA[rl * kK1Pad + 4 * lane]) = make_float4(a[0], a[1], a[2], a[3]);
+                uint16_t hb[4], lb[4];
+                if (p.mode == kModeBF16) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) split16<kModeBF16>(x[e], hb[e], lb[e]);
+                } else if (p.mode == kModeF16) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        split16<kModeF16>(x[e], hb[e], lb[e]);
+                        bad_hr |= half_range_bad<kModeF16>(x[e]);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        split16<kModeF32E>(x[e], hb[e], lb[e]);
+                        bad_hr |= half_range_bad<kModeF32E>(x[e]);
+                    }
+                }
+                const size_t orow = ((size_t)m * np + row0 + rl) * np;
+                uint2 hv, lv;
+                hv.x = hb[0] | ((uint32_t)hb[1] << 16); hv.y = hb[2] | ((uint32_t)hb[3] << 16);
+                lv.x = lb[0] | ((uint32_t)lb[1] << 16); lv.y = lb[2] | ((uint32_t)lb[3] << 16);
+                *reinterpret_cast<uint2*>(p.hi + orow + c0) = hv;
+                if (p.mode == kModeF32E) *reinterpret_cast<uint2*>(p.lo + orow + c0) = lv;
+            }
+        }
+        if (p.write_operands && (!p.xa_used || p.xa_used[I * nb + J])) {
+            __syncthreads();
+            // block (I, J), rows 32q .. 32q+31: [c4][row][4]; thread t -> c4 = t / 8, rows 4(t%8)..+3
+            const size_t tb = xa_tile_base(m, I, J, nb);
+            const int c4 = threadIdx.x >> 3, r4 = (threadIdx.x & 7) * 4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int rl = r4 + k;
+                const float4 xv = *reinterpret_cast<const float4*>(&sX[rl * kK1Pad + 4 * c4]);
+                const float4 av = *reinterpret_cast<const float4*>(&sA[rl * kK1Pad + 4 * c4]);
+                const size_t o = tb + xa_off(q * kK1Rows + rl, c4);
+                *reinterpret_cast<float4*>(p.X + o) = xv;
+                *reinterpret_cast<float4*>(p.A + o) = av;
+            }
+        }
+        __syncthreads();
+    }
+    // per-row Gershgorin intervals (fixed-order warp trees), CTA min/max, ordered-key atomics
+    double rlo = DBL_MAX, rhi = -DBL_MAX;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double r = radius[k], d = hii[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            r += __shfl_xor_sync(0xffffffffu, r, o);
+            d += __shfl_xor_sync(0xffffffffu, d, o);  // exactly one lane holds H_ii
+        }
+        if (row0 + warp * 4 + k < n) {
+            rlo = fmin(rlo, d - r);
+            rhi = fmax(rhi, d + r);
+        }
+    }
+    if (lane == 0) {
+        s_lo[warp] = rlo;
+        s_hi[warp] = rhi;
+    }
+    const bool any_nf = __any_sync(0xffffffffu, bad_nf);
+    const bool any_hr = __any_sync(0xffffffffu, bad_hr);
+    if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], 0);
+    if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], 0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double lo = s_lo[0], hi = s_hi[0];
+        for (int w = 1; w < 8; ++w) {
+            lo = fmin(lo, s_lo[w]);
+            hi = fmax(hi, s_hi[w]);
+        }
+        if (lo <= hi) {
+            atomicMin(&p.bounds[2 * m + 0], ordered_key(lo));
+            atomicMax(&p.bounds[2 * m + 1], ordered_key(hi));
+        }
+    }
+}
+
 // ===================================================================================== K2
 struct LayerParams {
     float* X;             // [B][np][np] in/out (upper tiles)
@@ -260,16 +413,6 @@ struct LayerMaps {
     CUtensorMap hip, lop;    // destination (parity (l+1)&1): 32 x 32 pieces, SW64
 };
 
-// X and A live in a tile-interleaved layout: tile (I,J) of matrix m is a contiguous
-// 128x128 fp32 block stored as [32 column-quads][128 rows][4]; element (r, c) of the tile
-// at ((c/4)*128 + r)*4 + c%4.  A warp whose lanes own consecutive rows then reads/writes
-// 512 contiguous bytes per float4 access.
-__host__ __device__ __forceinline__ size_t xa_tile_base(int m, int I, int J, int nb) {
-    return (((size_t)m * nb + I) * nb + J) * (size_t)(kBM * kBN);
-}
-__host__ __device__ __forceinline__ uint32_t xa_off(int r, int c4) {  // float offset of quad c4, row r
-    return ((uint32_t)c4 * kBM + (uint32_t)r) * 4u;
-}
 // byte offset of 16-byte chunk c of row r in a tile of 64-byte rows, 64B swizzle
 __device__ __forceinline__ uint32_t sw64(uint32_t r, uint32_t c) {
     return r * 64u + ((c ^ ((r >> 1) & 3u)) << 4);
