@@ -867,8 +867,11 @@ __global__ void __launch_bounds__(256) finalize_stats_kernel(const __grid_consta
             xmax = p.mu0 + p.scale[m] * (hi - p.mu[m]);
             if (!(xmin >= 0.0) || !(xmax <= 1.0)) st = 2;  // FFG_ERR_OUT_OF_REGION
         }
-        if (st == 0 && p.flags[2 * m + 0] != INT_MAX) st = 3;  // FFG_ERR_DIVERGED
-        if (st == 0 && p.flags[2 * m + 1] != INT_MAX) st = 4;  // FFG_ERR_HALF_RANGE
+        // the earlier event wins (a binary16 split overflow at X_k precedes a non-finite X_{k+1});
+        // a non-finite X_k also overflows its split, so ties report divergence
+        const int nf = p.flags[2 * m + 0], hr = p.flags[2 * m + 1];
+        if (st == 0 && nf != INT_MAX && nf <= hr) st = 3;       // FFG_ERR_DIVERGED
+        if (st == 0 && hr != INT_MAX) st = 4;                    // FFG_ERR_HALF_RANGE
         p.status[m] = st;
         p.bounds_out[4 * m + 0] = lo;
         p.bounds_out[4 * m + 1] = hi;

@@ -369,3 +369,55 @@ def test_async_host_path_matches_sync(model):
     assert all(p.status == 0 for p in pv1 + pv2)
     with pytest.raises(E.ValidationError, match="ticket"):
         h1.wait()
+
+
+def test_nonfinite_input_reports_layer_zero(model):
+    """A NaN entry of H is a non-finite X_0: DivergedEvaluationError naming layer 0
+    (trainer.hpp:20-25 semantics: first non-finite intermediate)."""
+    H = tight_binding(128, seed=4)
+    H[5, 7] = H[7, 5] = np.nan
+    with pytest.raises(E.DivergedEvaluationError, match="layer 0") as ei:
+        E.compute_density_matrix(H, 0.0, 0.01, model)
+    assert ei.value.layer == 0
+
+
+def test_half_range_error(model):
+    """apply_model on H0 with X_0 = I - H0 outside the binary16 range of the 2^14-scaled split
+    (|X| >= 65504 / 2^14) raises HalfRangeError (half_precision.hpp:13-16); BF16 has no such
+    limit."""
+    H0 = np.diag([-5.0, 0.5, 0.25])
+    with pytest.raises(E.HalfRangeError):
+        E.apply_model(H0, model, E.PrecisionMode.MIXED_EMULATED)
+    with pytest.raises(E.HalfRangeError):
+        E.apply_model(H0, model, E.PrecisionMode.FP16)
+
+
+def test_batch_statuses_are_per_matrix(model):
+    """One out-of-region member does not poison the batch: the device path reports a status per
+    matrix and the in-region members are unchanged; the host path names the failing member."""
+    import torch
+    B, n = 4, 256
+    Hs = [tight_binding(n, seed=30 + k) for k in range(B)]
+    mu = np.zeros(B)
+    kT = np.array([0.01, 0.0005, 0.01, 0.01])    # member 1: beta' far above beta0
+    H_dev = torch.from_numpy(np.stack(Hs)).cuda()
+    D_dev = torch.empty_like(H_dev)
+    stats, status, bounds = E.compute_density_matrices_device(H_dev, mu, kT, model, D_dev=D_dev)
+    torch.cuda.synchronize()
+    assert status.cpu().tolist() == [0, E.OutOfRegionError.status, 0, 0]
+    ok, _, _ = E.compute_density_matrices([Hs[k] for k in (0, 2, 3)], mu[[0, 2, 3]], kT[[0, 2, 3]], model)
+    Dd = D_dev.cpu().numpy()
+    for k, j in zip((0, 2, 3), range(3)):
+        assert np.array_equal(Dd[k], ok[j])
+    with pytest.raises(E.OutOfRegionError, match="matrix 1"):
+        E.compute_density_matrices(Hs, mu, kT, model)
+
+
+def test_bitwise_deterministic(model):
+    """Fixed-order reductions: repeated runs are bit-identical, in
+    every mode, for D and the statistics."""
+    H = tight_binding(512, seed=77)
+    for mode in (E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16):
+        D1, s1, _ = E.compute_density_matrix(H, 0.02, 0.011, model, mode)
+        D2, s2, _ = E.compute_density_matrix(H, 0.02, 0.011, model, mode)
+        assert np.array_equal(D1, D2) and s1 == s2
