@@ -237,6 +237,80 @@ __device__ __forceinline__ void epi_sub_mid(const uint32_t (&v)[16], float* Xt, 
     }
 }
 
+// FFG_A_RED: A' = A + d'X' as a fire-and-forget vector reduction at L2 (no read of A, no round
+// trip; every element receives exactly one add per layer, so the result is deterministic).  The
+// sum d'X' is formed in fp32 from the hi/lo coefficient (one more rounding than acc_step's fused
+// form; both ~1 ulp).
+__device__ __forceinline__ void red_add_v4(float* gp, float a, float b, float c, float d) {
+    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gp), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ float acc_term(float x, const EpiCoef& k) { return fmaf(k.d_hi, x, k.d_lo * x); }
+
+// X of 16 columns (c0 .. c0+15) of row r
+__device__ __forceinline__ void epi_loadx16(const float* Xt, int r, int c0, float4 (&xq)[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
+}
+
+// epi_sub_mid with X already in registers and A updated by reduction (FFG_A_RED)
+template <int MODE, bool DIAG>
+__device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const float4 (&xq)[4], float* Xt, float* At,
+                                                int r, int c0, int lane, int sub, bool c_on, const EpiCoef& k,
+                                                uint32_t stg_d, bool dblk, EpiHealth& hl) {
+    using Tr = ModeTraits<MODE>;
+    uint32_t hp[8], lp[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
+        float ts[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float y = __uint_as_float(v[4 * j + e]);
+            float xn;
+            if constexpr (DIAG) {
+                const int cl = c0 + 4 * j + e;
+                xn = (cl == r && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
+                if (cl >= r) hl.add(xn);
+            } else {
+                xn = poly_step<false>(y, xs[e], k);
+                hl.add(xn);
+            }
+            ts[e] = acc_term(xn, k);
+            xs[e] = xn;
+        }
+        __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
+        red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
+    }
+    if (!dblk) {
+        sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
+        sts_v4(stg_d + sw64(lane, 2 * sub + 1), hp[4], hp[5], hp[6], hp[7]);
+        if (Tr::kHasLo) {
+            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 0), lp[0], lp[1], lp[2], lp[3]);
+            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 1), lp[4], lp[5], lp[6], lp[7]);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const uint32_t col = 16 * sub + e;
+            if ((int)col < lane) continue;
+            const uint16_t hb = (uint16_t)(hp[e >> 1] >> (16 * (e & 1)));
+            const uint16_t lb = (uint16_t)(lp[e >> 1] >> (16 * (e & 1)));
+            const uint32_t off = sw64(col, lane >> 3) + (lane & 7) * 2;
+            const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
+            sts_u16(stg_d + off, hb);
+            sts_u16(stg_d + doff, hb);
+            if (Tr::kHasLo) {
+                sts_u16(stg_d + kPieceBytes + off, lb);
+                sts_u16(stg_d + kPieceBytes + doff, lb);
+            }
+        }
+    }
+}
+
 // X/A of 16 columns (c0 .. c0+15) of row r: four float4 each.
 __device__ __forceinline__ void epi_load16(const float* Xt, const float* At, int r, int c0, float4 (&xq)[4],
                                            float4 (&aq)[4]) {
@@ -325,6 +399,107 @@ __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const floa
             const float y = __uint_as_float(v[4 * j + e]);
             const bool dg = DIAG && cl == r;
             const float xn = (dg && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
+            const bool own = !DIAG || cl >= r;
+            if (own) hl.add(xn);
+            if (own && gi < n && gj < n) {
+                const double dv = (double)as[e] + (double)xn;
+                if (Dm) {
+                    Dm[(size_t)gi * n + gj] = dv;
+                    if (!dg) Dm[(size_t)gj * n + gi] = dv;
+                }
+                if (dg) {
+                    tr += dv;
+                    sq += dv * dv;
+                } else {
+                    sq += 2.0 * dv * dv;
+                }
+            }
+        }
+    }
+}
+
+
+// Eight columns (c0..c0+7, c0 a multiple of 8) of row r from Y values already in registers
+// (two-group workers): X/A in place, hi/lo into the 16-byte chunk (c0 & 31) / 8 of the warp's
+// direct 32x32 pieces (hi at stg, lo at stg + kPieceBytes); dblk: symmetric completion of a
+// diagonal piece in place.
+template <int MODE, bool DIAG>
+__device__ __forceinline__ void epi_oct_mid_y(const float (&y)[8], float* Xt, float* At, int r, int c0, int lane,
+                                              bool c_on, const EpiCoef& k, uint32_t stg, bool dblk,
+                                              EpiHealth& hl) {
+    using Tr = ModeTraits<MODE>;
+    float4 xq[2], aq[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
+        aq[j] = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
+    }
+    uint32_t hp[4], lp[4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
+        float as[4] = {aq[j].x, aq[j].y, aq[j].z, aq[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float xn;
+            if constexpr (DIAG) {
+                const int cl = c0 + 4 * j + e;
+                xn = (cl == r && c_on) ? poly_step<true>(y[4 * j + e], xs[e], k)
+                                       : poly_step<false>(y[4 * j + e], xs[e], k);
+                if (cl >= r) hl.add(xn);
+            } else {
+                xn = poly_step<false>(y[4 * j + e], xs[e], k);
+                hl.add(xn);
+            }
+            as[e] = acc_step(as[e], xn, k);
+            xs[e] = xn;
+        }
+        __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
+        __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
+    }
+    const int ch = (c0 & 31) >> 3;
+    if (!dblk) {
+        sts_v4(stg + sw64(lane, ch), hp[0], hp[1], hp[2], hp[3]);
+        if (Tr::kHasLo) sts_v4(stg + kPieceBytes + sw64(lane, ch), lp[0], lp[1], lp[2], lp[3]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t col = 8 * ch + e;
+            if ((int)col < lane) continue;
+            const uint16_t hb = (uint16_t)(hp[e >> 1] >> (16 * (e & 1)));
+            const uint16_t lb = (uint16_t)(lp[e >> 1] >> (16 * (e & 1)));
+            const uint32_t off = sw64(col, lane >> 3) + (lane & 7) * 2;
+            const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
+            sts_u16(stg + off, hb);
+            sts_u16(stg + doff, hb);
+            if (Tr::kHasLo) {
+                sts_u16(stg + kPieceBytes + off, lb);
+                sts_u16(stg + kPieceBytes + doff, lb);
+            }
+        }
+    }
+}
+
+// Last layer from register Y: D = A + X_L (fp64) and the owned elements' statistics; 8 columns.
+template <bool DIAG>
+__device__ __forceinline__ void epi_oct_last_y(const float (&y)[8], const float* Xt, const float* At, int r,
+                                               int c0, int gi, int gj0, int n, bool c_on, const EpiCoef& k,
+                                               double* Dm, EpiHealth& hl, double& tr, double& sq) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const float4 xq = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
+        const float4 aq = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
+        const float xs[4] = {xq.x, xq.y, xq.z, xq.w};
+        const float as[4] = {aq.x, aq.y, aq.z, aq.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int cl = c0 + 4 * j + e;
+            const int gj = gj0 + cl;
+            const bool dg = DIAG && cl == r;
+            const float xn = (dg && c_on) ? poly_step<true>(y[4 * j + e], xs[e], k)
+                                          : poly_step<false>(y[4 * j + e], xs[e], k);
             const bool own = !DIAG || cl >= r;
             if (own) hl.add(xn);
             if (own && gi < n && gj < n) {

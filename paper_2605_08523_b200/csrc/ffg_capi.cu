@@ -438,6 +438,15 @@ int exact_drain_layers() {
     return v;
 }
 
+// Layers after the exact ones that drain every 2 K16 steps (default 0: measurement knob)
+int semi_drain_layers() {
+    static int v = [] {
+        const char* e = getenv("FFG_SEMI_DRAIN_LAYERS");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 int debug_flags() {
     static int v = [] {
         const char* e = getenv("FFG_DEBUG_K2");
@@ -549,11 +558,11 @@ int pair_capacity(int* out) {
     static int max_pairs = -1;
     if (max_pairs < 0) {
         CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                PairCfg<MODE>::kSmem));
+                                PairCfg<MODE, RES>::kSmem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * (num_sms() / 2));
         cfg.blockDim = dim3(kPairThreads);
-        cfg.dynamicSmemBytes = PairCfg<MODE>::kSmem;
+        cfg.dynamicSmemBytes = PairCfg<MODE, RES>::kSmem;
         int nc = 0;
         CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_pair_kernel<MODE, RES>, &cfg));
         if (nc < 1) return set_err(FFG_ERR_CUDA, "pair kernel: no co-resident CTA pair fits");
@@ -572,7 +581,7 @@ int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaS
     // pair item of a layer (each keeps its block for all layers), `items` = pairs per layer
     if (RES && items > cap) return set_err(FFG_ERR_CUDA, "resident K2: %lld pairs > %d resident", (long long)items, cap);
     const int pairs = (int)std::min<int64_t>(cap, items);
-    mlsp2_pair_kernel<MODE, RES><<<2 * pairs, kPairThreads, PairCfg<MODE>::kSmem, st>>>(maps, pp);
+    mlsp2_pair_kernel<MODE, RES><<<2 * pairs, kPairThreads, PairCfg<MODE, RES>::kSmem, st>>>(maps, pp);
     CK(cudaGetLastError());
     return FFG_OK;
 }
@@ -759,6 +768,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         pp.l1 = md.n_layers;
         pp.n_layers = md.n_layers;
         pp.exact_layers = exact_drain_layers();
+        pp.semi_layers = semi_drain_layers();
         pp.dbg = debug_flags();
         if (pp.dbg & 8) {
             static unsigned long long* prof = nullptr;

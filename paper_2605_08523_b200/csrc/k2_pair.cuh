@@ -28,6 +28,8 @@
 // Accumulation precision: hi*hi is drained after every MMA for the first
 // `exact_layers` layers and after every K-block afterwards; hi*lo + lo*hi accumulate apart.
 #pragma once
+#include <type_traits>
+
 #include "epilogue.cuh"
 
 namespace ffg {
@@ -38,12 +40,23 @@ constexpr int kPairThreads = 640;
 #ifndef FFG_DRAIN_BATCH
 #define FFG_DRAIN_BATCH 2  // x16 TMEM loads in flight per drain wait (1 or 2; measured: 2)
 #endif
-#if FFG_DRAIN_BATCH > 1
+#if defined(FFG_P_CTL)
+constexpr int kPRegsCtl = FFG_P_CTL, kPRegsDrain = FFG_P_DRAIN, kPRegsEpi = FFG_P_EPI;
+#elif FFG_DRAIN_BATCH > 1
 constexpr int kPRegsCtl = 48, kPRegsDrain = 104, kPRegsEpi = 112;
 #else
 constexpr int kPRegsCtl = 48, kPRegsDrain = 96, kPRegsEpi = 120;
 #endif
 static_assert(128 * kPRegsCtl + 256 * kPRegsDrain + 256 * kPRegsEpi <= 640 * 96, "setmaxnreg budget");
+#ifndef FFG_TWO_GROUPS
+#define FFG_TWO_GROUPS 0  // streaming workers as two drain+epilogue groups on alternate items
+#endif
+#ifndef FFG_G_CTL
+#define FFG_G_CTL 32
+#define FFG_G_WORK 112
+#endif
+constexpr int kGRegsCtl = FFG_G_CTL, kGRegsWork = FFG_G_WORK;
+static_assert(128 * kGRegsCtl + 512 * kGRegsWork <= 640 * 96, "setmaxnreg budget (two groups)");
 // resident variant: 16 worker warps (drain + epilogue) own 32 columns each of the CTA's block
 constexpr int kResWorkers = 16;
 constexpr int kRRegsCtl = 40, kRRegsWork = 104;
@@ -51,18 +64,28 @@ static_assert(128 * kRRegsCtl + 512 * kRRegsWork <= 640 * 96, "setmaxnreg budget
 constexpr int kPairHalf = kBN / 2;                  // B rows supplied by each CTA
 constexpr int kPairOpA = kBM * kBK * 2;             // 16 KB
 constexpr int kPairOpB = kPairHalf * kBK * 2;       // 8 KB
-constexpr int kPairStagingBytes = kEpiWarps2 * 4 * kPieceBytes;  // 64 KB
+#ifndef FFG_STAGING_INPLACE
+#define FFG_STAGING_INPLACE 0  // epilogue staging: direct pieces only, mirrors transposed in place
+#endif
+constexpr int kStgPieces = FFG_STAGING_INPLACE ? 2 : 4;  // 2 KB pieces per epilogue warp
+constexpr int kPairStagingBytes = kEpiWarps2 * kStgPieces * kPieceBytes;  // 32 or 64 KB
 
-template <int MODE>
+// staging: 64 KB for the resident / two-group workers (16 warps x 4 KB) and the 4-piece
+// epilogue; 32 KB with in-place mirrors, which buys an extra operand stage (two for BF16)
+template <int MODE, bool RES = false>
 struct PairCfg {
+    static constexpr bool kWide = RES || FFG_TWO_GROUPS || !FFG_STAGING_INPLACE;
+    static constexpr int kStagingBytes = kWide ? kEpiWarps2 * 4 * kPieceBytes : kPairStagingBytes;
     static constexpr int kStageBytes = ModeTraits<MODE>::kHasLo ? 2 * (kPairOpA + kPairOpB)
                                                                 : (kPairOpA + kPairOpB);
-    static constexpr int kStages = ModeTraits<MODE>::kHasLo ? 3 : 6;
+    static constexpr int kStages = (ModeTraits<MODE>::kHasLo ? 3 : 6) + (kWide ? 0 : (ModeTraits<MODE>::kHasLo ? 1 : 2));
     static constexpr int kStagingOff = kStages * kStageBytes;
-    static constexpr int kBarOff = kStagingOff + kPairStagingBytes;
+    static constexpr int kBarOff = kStagingOff + kStagingBytes;
     static constexpr int kSmem = kBarOff + 1024 + 1024;  // barriers/scratch + alignment slack
 };
 static_assert(PairCfg<kModeF32E>::kSmem <= 227 * 1024, "pair kernel smem");
+static_assert(PairCfg<kModeF32E, true>::kSmem <= 227 * 1024, "pair kernel smem");
+static_assert(PairCfg<kModeBF16, true>::kSmem <= 227 * 1024, "pair kernel smem");
 static_assert(PairCfg<kModeBF16>::kSmem <= 227 * 1024, "pair kernel smem");
 static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue warps alike");
 
@@ -72,6 +95,12 @@ static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue war
 // accumulate per K16 step into a chunk-sized partial (accumulation precision);
 // single-product modes: the whole K extent.  The drain warps sum chunks in registers with
 // round-to-nearest adds and write Y into the item's LAST slot, which the epilogue frees.
+#ifndef FFG_WARP_PUBLISH
+#define FFG_WARP_PUBLISH 0  // every epilogue warp publishes its part of a block (no block barrier)
+#endif
+#ifndef FFG_A_RED
+#define FFG_A_RED 1  // epilogue: A += d'X' by L2 vector reduction; X prefetched one sub-block ahead
+#endif
 #ifndef FFG_EPI_PREFETCH
 #define FFG_EPI_PREFETCH 0  // epilogue loads sub-block 1's X/A before computing sub-block 0
 #endif
@@ -87,11 +116,22 @@ static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue war
 #ifndef FFG_DRAIN_SPIN
 #define FFG_DRAIN_SPIN 1  // drain warps spin on slot_full (measured faster than sleeping)
 #endif
+#ifndef FFG_DRAIN_DEP
+#define FFG_DRAIN_DEP 1  // order drain batches (see the drain loop)
+#endif
 #ifndef FFG_EXACT_K16
 #define FFG_EXACT_K16 1  // K16 steps per chunk in exact-drain layers (1 or 2)
 #endif
 __host__ __device__ constexpr int pair_chunks(int mode, int nk, bool exact) {
     return mode == kModeF32E ? (exact ? nk * (kBK / kUK) / FFG_EXACT_K16 : nk) : 1;
+}
+// K16 steps per chunk of layer l: FFG_EXACT_K16 in the exact-drain layers, 2 in the following
+// `semi_layers`, a whole K-block (4) after that
+__host__ __device__ constexpr int layer_kstep(int l, int exact_layers, int semi_layers) {
+    return l < exact_layers ? FFG_EXACT_K16 : (l < exact_layers + semi_layers ? 2 : kBK / kUK);
+}
+__host__ __device__ constexpr int layer_chunks(int mode, int nk, int kstep) {
+    return mode == kModeF32E ? nk * (kBK / kUK) / kstep : 1;
 }
 
 struct PairMaps {
@@ -113,6 +153,7 @@ struct PairParams {
     int B, G;                 // matrices, group size
     int l0, l1, n_layers;     // layers of this launch, model depth
     int exact_layers;
+    int semi_layers;          // layers after the exact ones draining every 2 K16 steps
     int dbg;                  // measurement only: 1 skip epilogue math, 2 skip loads/MMAs,
                               // 4 skip dependency waits, 8 per-role wait cycles -> prof,
                               // 16 skip operand loads, 32 skip hi/lo stores, 64 skip X/A
@@ -121,6 +162,7 @@ struct PairParams {
     int m0;                   // first matrix of this launch (resident groups)
     uint16_t* hi[2];          // hi/lo parity buffers [B][np][np] (resident epilogue stores)
     uint16_t* lo[2];
+    uint32_t zero;            // always 0: an opaque operand for scheduling dependencies (drain)
 };
 
 __device__ __forceinline__ void pair_decode(const PairParams& p, int item, int& m, int& l, int& pi) {
@@ -205,7 +247,7 @@ __device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t t
     for (int item = pair_id; item < total; item += n_pairs) {
         const int l = l_first + (item - pair_id) / n_pairs;
         const bool last = (l == p.n_layers - 1);
-        const int chunks = (p.dbg & 2) ? 1 : pair_chunks(MODE, nk, l < p.exact_layers);
+        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
         int ysl = 0;
         {
             float yacc[32];
@@ -392,6 +434,186 @@ __device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t t
     }
 }
 
+// Two-group streaming workers (FFG_TWO_GROUPS): warps 4-19 form two groups of 8 that take
+// alternate items of this CTA pair.  A group drains the item's chunks into REGISTER sums (each
+// TMEM slot is released as soon as it is read, so all four slots keep rotating) and then runs
+// the epilogue straight from those registers, while the other group drains the next item: two
+// epilogues are in flight per CTA.  Warp w of a group: TMEM lane quarter q = w & 3 (rows
+// 32q..32q+31), column half h (columns 64h..64h+63, quarters 2h and 2h + 1); thread = one row.
+template <int MODE>
+__device__ __forceinline__ void two_group_workers(const PairMaps& tm, const PairParams& p, uint32_t tmem,
+                                                  int warp, int lane, uint32_t rank, int pair_id,
+                                                  int n_pairs, int total, int nk, uint64_t* slot_full,
+                                                  uint64_t* slot_empty, uint64_t* hand, uint8_t* staging,
+                                                  double* red) {
+    using Tr = ModeTraits<MODE>;
+    const int wk = warp - 4, grp = wk >> 3, wq = wk & 7;
+    const int q = warp & 3, h = wq >> 2;
+    const int r = q * 32 + lane;
+    const int nb = p.nb, n = p.n, np = p.np;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + 64 * h;  // + slot * 128
+    const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
+    const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
+    uint8_t* stg = staging + wk * 2 * kPieceBytes;  // direct hi piece, lo piece (mirrors in place)
+    const uint32_t stg_a = smem_u32(stg);
+    double* gred = red + 16 * grp;
+    int g = 0, u = 0;
+    for (int item = pair_id; item < total; item += n_pairs, ++u) {
+        int m, l, pi;
+        pair_decode(p, item, m, l, pi);
+        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
+        if ((u & 1) != grp) {
+            g += chunks;
+            continue;
+        }
+        // the other group has seen every chunk of the previous item: slot_full phases are then
+        // at most one ahead of this group's waits (no parity aliasing)
+        if (u > 0) mbar_wait(&hand[grp ^ 1], ((u - 1) >> 1) & 1);
+        float yacc[64];
+#pragma unroll
+        for (int e = 0; e < 64; ++e) yacc[e] = 0.0f;
+#pragma unroll 1
+        for (int f = 0; f < chunks; ++f, ++g) {
+            const int sl = g & 3;
+            mbar_wait(&slot_full[sl], (g >> 2) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int ch = 0; ch < 4; ch += 2) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x16(tl + sl * 128 + ch * 16, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                tmem_ld_32x32b_x16(tl + sl * 128 + ch * 16 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                tmem_ld_wait();
+                if (ch == 2) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
+                }
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    const float2 acc = add_f32x2(make_float2(yacc[16 * ch + e], yacc[16 * ch + e + 1]),
+                                                 make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+                    yacc[16 * ch + e] = acc.x;
+                    yacc[16 * ch + e + 1] = acc.y;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hand[grp]);
+        // ------------------------------------------------------------- epilogue of the item
+        const uint32_t pr = __ldg(p.pairs + pi);
+        const int R = rank ? (pr >> 10) & 1023 : pr & 1023;
+        const int C = (pr >> 20) & 1023;
+        const bool dummy = rank && ((pr >> 30) & 1);
+        const bool last = (l == p.n_layers - 1);
+        const bool diag = R == C;
+        const int gi = R * kBM + r;
+        const bool c_on = gi < n;
+        const EpiCoef k = load_coef(p.coef, l, last);
+        const int nxt = (l + 1) & 1;
+        float* Xt = p.X + xa_tile_base(m, R, C, nb);
+        float* At = p.A + xa_tile_base(m, R, C, nb);
+        double* Dm = (last && p.D) ? p.D + (size_t)m * n * n : nullptr;
+        EpiHealth hl;
+        double tr = 0.0, sq = 0.0;
+#pragma unroll
+        for (int qi = 0; qi < 2; ++qi) {
+            const int qc = 2 * h + qi;  // column quarter (32 columns)
+            if (dummy || (p.dbg & 1) || (diag && qc < q)) continue;
+            const bool dblk = diag && qc == q;
+            if (!last) {
+                if (lane == 0) tma_store_wait_read();  // the staging pieces are free again
+                __syncwarp();
+            }
+#pragma unroll
+            for (int rd = 0; rd < 4; ++rd) {
+                const int c0 = 32 * qc + 8 * rd;
+                float y[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) y[e] = yacc[32 * qi + 8 * rd + e] * inv_s2;
+                if (!last) {
+                    if (diag)
+                        epi_oct_mid_y<MODE, true>(y, Xt, At, r, c0, lane, c_on, k, stg_a, dblk, hl);
+                    else
+                        epi_oct_mid_y<MODE, false>(y, Xt, At, r, c0, lane, c_on, k, stg_a, false, hl);
+                } else {
+                    if (diag)
+                        epi_oct_last_y<true>(y, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                    else
+                        epi_oct_last_y<false>(y, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                }
+            }
+            if (!last && !(p.dbg & 32)) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    const int prow = m * np + R * kBM + 32 * q;  // direct piece origin
+                    const int pcol = C * kBN + 32 * qc;
+                    tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
+                    if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
+                    tma_store_commit();
+                }
+                if (!dblk) {  // mirrored pieces: transpose the direct pieces in place once read
+                    if (lane == 0) tma_store_wait_read();
+                    __syncwarp();
+                    transpose_piece_inplace(stg_a, lane);
+                    if (Tr::kHasLo) transpose_piece_inplace(stg_a + kPieceBytes, lane);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int mrow = m * np + C * kBN + 32 * qc;
+                        const int mcol = R * kBM + 32 * q;
+                        tma_store_2d(&tm.p_hi[nxt], stg, mcol, mrow);
+                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, mcol, mrow);
+                        tma_store_commit();
+                    }
+                }
+            }
+        }
+        if (!dummy) {
+            const bool any_nf = __any_sync(0xffffffffu, hl.nonfinite());
+            const bool any_hr = !last && __any_sync(0xffffffffu, hl.template half_range<MODE>());
+            if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], l + 1);
+            if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], l + 1);
+        }
+        if (last) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                tr += __shfl_xor_sync(0xffffffffu, tr, o);
+                sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            }
+            named_bar_sync(3 + grp, 8 * 32);  // the group's previous partial consumed
+            if (lane == 0) {
+                gred[2 * wq + 0] = tr;
+                gred[2 * wq + 1] = sq;
+            }
+            named_bar_sync(3 + grp, 8 * 32);
+            if (wq == 0 && lane == 0) {
+                double T0 = 0.0, T1 = 0.0;
+                for (int w = 0; w < 8; ++w) {  // fixed order
+                    T0 += gred[2 * w + 0];
+                    T1 += gred[2 * w + 1];
+                }
+                p.partials[(size_t)m * 2 * p.PT + 2 * pi + rank] = make_double2(T0, T1);
+            }
+        } else if (!dummy && l + 1 < p.l1) {
+            // publish the block: hi/lo stores landed, X/A stores visible -> panel counters
+            if (lane == 0) {
+                tma_store_wait_all();
+                fence_proxy_async_global();
+            }
+            __syncwarp();
+            named_bar_sync(5 + grp, 8 * 32);
+            if (wq == 0 && lane == 0) {
+                __threadfence();
+                uint32_t* cm = p.counters + (size_t)m * nb;
+                red_release_gpu_add(cm + R, 1u);
+                if (C != R) red_release_gpu_add(cm + C, 1u);
+            }
+        }
+    }
+    if (lane == 0) tma_store_wait_all();
+}
+
 // dbg & 8: accumulate the cycles a role spends in a wait into a register counter
 #define FFG_TIMED(acc, stmt)                                     \
     do {                                                         \
@@ -404,12 +626,25 @@ __device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t t
         }                                                        \
     } while (0)
 
+// the drain warps run at the edge of their register budget: their wait timing (two registers
+// across the chunk loop) is compiled in only with FFG_ROLE_PROF
+#ifndef FFG_ROLE_PROF
+#define FFG_ROLE_PROF 0
+#endif
+#if FFG_ROLE_PROF
+#define FFG_TIMED_DRAIN(acc, stmt) FFG_TIMED(acc, stmt)
+#else
+#define FFG_TIMED_DRAIN(acc, stmt) stmt
+#endif
+
 template <int MODE, bool RES = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     mlsp2_pair_kernel(const __grid_constant__ PairMaps tm, const __grid_constant__ PairParams p) {
     constexpr int kSlots = RES ? 3 : 4;  // TMEM chunk ring (resident: slot 3 holds the X block)
+    // panel-counter increments per published block (per-warp publication: one per epilogue warp)
+    constexpr uint32_t kPub = (!RES && !FFG_TWO_GROUPS && FFG_WARP_PUBLISH) ? kEpiWarps2 : 1;
     using Tr = ModeTraits<MODE>;
-    using Cfg = PairCfg<MODE>;
+    using Cfg = PairCfg<MODE, RES>;
     constexpr bool kDrain = Tr::kProducts == 3;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -420,9 +655,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     uint64_t* empty = bars + S;            // [S]  both: stage consumed (multicast commit)
     uint64_t* slot_full = bars + 2 * S;    // [4]  both: chunk accumulated in TMEM slot
     uint64_t* slot_empty = bars + 2 * S + 4;  // [4] leader: slot read by both CTAs
-    uint64_t* y_full = bars + 2 * S + 8;   // [4]  local: Y formed in this slot (last chunk)
+    uint64_t* y_full = bars + 2 * S + 8;   // [4]  local: Y formed in this slot (last chunk);
+                                           //      two groups: [g] = group g drained an item
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 12);
-    double* red = reinterpret_cast<double*>(bars + 2 * S + 14);  // [8][2]
+    double* red = reinterpret_cast<double*>(bars + 2 * S + 14);  // [16][2]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -452,7 +688,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RES ? kRRegsCtl : kPRegsCtl) : "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RES ? kRRegsCtl : (FFG_TWO_GROUPS ? kGRegsCtl : kPRegsCtl)) : "memory");
         if (warp == 0 && lane == 0) {
             // ================================================= TMA producer (both CTAs)
             for (int i = 0; i < 2; ++i) {
@@ -475,7 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 const bool dummy = (pr >> 30) & 1;
                 const int ap = rank ? a1 : a0;
                 if (l > p.l0 && !(p.dbg & 4)) {
-                    const uint32_t need = (uint32_t)(nb * (l - p.l0));
+                    const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
                     const uint32_t* cm = p.counters + (size_t)m * nb;
                     const long long t0 = clock64();
                     while (ld_acquire_gpu(cm + ap) < need && (FFG_DEP_BACKOFF ? (__nanosleep(FFG_DEP_BACKOFF), 1) : 1))
@@ -546,7 +782,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             for (int item = pair_id; item < total; item += n_pairs) {
                 int m, l, pi;
                 pair_decode(p, item, m, l, pi);
-                const bool exact = l < p.exact_layers;
+                const int kst = layer_kstep(l, p.exact_layers, p.semi_layers);
+                const bool exact = kst < kBK / kUK;
                 uint32_t t_slot = 0;
                 auto open_slot = [&]() {
                     const int sl = g % kSlots;
@@ -576,25 +813,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                             __syncwarp();
                         }
                     } else if (exact) {
+                        auto issue = [&](auto kc) {
+                            constexpr int KST = decltype(kc)::value;
 #pragma unroll
-                        for (int k0 = 0; k0 < kBK / kUK; k0 += FFG_EXACT_K16) {
-                            open_slot();
-                            if (elect_one_sync()) {
+                            for (int k0 = 0; k0 < kBK / kUK; k0 += KST) {
+                                open_slot();
+                                if (elect_one_sync()) {
 #pragma unroll
-                                for (int kk = k0; kk < k0 + FFG_EXACT_K16; ++kk) {
-                                    const uint32_t koff = kk * kUK * 2;
-                                    umma_f16_pair(t_slot, D(sb, koff), D(sb, offBlo + koff), idesc, kk != k0);
-                                    umma_f16_pair(t_slot, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
+                                    for (int kk = k0; kk < k0 + KST; ++kk) {
+                                        const uint32_t koff = kk * kUK * 2;
+                                        umma_f16_pair(t_slot, D(sb, koff), D(sb, offBlo + koff), idesc, kk != k0);
+                                        umma_f16_pair(t_slot, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
+                                    }
+#pragma unroll
+                                    for (int kk = k0; kk < k0 + KST; ++kk) {
+                                        const uint32_t koff = kk * kUK * 2;
+                                        umma_f16_pair(t_slot, D(sb, koff), D(sb, offBhi + koff), idesc, 1u);
+                                    }
                                 }
-#pragma unroll
-                                for (int kk = k0; kk < k0 + FFG_EXACT_K16; ++kk) {
-                                    const uint32_t koff = kk * kUK * 2;
-                                    umma_f16_pair(t_slot, D(sb, koff), D(sb, offBhi + koff), idesc, 1u);
-                                }
+                                __syncwarp();
+                                close_slot();
                             }
-                            __syncwarp();
-                            close_slot();
-                        }
+                        };
+                        if (kst == FFG_EXACT_K16)
+                            issue(std::integral_constant<int, FFG_EXACT_K16>{});
+                        else
+                            issue(std::integral_constant<int, 2>{});
                     } else {
                         open_slot();
                         if (elect_one_sync()) {
@@ -633,6 +877,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         resident_workers<MODE>(p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk,
                                slot_full, slot_empty, smem + Cfg::kStagingOff,
                                reinterpret_cast<double*>(bars + 2 * S + 14));
+    } else if (FFG_TWO_GROUPS) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kGRegsWork) : "memory");
+        two_group_workers<MODE>(tm, p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk, slot_full,
+                                slot_empty, y_full, smem + Cfg::kStagingOff, red);
     } else if (warp < 4 + kEpiWarps) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsDrain) : "memory");
         // ===================================================== chunk drain -> Y (both CTAs)
@@ -646,7 +894,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int item = pair_id; item < total; item += n_pairs, ++u) {
             int m, l, pi;
             pair_decode(p, item, m, l, pi);
-            const int chunks = (p.dbg & 2) ? 1 : pair_chunks(MODE, nk, l < p.exact_layers);
+            const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
             float yacc[kEpiCols];
 #pragma unroll
             for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
@@ -654,18 +902,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             for (int f = 0; f < chunks; ++f, ++g) {
                 const int sl = g & 3;
                 #if FFG_DRAIN_SPIN
-                FFG_TIMED(w_sf, mbar_wait(&slot_full[sl], (g >> 2) & 1));
+                FFG_TIMED_DRAIN(w_sf, mbar_wait(&slot_full[sl], (g >> 2) & 1));
 #else
-                FFG_TIMED(w_sf, mbar_wait_sleep(&slot_full[sl], (g >> 2) & 1));
+                FFG_TIMED_DRAIN(w_sf, mbar_wait_sleep(&slot_full[sl], (g >> 2) & 1));
 #endif
                 tc_fence_after();
                 const bool lastc = f == chunks - 1;
+                // ptxas hoists TMEM loads above the previous batch's adds, and the extra
+                // registers in flight spill two accumulator pairs (local stores to L2 every
+                // chunk); making each batch's load address depend on the previous batch's last
+                // sum (AND with the runtime zero p.zero) keeps one batch in flight
+                uint32_t dep = 0;
 #pragma unroll
                 for (int ch = 0; ch < 4; ch += FFG_DRAIN_BATCH) {
                     uint32_t v[16 * FFG_DRAIN_BATCH];
 #pragma unroll
                     for (int b = 0; b < FFG_DRAIN_BATCH; ++b)
-                        tmem_ld_32x32b_x16(tlane + sl * 128 + (ch + b) * 16,
+                        tmem_ld_32x32b_x16(tlane + sl * 128 + (ch + b) * 16 + dep,
                                            *reinterpret_cast<uint32_t(*)[16]>(&v[16 * b]));
                     tmem_ld_wait();
                     if (ch + FFG_DRAIN_BATCH == 4 && !lastc) {
@@ -681,6 +934,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         yacc[16 * ch + e] = acc.x;
                         yacc[16 * ch + e + 1] = acc.y;
                     }
+                    if (FFG_DRAIN_DEP)
+                        dep = (__float_as_uint(yacc[16 * ch + 16 * FFG_DRAIN_BATCH - 1]) |
+                               __float_as_uint(yacc[16 * ch])) & p.zero;
                 }
                 if (lastc) {  // Y into this slot for the epilogue (which frees the slot)
 #pragma unroll
@@ -707,7 +963,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int r = q * 32 + lane;       // block row of this thread
         const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
         const int np = p.np, n = p.n;
-        uint8_t* stg = smem + Cfg::kStagingOff + ew * 4 * kPieceBytes;
+        uint8_t* stg = smem + Cfg::kStagingOff + ew * kStgPieces * kPieceBytes;
         const uint32_t stg_a = smem_u32(stg);
         const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
         int g = 0;
@@ -724,7 +980,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const bool last = (l == p.n_layers - 1);
             const EpiCoef k = load_coef(p.coef, l, last);
             const int nxt = (l + 1) & 1;   // hi/lo parity written by this layer
-            g += (p.dbg & 2) ? 1 : pair_chunks(MODE, nk, l < p.exact_layers);
+            g += (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
             const int ysl = (g - 1) & 3;   // slot holding this item's Y
             const bool diag = R == C;
             const int gi = R * kBM + r;
@@ -734,6 +990,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             float* At = p.A + xa_tile_base(m, R, C, nb);
             EpiHealth hl;
             double tr = 0.0, sq = 0.0;
+#if FFG_A_RED
+            // X of this warp's first sub-block is requested before the wait for Y; every
+            // sub-block then requests the next one's X before computing (software pipeline)
+            const bool ok0 = !(dummy || (p.dbg & 1) || (diag && s < q));
+            const bool ok1 = !(dummy || (p.dbg & 1) || (diag && s + 2 < q));
+            float4 xq[4];
+            if (!last && (ok0 || ok1)) {
+                // the block's X of layer l is complete once panel R is (the producer's
+                // dependency wait; the early read must not rely on the wait for Y)
+                if (l > p.l0) {
+                    if (lane == 0) {
+                        const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
+                        while (ld_acquire_gpu(p.counters + (size_t)m * nb + R) < need) {
+                        }
+                    }
+                    __syncwarp();
+                }
+                epi_loadx16(Xt, r, 32 * (ok0 ? s : s + 2), xq);
+            }
+#endif
 #if FFG_EPI_SPIN
             FFG_TIMED(w_y, mbar_wait(&y_full[ysl], (yph >> ysl) & 1));
 #else
@@ -766,7 +1042,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     tmem_ld_32x32b_x16(tacc + c0, v);
                     tmem_ld_wait();
                     if (!last) {
-#if FFG_EPI_PREFETCH
+#if FFG_A_RED
+                        float4 xn[4];
+                        const bool more = sub == 0 || (qi == 0 && ok1);
+                        if (more) epi_loadx16(Xt, r, sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
+                        if (diag)
+                            epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl);
+                        else
+                            epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl);
+                        if (more) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) xq[j] = xn[j];
+                        }
+#elif FFG_EPI_PREFETCH
                         // software pipeline: the next sub-block's X/A are in flight during this one
                         float4 xn[4], an[4];
                         if (sub == 0) epi_load16(Xt, At, r, c0 + 16, xn, an);
@@ -798,7 +1086,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 }
                 const long long t_c1 = (p.dbg & 8) ? clock64() : 0;
                 if (p.dbg & 8) w_cmp += (unsigned long long)(t_c1 - t_c0);
+#if FFG_STAGING_INPLACE
+                if (!last && !(p.dbg & 32)) {
+                    // direct pieces out, then the mirrored pieces transposed in place once the
+                    // direct stores have read the staging
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int prow = m * np + R * kBM + 32 * q;
+                        const int pcol = C * kBN + 32 * qc;
+                        tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
+                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
+                        tma_store_commit();
+                    }
+                    if (!dblk) {
+                        if (lane == 0) tma_store_wait_read();
+                        __syncwarp();
+                        transpose_piece_inplace(stg_a, lane);
+                        if (Tr::kHasLo) transpose_piece_inplace(stg_a + kPieceBytes, lane);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int mrow = m * np + C * kBN + 32 * qc;
+                            const int mcol = R * kBM + 32 * q;
+                            tma_store_2d(&tm.p_hi[nxt], stg, mcol, mrow);
+                            if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, mcol, mrow);
+                        }
+                    }
+                }
+                if (false) {
+#else
                 if (!last) {
+#endif
                     if (!dblk) {  // mirrored pieces: warp transpose of the direct pieces
                         __syncwarp();
                         transpose_piece(stg_a, stg_a + 2 * kPieceBytes, lane);
@@ -861,14 +1180,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     fence_proxy_async_global();
                 }
                 __syncwarp();
+#if FFG_WARP_PUBLISH
+                // per warp: no wait for the block's slowest warp (consumers count 8 per block)
+                if (lane == 0) {
+#else
                 named_bar_sync(4, kEpiWarps2 * 32);
-                if (p.dbg & 8) w_pub += (unsigned long long)(clock64() - tp);
                 if (ew == 0 && lane == 0) {
+#endif
                     __threadfence();
                     uint32_t* cm = p.counters + (size_t)m * nb;
                     red_release_gpu_add(cm + R, 1u);
                     if (C != R) red_release_gpu_add(cm + C, 1u);
                 }
+                if (p.dbg & 8) w_pub += (unsigned long long)(clock64() - tp);
             }
             if (p.dbg & 8) {
                 const long long te = clock64();
