@@ -548,7 +548,11 @@ int group_size(int B, int64_t np, int PT, int resident_pairs, int mode) {
     const double per = (double)np * np * (8.0 * 0.5625 + (mode == kModeF32E ? 8.0 : 4.0));
     const int fit = (int)(budget / per);
     const int fill = (2 * resident_pairs + PT - 1) / PT;
-    return std::max(1, std::min(B, std::max(fit, fill)));
+    const int g = std::max(1, std::min(B, std::max(fit, fill)));
+    // equal groups: a small remainder group would run its layers with most pairs idle and
+    // every item on the dependency chain (measured: 64 x N=512, groups 30+30+4 vs 22+22+20)
+    const int ng = (B + g - 1) / g;
+    return (B + ng - 1) / ng;
 }
 
 // Co-resident CTA pairs of the pair kernel (all pairs must be resident: the layer
