@@ -258,7 +258,7 @@ __device__ __forceinline__ void epi_loadx16(const float* Xt, int r, int c0, floa
 template <int MODE, bool DIAG>
 __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const float4 (&xq)[4], float* Xt, float* At,
                                                 int r, int c0, int lane, int sub, bool c_on, const EpiCoef& k,
-                                                uint32_t stg_d, bool dblk, EpiHealth& hl) {
+                                                uint32_t stg_d, bool dblk, EpiHealth& hl, bool nomem = false) {
     using Tr = ModeTraits<MODE>;
     uint32_t hp[8], lp[8];
 #pragma unroll
@@ -280,8 +280,10 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
             ts[e] = acc_term(xn, k);
             xs[e] = xn;
         }
-        __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
-        red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
+        if (!nomem) {  // (measurement only: dbg & 64)
+            __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
+            red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
+        }
         split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
         split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
     }

@@ -157,7 +157,7 @@ struct PairParams {
     int dbg;                  // measurement only: 1 skip epilogue math, 2 skip loads/MMAs,
                               // 4 skip dependency waits, 8 per-role wait cycles -> prof,
                               // 16 skip operand loads, 32 skip hi/lo stores, 64 skip X/A
-                              // global traffic (all measurement only: results are wrong)
+                              // stores (A: reductions), 128 skip X loads (all measurement only: results are wrong)
     unsigned long long* prof; // [gridDim][16] (dbg & 8)
     int m0;                   // first matrix of this launch (resident groups)
     uint16_t* hi[2];          // hi/lo parity buffers [B][np][np] (resident epilogue stores)
@@ -999,7 +999,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             if (!last && (ok0 || ok1)) {
                 // the block's X of layer l is complete once panel R is (the producer's
                 // dependency wait; the early read must not rely on the wait for Y)
-                if (l > p.l0) {
+                if (l > p.l0 && !(p.dbg & 4)) {
                     if (lane == 0) {
                         const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
                         while (ld_acquire_gpu(p.counters + (size_t)m * nb + R) < need) {
@@ -1007,7 +1007,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     }
                     __syncwarp();
                 }
-                epi_loadx16(Xt, r, 32 * (ok0 ? s : s + 2), xq);
+                if (!(p.dbg & 128)) epi_loadx16(Xt, r, 32 * (ok0 ? s : s + 2), xq);
             }
 #endif
 #if FFG_EPI_SPIN
@@ -1045,11 +1045,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #if FFG_A_RED
                         float4 xn[4];
                         const bool more = sub == 0 || (qi == 0 && ok1);
-                        if (more) epi_loadx16(Xt, r, sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
+                        if (more && !(p.dbg & 128)) epi_loadx16(Xt, r, sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
                         if (diag)
-                            epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl);
+                            epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl, p.dbg & 64);
                         else
-                            epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl);
+                            epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl, p.dbg & 64);
                         if (more) {
 #pragma unroll
                             for (int j = 0; j < 4; ++j) xq[j] = xn[j];
