@@ -95,6 +95,9 @@ static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue war
 // accumulate per K16 step into a chunk-sized partial (accumulation precision);
 // single-product modes: the whole K extent.  The drain warps sum chunks in registers with
 // round-to-nearest adds and write Y into the item's LAST slot, which the epilogue frees.
+#ifndef FFG_BLOCK_DEPS
+#define FFG_BLOCK_DEPS 1  // producer waits per 128-column block when a panel is incomplete (runtime: p.blockdeps)
+#endif
 #ifndef FFG_WARP_PUBLISH
 #define FFG_WARP_PUBLISH 0  // every epilogue warp publishes its part of a block (no block barrier)
 #endif
@@ -147,6 +150,8 @@ struct PairParams {
     double2* partials;        // last layer: [B][2*PT] per block (sum diag, sum sq)
     int* flags;               // [B][2]
     uint32_t* counters;       // [B][nb] panel completion counts (zero at launch)
+    uint32_t* bflags;         // [B][nb][nb] block completion counts, index min*nb+max (FFG_BLOCK_DEPS)
+    int blockdeps;            // 1: producer waits per block while a panel is incomplete (host: G == 1)
     const uint32_t* pairs;    // [PT]  A0 | A1 << 10 | S << 20 | dummy << 30
     const double* coef;       // [n_layers][4] a, b, c, d
     int n, np, nb, PT;
@@ -645,6 +650,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     constexpr uint32_t kPub = (!RES && !FFG_TWO_GROUPS && FFG_WARP_PUBLISH) ? kEpiWarps2 : 1;
     using Tr = ModeTraits<MODE>;
     using Cfg = PairCfg<MODE, RES>;
+    // (FP32-emulated only: a K-block pair there is 1.5K MMA cycles, enough to hide the polls)
+    constexpr bool kBlockDeps = FFG_BLOCK_DEPS && !RES && !FFG_TWO_GROUPS && !FFG_WARP_PUBLISH && Tr::kHasLo;
     constexpr bool kDrain = Tr::kProducts == 3;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -710,7 +717,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 const int a0 = pr & 1023, a1 = (pr >> 10) & 1023, sp = (pr >> 20) & 1023;
                 const bool dummy = (pr >> 30) & 1;
                 const int ap = rank ? a1 : a0;
-                if (l > p.l0 && !(p.dbg & 4)) {
+                // block-granular dependencies: when a panel is not complete yet, each K-block
+                // pair (one 128-column block of panels A_c and S) is waited for just before it is
+                // loaded, so the item's first K-blocks overlap the previous layer's tail
+                bool blockwise = false;
+                if (kBlockDeps && p.blockdeps && l > p.l0 && !(p.dbg & 4)) {
+                    const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
+                    const uint32_t* cm = p.counters + (size_t)m * nb;
+                    blockwise = ld_acquire_gpu(cm + ap) < need || ld_acquire_gpu(cm + sp) < need;
+                    if (!blockwise) fence_proxy_async_global();
+                } else if (l > p.l0 && !(p.dbg & 4)) {
                     const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
                     const uint32_t* cm = p.counters + (size_t)m * nb;
                     const long long t0 = clock64();
@@ -745,6 +761,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 const int rowB = m * p.np + sp * kBN + (int)rank * kPairHalf;
                 for (int kb = 0; kb < ((p.dbg & 2) ? 0 : nk); ++kb, ++it) {
                     const int s = it % S;
+                    if (kBlockDeps && blockwise && (kb & 1) == 0) {
+                        const int blk = kb >> 1;  // 128-column block of this K-block pair
+                        const uint32_t need = (uint32_t)(l - p.l0);
+                        const uint32_t* bf = p.bflags + (size_t)m * nb * nb;
+                        const uint32_t* fa = bf + (ap < blk ? ap * nb + blk : blk * nb + ap);
+                        const uint32_t* fs = bf + (sp < blk ? sp * nb + blk : blk * nb + sp);
+                        const uint32_t* cm = p.counters + (size_t)m * nb;
+                        const uint32_t needp = (uint32_t)(kPub * nb * (l - p.l0));
+                        const long long t0 = clock64();
+                        // the four polls in flight together; complete panels end the blockwise mode
+                        uint32_t va = ld_acquire_gpu(fa), vs = ld_acquire_gpu(fs);
+                        const uint32_t pa = ld_acquire_gpu(cm + ap), ps = ld_acquire_gpu(cm + sp);
+                        if (pa >= needp && ps >= needp) blockwise = false;
+                        while (va < need) {
+                            watchdog_check(t0, 5, ((unsigned long long)item << 32) | (uint32_t)(ap * 1024 + blk), need);
+                            va = ld_acquire_gpu(fa);
+                        }
+                        while (vs < need) {
+                            watchdog_check(t0, 6, ((unsigned long long)item << 32) | (uint32_t)(sp * 1024 + blk), need);
+                            vs = ld_acquire_gpu(fs);
+                        }
+                        if (p.dbg & 8) w_dep += (unsigned long long)(clock64() - t0);
+                        fence_proxy_async_global();
+                    }
                     FFG_TIMED(w_empty, mbar_wait(&empty[s], ((it / S) & 1) ^ 1));
                     const uint32_t fbar = mapa_shared(smem_u32(&full[s]), 0);
                     if (p.dbg & 16) {  // measurement: no operand traffic (MMAs on stale smem);
@@ -938,19 +978,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         dep = (__float_as_uint(yacc[16 * ch + 16 * FFG_DRAIN_BATCH - 1]) |
                                __float_as_uint(yacc[16 * ch])) & p.zero;
                 }
-                if (lastc) {  // Y into this slot for the epilogue (which frees the slot)
+            }
+            {  // Y into the item's last slot for the epilogue (which frees the slot); outside
+               // the chunk loop, so the loop keeps its registers for the sums in flight
+                const int sl = (g - 1) & 3;
 #pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
-                        uint32_t v[16];
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint32_t v[16];
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * ch + e] * inv_s2);
-                        tmem_st_32x32b_x16(tlane + sl * 128 + ch * 16, v);
-                    }
-                    tmem_st_wait();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&y_full[sl]);
+                    for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * ch + e] * inv_s2);
+                    tmem_st_32x32b_x16(tlane + sl * 128 + ch * 16, v);
                 }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&y_full[sl]);
             }
         }
         if ((p.dbg & 8) && warp == 4 && lane == 0) p.prof[(size_t)blockIdx.x * 16 + 5] = w_sf;
@@ -1001,8 +1043,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 // dependency wait; the early read must not rely on the wait for Y)
                 if (l > p.l0 && !(p.dbg & 4)) {
                     if (lane == 0) {
-                        const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
-                        while (ld_acquire_gpu(p.counters + (size_t)m * nb + R) < need) {
+                        if (kBlockDeps && p.blockdeps) {  // this block's own X of layer l
+                            const uint32_t* f = p.bflags + (size_t)m * nb * nb + (R < C ? R * nb + C : C * nb + R);
+                            while (ld_acquire_gpu(f) < (uint32_t)(l - p.l0)) {
+                            }
+                        } else {
+                            const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
+                            while (ld_acquire_gpu(p.counters + (size_t)m * nb + R) < need) {
+                            }
                         }
                     }
                     __syncwarp();
@@ -1189,8 +1237,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #endif
                     __threadfence();
                     uint32_t* cm = p.counters + (size_t)m * nb;
-                    red_release_gpu_add(cm + R, 1u);
-                    if (C != R) red_release_gpu_add(cm + C, 1u);
+                    // the fence above orders this block's writes before all three increments
+                    if (kBlockDeps && p.blockdeps)
+                        red_relaxed_gpu_add(p.bflags + (size_t)m * nb * nb + (R < C ? R * nb + C : C * nb + R), 1u);
+                    red_relaxed_gpu_add(cm + R, 1u);
+                    if (C != R) red_relaxed_gpu_add(cm + C, 1u);
                 }
                 if (p.dbg & 8) w_pub += (unsigned long long)(clock64() - tp);
             }
