@@ -924,78 +924,81 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     } else if (warp < 4 + kEpiWarps) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsDrain) : "memory");
         // ===================================================== chunk drain -> Y (both CTAs)
-        const int q = warp & 3;
-        const int hc = (warp - 4) >> 2;
-        const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + hc * kEpiCols;
-        const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
-        const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
-        int g = 0, u = 0;
-        unsigned long long w_sf = 0;
-        for (int item = pair_id; item < total; item += n_pairs, ++u) {
-            int m, l, pi;
-            pair_decode(p, item, m, l, pi);
-            const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
-            float yacc[kEpiCols];
-#pragma unroll
-            for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
-#pragma unroll 1
-            for (int f = 0; f < chunks; ++f, ++g) {
-                const int sl = g & 3;
-                #if FFG_DRAIN_SPIN
-                FFG_TIMED_DRAIN(w_sf, mbar_wait(&slot_full[sl], (g >> 2) & 1));
-#else
-                FFG_TIMED_DRAIN(w_sf, mbar_wait_sleep(&slot_full[sl], (g >> 2) & 1));
-#endif
-                tc_fence_after();
-                const bool lastc = f == chunks - 1;
-                // ptxas hoists TMEM loads above the previous batch's adds, and the extra
-                // registers in flight spill two accumulator pairs (local stores to L2 every
-                // chunk); making each batch's load address depend on the previous batch's last
-                // sum (AND with the runtime zero p.zero) keeps one batch in flight
-                uint32_t dep = 0;
-#pragma unroll
-                for (int ch = 0; ch < 4; ch += FFG_DRAIN_BATCH) {
-                    uint32_t v[16 * FFG_DRAIN_BATCH];
-#pragma unroll
-                    for (int b = 0; b < FFG_DRAIN_BATCH; ++b)
-                        tmem_ld_32x32b_x16(tlane + sl * 128 + (ch + b) * 16 + dep,
-                                           *reinterpret_cast<uint32_t(*)[16]>(&v[16 * b]));
-                    tmem_ld_wait();
-                    if (ch + FFG_DRAIN_BATCH == 4 && !lastc) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
+        // (FP32-emulated only: single-product modes hand the accumulator to the epilogue)
+        if constexpr (kDrain) {
+            const int q = warp & 3;
+            const int hc = (warp - 4) >> 2;
+            const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + hc * kEpiCols;
+            const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
+            const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
+            int g = 0, u = 0;
+            unsigned long long w_sf = 0;
+            for (int item = pair_id; item < total; item += n_pairs, ++u) {
+                int m, l, pi;
+                pair_decode(p, item, m, l, pi);
+                const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
+                float yacc[kEpiCols];
+    #pragma unroll
+                for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
+    #pragma unroll 1
+                for (int f = 0; f < chunks; ++f, ++g) {
+                    const int sl = g & 3;
+                    #if FFG_DRAIN_SPIN
+                    FFG_TIMED_DRAIN(w_sf, mbar_wait(&slot_full[sl], (g >> 2) & 1));
+    #else
+                    FFG_TIMED_DRAIN(w_sf, mbar_wait_sleep(&slot_full[sl], (g >> 2) & 1));
+    #endif
+                    tc_fence_after();
+                    const bool lastc = f == chunks - 1;
+                    // ptxas hoists TMEM loads above the previous batch's adds, and the extra
+                    // registers in flight spill two accumulator pairs (local stores to L2 every
+                    // chunk); making each batch's load address depend on the previous batch's last
+                    // sum (AND with the runtime zero p.zero) keeps one batch in flight
+                    uint32_t dep = 0;
+    #pragma unroll
+                    for (int ch = 0; ch < 4; ch += FFG_DRAIN_BATCH) {
+                        uint32_t v[16 * FFG_DRAIN_BATCH];
+    #pragma unroll
+                        for (int b = 0; b < FFG_DRAIN_BATCH; ++b)
+                            tmem_ld_32x32b_x16(tlane + sl * 128 + (ch + b) * 16 + dep,
+                                               *reinterpret_cast<uint32_t(*)[16]>(&v[16 * b]));
+                        tmem_ld_wait();
+                        if (ch + FFG_DRAIN_BATCH == 4 && !lastc) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
+                        }
+    #pragma unroll
+                        for (int e = 0; e < 16 * FFG_DRAIN_BATCH; e += 2) {
+                            const float2 acc = add_f32x2(
+                                make_float2(yacc[16 * ch + e], yacc[16 * ch + e + 1]),
+                                make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+                            yacc[16 * ch + e] = acc.x;
+                            yacc[16 * ch + e + 1] = acc.y;
+                        }
+                        if (FFG_DRAIN_DEP)
+                            dep = (__float_as_uint(yacc[16 * ch + 16 * FFG_DRAIN_BATCH - 1]) |
+                                   __float_as_uint(yacc[16 * ch])) & p.zero;
                     }
-#pragma unroll
-                    for (int e = 0; e < 16 * FFG_DRAIN_BATCH; e += 2) {
-                        const float2 acc = add_f32x2(
-                            make_float2(yacc[16 * ch + e], yacc[16 * ch + e + 1]),
-                            make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
-                        yacc[16 * ch + e] = acc.x;
-                        yacc[16 * ch + e + 1] = acc.y;
+                }
+                {  // Y into the item's last slot for the epilogue (which frees the slot); outside
+                   // the chunk loop, so the loop keeps its registers for the sums in flight
+                    const int sl = (g - 1) & 3;
+    #pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t v[16];
+    #pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * ch + e] * inv_s2);
+                        tmem_st_32x32b_x16(tlane + sl * 128 + ch * 16, v);
                     }
-                    if (FFG_DRAIN_DEP)
-                        dep = (__float_as_uint(yacc[16 * ch + 16 * FFG_DRAIN_BATCH - 1]) |
-                               __float_as_uint(yacc[16 * ch])) & p.zero;
+                    tmem_st_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&y_full[sl]);
                 }
             }
-            {  // Y into the item's last slot for the epilogue (which frees the slot); outside
-               // the chunk loop, so the loop keeps its registers for the sums in flight
-                const int sl = (g - 1) & 3;
-#pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t v[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * ch + e] * inv_s2);
-                    tmem_st_32x32b_x16(tlane + sl * 128 + ch * 16, v);
-                }
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&y_full[sl]);
-            }
+            if ((p.dbg & 8) && warp == 4 && lane == 0) p.prof[(size_t)blockIdx.x * 16 + 5] = w_sf;
         }
-        if ((p.dbg & 8) && warp == 4 && lane == 0) p.prof[(size_t)blockIdx.x * 16 + 5] = w_sf;
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsEpi) : "memory");
         // ===================================================== epilogue (both CTAs)
@@ -1058,12 +1061,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 if (!(p.dbg & 128)) epi_loadx16(Xt, r, 32 * (ok0 ? s : s + 2), xq);
             }
 #endif
+            if constexpr (!kDrain) {
+                // single-product modes: the slot holds the whole-K accumulator, read directly
+                // (no drain pass); the 1/scale^2 is applied as it is loaded
+                FFG_TIMED(w_y, mbar_wait_sleep(&slot_full[ysl], ((g - 1) >> 2) & 1));
+            } else {
 #if FFG_EPI_SPIN
-            FFG_TIMED(w_y, mbar_wait(&y_full[ysl], (yph >> ysl) & 1));
+                FFG_TIMED(w_y, mbar_wait(&y_full[ysl], (yph >> ysl) & 1));
 #else
-            FFG_TIMED(w_y, mbar_wait_sleep(&y_full[ysl], (yph >> ysl) & 1));
+                FFG_TIMED(w_y, mbar_wait_sleep(&y_full[ysl], (yph >> ysl) & 1));
 #endif
-            yph ^= 1u << ysl;
+                yph ^= 1u << ysl;
+            }
             tc_fence_after();
 #pragma unroll 1
             for (int qi = 0; qi < 2; ++qi) {
@@ -1089,6 +1098,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     uint32_t v[16];
                     tmem_ld_32x32b_x16(tacc + c0, v);
                     tmem_ld_wait();
+                    if constexpr (!kDrain && Tr::kScale != 1.0f) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            v[e] = __float_as_uint(__uint_as_float(v[e]) * (1.0f / (Tr::kScale * Tr::kScale)));
+                    }
                     if (!last) {
 #if FFG_A_RED
                         float4 xn[4];
