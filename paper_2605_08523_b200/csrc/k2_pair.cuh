@@ -1237,25 +1237,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             } else if (!dummy && l + 1 < p.l1) {
                 // publish the block: hi/lo stores landed, X/A stores visible -> panel counters
                 const long long tp = clock64();
-                if (lane == 0) {
+                if (lane == 0 && !(p.dbg & 256)) {  // dbg & 256: measurement only, no wait
                     tma_store_wait_all();
                     fence_proxy_async_global();
                 }
                 __syncwarp();
+                if (p.dbg & 256) {
+                    if (ew == 0 && lane == 0) {
+                        uint32_t* cm = p.counters + (size_t)m * nb;
+                        red_relaxed_gpu_add(cm + R, 1u);
+                        if (C != R) red_relaxed_gpu_add(cm + C, 1u);
+                    }
+                } else {
 #if FFG_WARP_PUBLISH
-                // per warp: no wait for the block's slowest warp (consumers count 8 per block)
-                if (lane == 0) {
+                    // per warp: no wait for the block's slowest warp (consumers count 8 per block)
+                    if (lane == 0) {
 #else
-                named_bar_sync(4, kEpiWarps2 * 32);
-                if (ew == 0 && lane == 0) {
+                    named_bar_sync(4, kEpiWarps2 * 32);
+                    if (ew == 0 && lane == 0) {
 #endif
-                    __threadfence();
-                    uint32_t* cm = p.counters + (size_t)m * nb;
-                    // the fence above orders this block's writes before all three increments
-                    if (kBlockDeps && p.blockdeps)
-                        red_relaxed_gpu_add(p.bflags + (size_t)m * nb * nb + (R < C ? R * nb + C : C * nb + R), 1u);
-                    red_relaxed_gpu_add(cm + R, 1u);
-                    if (C != R) red_relaxed_gpu_add(cm + C, 1u);
+                        __threadfence();
+                        uint32_t* cm = p.counters + (size_t)m * nb;
+                        // the fence above orders this block's writes before all three increments
+                        if (kBlockDeps && p.blockdeps)
+                            red_relaxed_gpu_add(p.bflags + (size_t)m * nb * nb + (R < C ? R * nb + C : C * nb + R), 1u);
+                        red_relaxed_gpu_add(cm + R, 1u);
+                        if (C != R) red_relaxed_gpu_add(cm + C, 1u);
+                    }
                 }
                 if (p.dbg & 8) w_pub += (unsigned long long)(clock64() - tp);
             }
