@@ -258,7 +258,8 @@ __device__ __forceinline__ void epi_loadx16(const float* Xt, int r, int c0, floa
 template <int MODE, bool DIAG>
 __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const float4 (&xq)[4], float* Xt, float* At,
                                                 int r, int c0, int lane, int sub, bool c_on, const EpiCoef& k,
-                                                uint32_t stg_d, bool dblk, EpiHealth& hl, bool nomem = false) {
+                                                uint32_t stg_d, bool dblk, EpiHealth& hl, bool nomem = false,
+                                                bool store_x = true) {
     using Tr = ModeTraits<MODE>;
     uint32_t hp[8], lp[8];
 #pragma unroll
@@ -281,7 +282,8 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
             xs[e] = xn;
         }
         if (!nomem) {  // (measurement only: dbg & 64)
-            __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
+            if (store_x)
+                __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
             red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
         }
         split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
@@ -308,6 +310,67 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
             if (Tr::kHasLo) {
                 sts_u16(stg_d + kPieceBytes + off, lb);
                 sts_u16(stg_d + kPieceBytes + doff, lb);
+            }
+        }
+    }
+}
+
+// FFG_X_HILO (FP32-emulated): X of 16 columns rebuilt from the binary16 hi/lo operand row the previous
+// layer stored (x = (hi + lo) 2^-14, exact in fp32: ~22 significant bits, the same X the MMA squares), so
+// K2 never stores or reads the fp32 X blocks.  hrow/lrow point at column c0 of the thread's row.
+__device__ __forceinline__ void epi_loadx16_hilo(const uint16_t* hrow, const uint16_t* lrow, float4 (&xq)[4]) {
+    uint4 h[2], q[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        h[i] = __ldcg(reinterpret_cast<const uint4*>(hrow) + i);
+        q[i] = __ldcg(reinterpret_cast<const uint4*>(lrow) + i);
+    }
+    const uint32_t hw[8] = {h[0].x, h[0].y, h[0].z, h[0].w, h[1].x, h[1].y, h[1].z, h[1].w};
+    const uint32_t lw[8] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w};
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&hw[i]));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&lw[i]));
+        v[2 * i + 0] = (a.x + b.x) * (1.0f / kHalfScale);
+        v[2 * i + 1] = (a.y + b.y) * (1.0f / kHalfScale);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xq[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+
+// last layer with X already in registers (FFG_X_HILO)
+template <bool DIAG>
+__device__ __forceinline__ void epi_sub_last_x(const uint32_t (&v)[16], const float4 (&xq)[4], const float* At,
+                                               int r, int c0, int gi, int gj0, int n, bool c_on,
+                                               const EpiCoef& k, double* Dm, EpiHealth& hl, double& tr,
+                                               double& sq) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float4 aq = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
+        const float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
+        const float as[4] = {aq.x, aq.y, aq.z, aq.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int cl = c0 + 4 * j + e;
+            const int gj = gj0 + cl;
+            const float y = __uint_as_float(v[4 * j + e]);
+            const bool dg = DIAG && cl == r;
+            const float xn = (dg && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
+            const bool own = !DIAG || cl >= r;
+            if (own) hl.add(xn);
+            if (own && gi < n && gj < n) {
+                const double dv = (double)as[e] + (double)xn;
+                if (Dm) {
+                    Dm[(size_t)gi * n + gj] = dv;
+                    if (!dg) Dm[(size_t)gj * n + gi] = dv;
+                }
+                if (dg) {
+                    tr += dv;
+                    sq += dv * dv;
+                } else {
+                    sq += 2.0 * dv * dv;
+                }
             }
         }
     }

@@ -95,6 +95,9 @@ static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue war
 // accumulate per K16 step into a chunk-sized partial (accumulation precision);
 // single-product modes: the whole K extent.  The drain warps sum chunks in registers with
 // round-to-nearest adds and write Y into the item's LAST slot, which the epilogue frees.
+#ifndef FFG_X_HILO
+#define FFG_X_HILO 0  // FP32E epilogue: X rebuilt from the hi/lo operands, no fp32 X traffic in K2
+#endif
 #ifndef FFG_BLOCK_DEPS
 #define FFG_BLOCK_DEPS 1  // producer waits per 128-column block when a panel is incomplete (runtime: p.blockdeps)
 #endif
@@ -651,6 +654,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     using Tr = ModeTraits<MODE>;
     using Cfg = PairCfg<MODE, RES>;
     // (FP32-emulated only: a K-block pair there is 1.5K MMA cycles, enough to hide the polls)
+    constexpr bool kXHilo = FFG_X_HILO && MODE == kModeF32E;
     constexpr bool kBlockDeps = FFG_BLOCK_DEPS && !RES && !FFG_TWO_GROUPS && !FFG_WARP_PUBLISH && Tr::kHasLo;
     constexpr bool kDrain = Tr::kProducts == 3;
     constexpr int S = Cfg::kStages;
@@ -1033,6 +1037,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const uint32_t tacc = tlane + ysl * 128;
             float* Xt = p.X + xa_tile_base(m, R, C, nb);
             float* At = p.A + xa_tile_base(m, R, C, nb);
+            // X of layer l: fp32 block, or (FFG_X_HILO, FP32E) rebuilt from the hi/lo operand row
+            const size_t xrow = ((size_t)m * np + R * kBM + r) * np + C * kBN;
+            const uint16_t* hrow = p.hi[l & 1] + xrow;
+            const uint16_t* lrow = p.lo[l & 1] + xrow;
+            auto loadx = [&](int c0, float4(&x)[4]) {
+                if constexpr (kXHilo)
+                    epi_loadx16_hilo(hrow + c0, lrow + c0, x);
+                else
+                    epi_loadx16(Xt, r, c0, x);
+            };
             EpiHealth hl;
             double tr = 0.0, sq = 0.0;
 #if FFG_A_RED
@@ -1058,7 +1072,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     }
                     __syncwarp();
                 }
-                if (!(p.dbg & 128)) epi_loadx16(Xt, r, 32 * (ok0 ? s : s + 2), xq);
+                if (!(p.dbg & 128)) loadx(32 * (ok0 ? s : s + 2), xq);
             }
 #endif
             if constexpr (!kDrain) {
@@ -1107,11 +1121,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #if FFG_A_RED
                         float4 xn[4];
                         const bool more = sub == 0 || (qi == 0 && ok1);
-                        if (more && !(p.dbg & 128)) epi_loadx16(Xt, r, sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
+                        if (more && !(p.dbg & 128)) loadx(sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
                         if (diag)
-                            epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl, p.dbg & 64);
+                            epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
+                                                        p.dbg & 64, !kXHilo);
                         else
-                            epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl, p.dbg & 64);
+                            epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
+                                                         p.dbg & 64, !kXHilo);
                         if (more) {
 #pragma unroll
                             for (int j = 0; j < 4; ++j) xq[j] = xn[j];
@@ -1140,10 +1156,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #endif
                     } else {
                         double* Dm = p.D ? p.D + (size_t)m * n * n : nullptr;
-                        if (diag)
+                        if constexpr (kXHilo) {
+                            float4 xl[4];
+                            loadx(c0, xl);
+                            if (diag)
+                                epi_sub_last_x<true>(v, xl, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                            else
+                                epi_sub_last_x<false>(v, xl, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                        } else if (diag) {
                             epi_sub_last<true>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
-                        else
+                        } else {
                             epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                        }
                     }
                 }
                 const long long t_c1 = (p.dbg & 8) ? clock64() : 0;

@@ -421,3 +421,24 @@ def test_bitwise_deterministic(model):
         D1, s1, _ = E.compute_density_matrix(H, 0.02, 0.011, model, mode)
         D2, s2, _ = E.compute_density_matrix(H, 0.02, 0.011, model, mode)
         assert np.array_equal(D1, D2) and s1 == s2
+
+
+def test_schedule_invariance(model, monkeypatch):
+    """The schedule changes only the order of independent work, never the arithmetic: results are
+    bit-identical across L2 group sizes (FFG_GROUP) and with block-granular dependency waits
+    forced on or off (FFG_BLOCKDEPS), for a batch and for a single matrix."""
+    mu, kT = batch_params(6)
+    Hs = [tight_binding(512, seed=500 + k) for k in range(6)]
+    ref_b, st_b, _ = E.compute_density_matrices(Hs, mu, kT, model)
+    H1 = tight_binding(1024, seed=9)
+    ref_1, st_1, _ = E.compute_density_matrix(H1, 0.0, 0.01, model)
+    for env in ({"FFG_GROUP": "1"}, {"FFG_GROUP": "4"}, {"FFG_BLOCKDEPS": "1"}, {"FFG_BLOCKDEPS": "0"},
+                {"FFG_GROUP": "2", "FFG_BLOCKDEPS": "1"}):
+        with monkeypatch.context() as mp:
+            for k, v in env.items():
+                mp.setenv(k, v)
+            Db, sb, _ = E.compute_density_matrices(Hs, mu, kT, model)
+            D1, s1, _ = E.compute_density_matrix(H1, 0.0, 0.01, model)
+        assert all(np.array_equal(a, b) for a, b in zip(Db, ref_b)), env
+        assert [(s.trace, s.trace_square) for s in sb] == [(s.trace, s.trace_square) for s in st_b], env
+        assert np.array_equal(D1, ref_1) and (s1.trace, s1.trace_square) == (st_1.trace, st_1.trace_square), env
