@@ -48,6 +48,9 @@ constexpr int kPRegsCtl = 48, kPRegsDrain = 104, kPRegsEpi = 112;
 constexpr int kPRegsCtl = 48, kPRegsDrain = 96, kPRegsEpi = 120;
 #endif
 static_assert(128 * kPRegsCtl + 256 * kPRegsDrain + 256 * kPRegsEpi <= 640 * 96, "setmaxnreg budget");
+#ifndef FFG_STREAM16
+#define FFG_STREAM16 0  // 16 worker warps: each drains and runs the epilogue of one 32-column piece
+#endif
 #ifndef FFG_TWO_GROUPS
 #define FFG_TWO_GROUPS 0  // streaming workers as two drain+epilogue groups on alternate items
 #endif
@@ -74,7 +77,7 @@ constexpr int kPairStagingBytes = kEpiWarps2 * kStgPieces * kPieceBytes;  // 32 
 // epilogue; 32 KB with in-place mirrors, which buys an extra operand stage (two for BF16)
 template <int MODE, bool RES = false>
 struct PairCfg {
-    static constexpr bool kWide = RES || FFG_TWO_GROUPS || !FFG_STAGING_INPLACE;
+    static constexpr bool kWide = RES || FFG_TWO_GROUPS || FFG_STREAM16 || !FFG_STAGING_INPLACE;
     static constexpr int kStagingBytes = kWide ? kEpiWarps2 * 4 * kPieceBytes : kPairStagingBytes;
     static constexpr int kStageBytes = ModeTraits<MODE>::kHasLo ? 2 * (kPairOpA + kPairOpB)
                                                                 : (kPairOpA + kPairOpB);
@@ -622,6 +625,184 @@ __device__ __forceinline__ void two_group_workers(const PairMaps& tm, const Pair
     if (lane == 0) tma_store_wait_all();
 }
 
+// Streaming 16-worker epilogue (FFG_STREAM16): warps 4-19 all work on every item.  Warp w:
+// TMEM lane quarter q = w & 3 (rows 32q..32q+31), column quarter c = (w - 4) >> 2 (32 columns).
+// The warp drains its 32 columns of every chunk into register sums and releases each TMEM slot
+// as soon as it is read (Y never holds a slot, so the MMA always has the four-slot ring), then
+// runs the epilogue of its 32x32 piece straight from those registers: one piece per warp per item
+// instead of two, sixteen in flight per CTA.
+template <int MODE>
+__device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairParams& p, uint32_t tmem,
+                                                 int warp, int lane, uint32_t rank, int pair_id, int n_pairs,
+                                                 int total, int nk, uint64_t* slot_full, uint64_t* slot_empty,
+                                                 uint8_t* staging, double* red) {
+    using Tr = ModeTraits<MODE>;
+    const int wk = warp - 4, q = warp & 3, c = wk >> 2;
+    const int r = q * 32 + lane;
+    const int nb = p.nb, n = p.n, np = p.np;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + 32 * c;  // + slot * 128
+    const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
+    const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
+    uint8_t* stg = staging + wk * 2 * kPieceBytes;  // direct hi piece, lo piece (mirrors in place)
+    const uint32_t stg_a = smem_u32(stg);
+    int g = 0;
+    for (int item = pair_id; item < total; item += n_pairs) {
+        int m, l, pi;
+        pair_decode(p, item, m, l, pi);
+        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
+        float yacc[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) yacc[e] = 0.0f;
+#pragma unroll 1
+        for (int f = 0; f < chunks; ++f, ++g) {
+            const int sl = g & 3;
+            mbar_wait(&slot_full[sl], (g >> 2) & 1);
+            tc_fence_after();
+            uint32_t v[32];
+            tmem_ld_32x32b_x16(tl + sl * 128, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+            tmem_ld_32x32b_x16(tl + sl * 128 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+                const float2 acc = add_f32x2(make_float2(yacc[e], yacc[e + 1]),
+                                             make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
+                yacc[e] = acc.x;
+                yacc[e + 1] = acc.y;
+            }
+        }
+        // ------------------------------------------------------------- epilogue of the item
+        const uint32_t pr = __ldg(p.pairs + pi);
+        const int R = rank ? (pr >> 10) & 1023 : pr & 1023;
+        const int C = (pr >> 20) & 1023;
+        const bool dummy = rank && ((pr >> 30) & 1);
+        const bool last = (l == p.n_layers - 1);
+        const bool diag = R == C;
+        const bool skip = dummy || (p.dbg & 1) || (diag && c < q);
+        const bool dblk = diag && c == q;
+        const int gi = R * kBM + r;
+        const bool c_on = gi < n;
+        const EpiCoef k = load_coef(p.coef, l, last);
+        const int nxt = (l + 1) & 1;
+        float* Xt = p.X + xa_tile_base(m, R, C, nb);
+        float* At = p.A + xa_tile_base(m, R, C, nb);
+        EpiHealth hl;
+        double tr = 0.0, sq = 0.0;
+        if (!skip) {
+            if (!last) {
+                if (lane == 0) tma_store_wait_read();  // the staging pieces are free again
+                __syncwarp();
+                float4 xq[4];
+                if (!(p.dbg & 128)) epi_loadx16(Xt, r, 32 * c, xq);
+#pragma unroll
+                for (int sub = 0; sub < 2; ++sub) {
+                    const int c0 = 32 * c + 16 * sub;
+                    float4 xn[4];
+                    if (sub == 0 && !(p.dbg & 128)) epi_loadx16(Xt, r, c0 + 16, xn);
+                    uint32_t v[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * sub + e] * inv_s2);
+                    if (diag)
+                        epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
+                                                    p.dbg & 64);
+                    else
+                        epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
+                                                     p.dbg & 64);
+                    if (sub == 0) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) xq[j] = xn[j];
+                    }
+                }
+                if (!(p.dbg & 32)) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int prow = m * np + R * kBM + 32 * q;  // direct piece origin
+                        const int pcol = C * kBN + 32 * c;
+                        tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
+                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
+                        tma_store_commit();
+                    }
+                    if (!dblk) {  // mirrored pieces: transpose in place once the direct stores read them
+                        if (lane == 0) tma_store_wait_read();
+                        __syncwarp();
+                        transpose_piece_inplace(stg_a, lane);
+                        if (Tr::kHasLo) transpose_piece_inplace(stg_a + kPieceBytes, lane);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int mrow = m * np + C * kBN + 32 * c;
+                            const int mcol = R * kBM + 32 * q;
+                            tma_store_2d(&tm.p_hi[nxt], stg, mcol, mrow);
+                            if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, mcol, mrow);
+                            tma_store_commit();
+                        }
+                    }
+                }
+            } else {
+                double* Dm = p.D ? p.D + (size_t)m * n * n : nullptr;
+#pragma unroll
+                for (int sub = 0; sub < 2; ++sub) {
+                    const int c0 = 32 * c + 16 * sub;
+                    uint32_t v[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * sub + e] * inv_s2);
+                    if (diag)
+                        epi_sub_last<true>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                    else
+                        epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                }
+            }
+        }
+        if (!dummy) {
+            const bool any_nf = __any_sync(0xffffffffu, hl.nonfinite());
+            const bool any_hr = !last && __any_sync(0xffffffffu, hl.template half_range<MODE>());
+            if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], l + 1);
+            if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], l + 1);
+        }
+        if (last) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                tr += __shfl_xor_sync(0xffffffffu, tr, o);
+                sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            }
+            named_bar_sync(3, 16 * 32);  // the previous block's partial consumed
+            if (lane == 0) {
+                red[2 * wk + 0] = tr;
+                red[2 * wk + 1] = sq;
+            }
+            named_bar_sync(3, 16 * 32);
+            if (wk == 0 && lane == 0) {
+                double T0 = 0.0, T1 = 0.0;
+                for (int w = 0; w < 16; ++w) {  // fixed order
+                    T0 += red[2 * w + 0];
+                    T1 += red[2 * w + 1];
+                }
+                p.partials[(size_t)m * 2 * p.PT + 2 * pi + rank] = make_double2(T0, T1);
+            }
+        } else if (!dummy && l + 1 < p.l1) {
+            // publish the block: hi/lo stores landed, X/A writes ordered -> block / panel counters
+            if (lane == 0) {
+                tma_store_wait_all();
+                fence_proxy_async_global();
+            }
+            __syncwarp();
+            named_bar_sync(4, 16 * 32);
+            if (wk == 0 && lane == 0) {
+                __threadfence();
+                uint32_t* cm = p.counters + (size_t)m * nb;
+                if (FFG_BLOCK_DEPS && MODE == kModeF32E && p.blockdeps)
+                    red_relaxed_gpu_add(p.bflags + (size_t)m * nb * nb + (R < C ? R * nb + C : C * nb + R), 1u);
+                red_relaxed_gpu_add(cm + R, 1u);
+                if (C != R) red_relaxed_gpu_add(cm + C, 1u);
+            }
+        }
+    }
+    if (lane == 0) tma_store_wait_all();
+}
+
 // dbg & 8: accumulate the cycles a role spends in a wait into a register counter
 #define FFG_TIMED(acc, stmt)                                     \
     do {                                                         \
@@ -687,7 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int i = 0; i < 4; ++i) {
             mbar_init(&slot_full[i], 1);
             // streaming: drain warps, or epilogue warps (Y slot); resident: the 16 worker warps
-            mbar_init(&slot_empty[i], RES ? 2 * kResWorkers : 2 * kEpiWarps);
+            mbar_init(&slot_empty[i], (RES || FFG_STREAM16) ? 2 * kResWorkers : 2 * kEpiWarps);
         }
         for (int i = 0; i < 4; ++i) mbar_init(&y_full[i], kEpiWarps);
         fence_barrier_init();
@@ -699,7 +880,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RES ? kRRegsCtl : (FFG_TWO_GROUPS ? kGRegsCtl : kPRegsCtl)) : "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"((RES || FFG_STREAM16) ? kRRegsCtl : (FFG_TWO_GROUPS ? kGRegsCtl : kPRegsCtl)) : "memory");
         if (warp == 0 && lane == 0) {
             // ================================================= TMA producer (both CTAs)
             for (int i = 0; i < 2; ++i) {
@@ -921,6 +1102,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         resident_workers<MODE>(p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk,
                                slot_full, slot_empty, smem + Cfg::kStagingOff,
                                reinterpret_cast<double*>(bars + 2 * S + 14));
+    } else if (FFG_STREAM16) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRRegsWork) : "memory");
+        stream16_workers<MODE>(tm, p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk, slot_full,
+                               slot_empty, smem + Cfg::kStagingOff, red);
     } else if (FFG_TWO_GROUPS) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kGRegsWork) : "memory");
         two_group_workers<MODE>(tm, p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk, slot_full,
