@@ -557,18 +557,18 @@ int group_size(int B, int64_t np, int PT, int resident_pairs, int mode) {
 
 // Co-resident CTA pairs of the pair kernel (all pairs must be resident: the layer
 // dependencies are waited for inside the kernel).
-template <int MODE, bool RES>
+template <int MODE, int V>
 int pair_capacity(int* out) {
     static int max_pairs = -1;
     if (max_pairs < 0) {
-        CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                PairCfg<MODE, RES>::kSmem));
+        CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                PairCfg<MODE, (V != 0)>::kSmem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * (num_sms() / 2));
         cfg.blockDim = dim3(kPairThreads);
-        cfg.dynamicSmemBytes = PairCfg<MODE, RES>::kSmem;
+        cfg.dynamicSmemBytes = PairCfg<MODE, (V != 0)>::kSmem;
         int nc = 0;
-        CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_pair_kernel<MODE, RES>, &cfg));
+        CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_pair_kernel<MODE, V>, &cfg));
         if (nc < 1) return set_err(FFG_ERR_CUDA, "pair kernel: no co-resident CTA pair fits");
         max_pairs = nc;
     }
@@ -576,35 +576,46 @@ int pair_capacity(int* out) {
     return FFG_OK;
 }
 
-template <int MODE, bool RES>
+template <int MODE, int V>
 int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
+    constexpr bool RES = V == 1;
     int cap, rc;
-    if ((rc = pair_capacity<MODE, RES>(&cap))) return rc;
+    if ((rc = pair_capacity<MODE, V>(&cap))) return rc;
     if ((rc = install_watchdog())) return set_err(FFG_ERR_CUDA, "watchdog buffer");
     // streaming: persistent pairs walk all items round-robin; resident: exactly one CTA pair per
     // pair item of a layer (each keeps its block for all layers), `items` = pairs per layer
     if (RES && items > cap) return set_err(FFG_ERR_CUDA, "resident K2: %lld pairs > %d resident", (long long)items, cap);
     const int pairs = (int)std::min<int64_t>(cap, items);
-    mlsp2_pair_kernel<MODE, RES><<<2 * pairs, kPairThreads, PairCfg<MODE, RES>::kSmem, st>>>(maps, pp);
+    mlsp2_pair_kernel<MODE, V><<<2 * pairs, kPairThreads, PairCfg<MODE, (V != 0)>::kSmem, st>>>(maps, pp);
     CK(cudaGetLastError());
     return FFG_OK;
 }
 
-template <bool RES>
+// V: 0 streaming, 1 resident, 2 streaming with 16 workers (single-product modes only)
+template <int V>
 int pair_capacity_mode(int mode, int* cap) {
     switch (mode) {
-        case kModeF32E: return pair_capacity<kModeF32E, RES>(cap);
-        case kModeF16: return pair_capacity<kModeF16, RES>(cap);
-        default: return pair_capacity<kModeBF16, RES>(cap);
+        case kModeF32E: return pair_capacity<kModeF32E, V == 2 ? 0 : V>(cap);
+        case kModeF16: return pair_capacity<kModeF16, V>(cap);
+        default: return pair_capacity<kModeBF16, V>(cap);
     }
 }
-template <bool RES>
+template <int V>
 int launch_pair_mode(int mode, const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
     switch (mode) {
-        case kModeF32E: return launch_pair<kModeF32E, RES>(maps, pp, items, st);
-        case kModeF16: return launch_pair<kModeF16, RES>(maps, pp, items, st);
-        default: return launch_pair<kModeBF16, RES>(maps, pp, items, st);
+        case kModeF32E: return launch_pair<kModeF32E, V == 2 ? 0 : V>(maps, pp, items, st);
+        case kModeF16: return launch_pair<kModeF16, V>(maps, pp, items, st);
+        default: return launch_pair<kModeBF16, V>(maps, pp, items, st);
     }
+}
+
+// Single-product modes at np <= 512: sixteen drain+epilogue workers (no separate drain pass
+// exists there, and each worker finishes one 32-column piece) measured 18% faster at 64 x N=512;
+// equal at N=1024, 6% slower at N=4096.  FFG_S16=0/1 overrides.
+bool use_s16(int mode, int64_t np) {
+    const char* e = getenv("FFG_S16");
+    if (e) return mode != kModeF32E && atoi(e) != 0;
+    return mode != kModeF32E && np <= 512;
 }
 
 // Resident K2 (one block per CTA for the whole recursion, k2_pair.cuh resident_workers) when
@@ -783,7 +794,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
             g_prof_buf = prof;
         }
         int cap_res = 0, cap = 0;
-        if ((rc = pair_capacity_mode<true>(j.mode, &cap_res))) return rc;
+        if ((rc = pair_capacity_mode<1>(j.mode, &cap_res))) return rc;
         cudaEvent_t stop;
         if ((rc = prof_begin(st, &stop, layer_flops * md.n_layers))) return rc;
         if (use_resident(w.PT, cap_res)) {
@@ -794,10 +805,11 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
                 gp.m0 = m0;
                 gp.B = std::min(G, B - m0);
                 gp.G = gp.B;
-                if ((rc = launch_pair_mode<true>(j.mode, w.pmaps, gp, (int64_t)gp.B * w.PT, st))) return rc;
+                if ((rc = launch_pair_mode<1>(j.mode, w.pmaps, gp, (int64_t)gp.B * w.PT, st))) return rc;
             }
         } else {
-            if ((rc = pair_capacity_mode<false>(j.mode, &cap))) return rc;
+            const bool s16 = use_s16(j.mode, np);
+            if ((rc = s16 ? pair_capacity_mode<2>(j.mode, &cap) : pair_capacity_mode<0>(j.mode, &cap))) return rc;
             pp.G = group_size(B, np, w.PT, cap, j.mode);
             // single-matrix groups: a layer is one matrix, so its items wait on each other;
             // block-granular waits let a next-layer item start on its completed blocks
@@ -806,7 +818,9 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
             const char* bd = getenv("FFG_BLOCKDEPS");
             pp.blockdeps = bd ? atoi(bd) : (pp.G == 1);
             const int64_t items = (int64_t)md.n_layers * B * w.PT;
-            if ((rc = launch_pair_mode<false>(j.mode, w.pmaps, pp, items, st))) return rc;
+            if ((rc = s16 ? launch_pair_mode<2>(j.mode, w.pmaps, pp, items, st)
+                          : launch_pair_mode<0>(j.mode, w.pmaps, pp, items, st)))
+                return rc;
         }
         if (stop) CK(cudaEventRecord(stop, st));
     } else {

@@ -75,9 +75,9 @@ constexpr int kPairStagingBytes = kEpiWarps2 * kStgPieces * kPieceBytes;  // 32 
 
 // staging: 64 KB for the resident / two-group workers (16 warps x 4 KB) and the 4-piece
 // epilogue; 32 KB with in-place mirrors, which buys an extra operand stage (two for BF16)
-template <int MODE, bool RES = false>
+template <int MODE, bool WIDE = false>
 struct PairCfg {
-    static constexpr bool kWide = RES || FFG_TWO_GROUPS || FFG_STREAM16 || !FFG_STAGING_INPLACE;
+    static constexpr bool kWide = WIDE || FFG_TWO_GROUPS || FFG_STREAM16 || !FFG_STAGING_INPLACE;
     static constexpr int kStagingBytes = kWide ? kEpiWarps2 * 4 * kPieceBytes : kPairStagingBytes;
     static constexpr int kStageBytes = ModeTraits<MODE>::kHasLo ? 2 * (kPairOpA + kPairOpB)
                                                                 : (kPairOpA + kPairOpB);
@@ -826,14 +826,17 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
 #define FFG_TIMED_DRAIN(acc, stmt) stmt
 #endif
 
-template <int MODE, bool RES = false>
+// V: 0 streaming (drain + epilogue warps), 1 resident (RES), 2 streaming with 16 workers (S16)
+template <int MODE, int V = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     mlsp2_pair_kernel(const __grid_constant__ PairMaps tm, const __grid_constant__ PairParams p) {
+    constexpr bool RES = V == 1;
+    constexpr bool S16 = V == 2 || (V == 0 && FFG_STREAM16);
     constexpr int kSlots = RES ? 3 : 4;  // TMEM chunk ring (resident: slot 3 holds the X block)
     // panel-counter increments per published block (per-warp publication: one per epilogue warp)
     constexpr uint32_t kPub = (!RES && !FFG_TWO_GROUPS && FFG_WARP_PUBLISH) ? kEpiWarps2 : 1;
     using Tr = ModeTraits<MODE>;
-    using Cfg = PairCfg<MODE, RES>;
+    using Cfg = PairCfg<MODE, (V != 0)>;
     // (FP32-emulated only: a K-block pair there is 1.5K MMA cycles, enough to hide the polls)
     constexpr bool kXHilo = FFG_X_HILO && MODE == kModeF32E;
     constexpr bool kBlockDeps = FFG_BLOCK_DEPS && !RES && !FFG_TWO_GROUPS && !FFG_WARP_PUBLISH && Tr::kHasLo;
@@ -868,7 +871,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int i = 0; i < 4; ++i) {
             mbar_init(&slot_full[i], 1);
             // streaming: drain warps, or epilogue warps (Y slot); resident: the 16 worker warps
-            mbar_init(&slot_empty[i], (RES || FFG_STREAM16) ? 2 * kResWorkers : 2 * kEpiWarps);
+            mbar_init(&slot_empty[i], (RES || S16) ? 2 * kResWorkers : 2 * kEpiWarps);
         }
         for (int i = 0; i < 4; ++i) mbar_init(&y_full[i], kEpiWarps);
         fence_barrier_init();
@@ -880,7 +883,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"((RES || FFG_STREAM16) ? kRRegsCtl : (FFG_TWO_GROUPS ? kGRegsCtl : kPRegsCtl)) : "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"((RES || S16) ? kRRegsCtl : (FFG_TWO_GROUPS ? kGRegsCtl : kPRegsCtl)) : "memory");
         if (warp == 0 && lane == 0) {
             // ================================================= TMA producer (both CTAs)
             for (int i = 0; i < 2; ++i) {
@@ -1102,7 +1105,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         resident_workers<MODE>(p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk,
                                slot_full, slot_empty, smem + Cfg::kStagingOff,
                                reinterpret_cast<double*>(bars + 2 * S + 14));
-    } else if (FFG_STREAM16) {
+    } else if constexpr (S16) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRRegsWork) : "memory");
         stream16_workers<MODE>(tm, p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk, slot_full,
                                slot_empty, smem + Cfg::kStagingOff, red);
