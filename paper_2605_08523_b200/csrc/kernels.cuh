@@ -258,9 +258,10 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
     (void)d0f;
     double radius[4] = {0.0, 0.0, 0.0, 0.0}, hii[4] = {0.0, 0.0, 0.0, 0.0};
     bool bad_nf = false, bad_hr = false;
-    for (int J = 0; J < nb; ++J) {
-        const int c0 = J * 128 + 4 * lane;           // this lane's 4 columns
-        double hk[4][4];                              // all four rows' loads in flight together
+    // the four rows of tile J (this lane's 4 columns); tile J+1 is requested before tile J is
+    // processed, so the loads overlap the stores and barriers of the previous tile
+    auto load_tile = [&](int J, double (&hk)[4][4]) {
+        const int c0 = J * 128 + 4 * lane;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int i = row0 + warp * 4 + k;
@@ -278,6 +279,17 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
                 }
             }
         }
+    };
+    double hnext[4][4];
+    load_tile(0, hnext);
+    for (int J = 0; J < nb; ++J) {
+        const int c0 = J * 128 + 4 * lane;           // this lane's 4 columns
+        double hk[4][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hk[k][e] = hnext[k][e];
+        if (J + 1 < nb) load_tile(J + 1, hnext);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int rl = warp * 4 + k;              // local row 0..31
