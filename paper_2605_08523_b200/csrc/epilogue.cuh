@@ -17,18 +17,12 @@ struct EpiCoef {
     float a_hi, a_lo, b_hi, b_lo, c_hi, c_lo, d_hi, d_lo;
 };
 
-__device__ __forceinline__ void split_f64(double v, float& hi, float& lo) {
-    hi = (float)v;
-    lo = (float)(v - (double)hi);
-}
-
-__device__ __forceinline__ EpiCoef load_coef(const double* coef, int l, bool last) {
-    EpiCoef k;
-    split_f64(__ldg(coef + 4 * l + 0), k.a_hi, k.a_lo);
-    split_f64(__ldg(coef + 4 * l + 1), k.b_hi, k.b_lo);
-    split_f64(__ldg(coef + 4 * l + 2), k.c_hi, k.c_lo);
-    split_f64(last ? 0.0 : __ldg(coef + 4 * (l + 1) + 3), k.d_hi, k.d_lo);
-    return k;
+// Layer l's coefficients as hi/lo fp32 pairs {a_hi, a_lo, b_hi, b_lo, c_hi, c_lo, d_hi, d_lo}, split on
+// the host from the fp64 model (hi = rn_f32(v), lo = rn_f32(v - hi)); d is the NEXT layer's d (0 after
+// the last layer), the accumulate that follows this layer's X'.
+__device__ __forceinline__ EpiCoef load_coef(const float4* coef, int l, bool /*last*/) {
+    const float4 u = __ldg(coef + 2 * l), w = __ldg(coef + 2 * l + 1);
+    return EpiCoef{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
 }
 
 #ifndef FFG_EPI_EFT

@@ -189,7 +189,7 @@ struct Workspace {
     size_t cap_used = 0;
     int pairs_nb = -1, PT = 0;
     size_t cap_pairs = 0;
-    double* coef = nullptr;
+    float* coef = nullptr;              // [L][8] hi/lo fp32 coefficients (load_coef)
     size_t cap_coef = 0;
     int pm_B = -1, pm_np = -1;
     PairMaps pmaps;
@@ -673,9 +673,9 @@ int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L) {
         w.pairs_nb = nb;
         w.PT = (int)t.size();
     }
-    if ((size_t)4 * L > w.cap_coef) {
-        if ((rc = grow(&w.coef, dummy, (size_t)4 * L))) return rc;
-        w.cap_coef = (size_t)4 * L;
+    if ((size_t)8 * L > w.cap_coef) {
+        if ((rc = grow(&w.coef, dummy, (size_t)8 * L))) return rc;
+        w.cap_coef = (size_t)8 * L;
     }
     if (w.pm_B != B || w.pm_np != (int)np) {
         for (int par = 0; par < 2; ++par) {
@@ -735,8 +735,22 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         ph[3 * B + m] = j.mu ? j.mu[m] : 0.0;
     }
     if ((rc = upload_small(w, w.params, ph.data(), sizeof(double) * 4 * B, st))) return rc;
-    if (pair && (rc = upload_small(w, w.coef, md.abcd, sizeof(double) * 4 * md.n_layers, st)))
-        return rc;
+    if (pair) {
+        // hi/lo fp32 split of a, b, c and the next layer's d, per layer (epilogue.cuh load_coef)
+        std::vector<float> cf((size_t)8 * md.n_layers);
+        auto split = [](double v, float* o) {
+            o[0] = (float)v;
+            o[1] = (float)(v - (double)o[0]);
+        };
+        for (int l = 0; l < md.n_layers; ++l) {
+            float* o = cf.data() + 8 * l;
+            split(md.abcd[4 * l + 0], o + 0);
+            split(md.abcd[4 * l + 1], o + 2);
+            split(md.abcd[4 * l + 2], o + 4);
+            split(l + 1 < md.n_layers ? md.abcd[4 * (l + 1) + 3] : 0.0, o + 6);
+        }
+        if ((rc = upload_small(w, w.coef, cf.data(), sizeof(float) * cf.size(), st))) return rc;
+    }
     const int ncnt = pair ? B * nb * (1 + nb) : 0;
     reset_kernel<<<(std::max(B, ncnt) + 127) / 128, 128, 0, st>>>(w.bounds, w.flags, B, w.counters, ncnt);
     CK(cudaGetLastError());
@@ -771,7 +785,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         pp.counters = w.counters;
         pp.bflags = w.counters + (size_t)B * nb;
         pp.pairs = w.pairs;
-        pp.coef = w.coef;
+        pp.coef = reinterpret_cast<const float4*>(w.coef);
         pp.n = (int)n;
         pp.np = (int)np;
         pp.nb = nb;
