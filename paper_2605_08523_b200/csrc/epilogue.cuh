@@ -15,6 +15,7 @@ namespace ffg {
 
 struct EpiCoef {
     float a_hi, a_lo, b_hi, b_lo, c_hi, c_lo, d_hi, d_lo;
+    bool fixed;  // split X' with the fixed-point hi (the next layer accumulates hi*hi exactly)
 };
 
 // Layer l's coefficients as hi/lo fp32 pairs {a_hi, a_lo, b_hi, b_lo, c_hi, c_lo, d_hi, d_lo}, split on
@@ -22,7 +23,7 @@ struct EpiCoef {
 // the last layer), the accumulate that follows this layer's X'.
 __device__ __forceinline__ EpiCoef load_coef(const float4* coef, int l, bool /*last*/) {
     const float4 u = __ldg(coef + 2 * l), w = __ldg(coef + 2 * l + 1);
-    return EpiCoef{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
+    return EpiCoef{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w, false};
 }
 
 #ifndef FFG_EPI_EFT
@@ -73,16 +74,21 @@ __device__ __forceinline__ float acc_step(float a, float x, const EpiCoef& k) {
 }
 
 // packed binary16 split of two values: hi = rn(x * 2^14), lo = rn(x * 2^14 - hi)
-// (bf16 mode: hi = rn_bf16(x), lo = 0)
+// (bf16 mode: hi = rn_bf16(x), lo = 0).  fixed (FP32E, the layers before `exact_layers`): hi is
+// rounded to a multiple of 8 in the 2^14-scaled domain (x on a 2^-11 grid; exact in binary16 for
+// |x| < 2), so the next layer's hi*hi products and all their partial sums lie on the 2^6 grid and
+// an fp32 accumulator adds them exactly (|sums| < 2^30 for a spectrum in [0, 1]).
 template <int MODE>
-__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo, bool fixed = false) {
     if constexpr (MODE == kModeBF16) {
         const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
         hi = *reinterpret_cast<const uint32_t*>(&h);
         lo = 0u;
     } else {
         const float s0 = x0 * kHalfScale, s1 = x1 * kHalfScale;
-        const __half2 h = __floats2half2_rn(s0, s1);
+        const __half2 h = (MODE == kModeF32E && fixed)
+                              ? __floats2half2_rn(rintf(s0 * 0.125f) * 8.0f, rintf(s1 * 0.125f) * 8.0f)
+                              : __floats2half2_rn(s0, s1);
         hi = *reinterpret_cast<const uint32_t*>(&h);
         if constexpr (MODE == kModeF32E) {
             const float2 f = __half22float2(h);
@@ -202,8 +208,8 @@ __device__ __forceinline__ void epi_sub_mid(const uint32_t (&v)[16], float* Xt, 
             __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
             __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
         }
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
     }
     if (!dblk) {
         sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
@@ -280,8 +286,8 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
                 __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
             red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
         }
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
     }
     if (!dblk) {
         sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
@@ -409,8 +415,8 @@ __device__ __forceinline__ void epi_sub_mid_pre(const uint32_t (&v)[16], const f
         }
         __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
         __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
     }
     if (!dblk) {
         sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
@@ -515,8 +521,8 @@ __device__ __forceinline__ void epi_oct_mid_y(const float (&y)[8], float* Xt, fl
         }
         __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
         __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j]);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1]);
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
     }
     const int ch = (c0 & 31) >> 3;
     if (!dblk) {

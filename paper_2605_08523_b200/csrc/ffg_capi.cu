@@ -447,6 +447,16 @@ int semi_drain_layers() {
     return v;
 }
 
+// K16 steps per hi*hi chunk after the exact layers: 4, 8 or 16 (one, two or four K-blocks)
+int normal_kstep() {
+    static int v = [] {
+        const char* e = getenv("FFG_NORMAL_KSTEP");
+        const int k = e ? atoi(e) : 8;  // measured: 8 as fast as 16, inside the gates with margin
+        return (k == 4 || k == 16) ? k : 8;
+    }();
+    return v;
+}
+
 int debug_flags() {
     static int v = [] {
         const char* e = getenv("FFG_DEBUG_K2");
@@ -530,7 +540,8 @@ unsigned long long* g_prof_buf = nullptr;  // FFG_DEBUG_K2 & 8: per-CTA role wai
 int k2_impl() {
     static int v = [] {
         const char* e = getenv("FFG_K2");
-        return e ? atoi(e) : 2;
+        // the per-layer kernel has no lo*lo product, which the fixed-point split needs
+        return (e && !FFG_FIXED_SPLIT) ? atoi(e) : 2;
     }();
     return v;
 }
@@ -770,6 +781,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     rp.np = (int)np;
     rp.mode = j.mode;
     rp.write_operands = 1;
+    rp.fixed = (pair && FFG_FIXED_SPLIT && j.mode == kModeF32E && exact_drain_layers() > 0) ? 1 : 0;
     rp.xa_used = pair ? w.xa_used : nullptr;   // the per-layer kernel reads every upper block
     rescale_tiles_kernel<<<dim3((unsigned)(np / kK1Rows), (unsigned)B), 256, 0, st>>>(rp);
     CK(cudaGetLastError());
@@ -800,6 +812,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         pp.n_layers = md.n_layers;
         pp.exact_layers = exact_drain_layers();
         pp.semi_layers = semi_drain_layers();
+        pp.normal_kstep = normal_kstep();
         pp.dbg = debug_flags();
         if (pp.dbg & 8) {
             static unsigned long long* prof = nullptr;

@@ -128,6 +128,12 @@ static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue war
 #ifndef FFG_DRAIN_DEP
 #define FFG_DRAIN_DEP 1  // order drain batches (see the drain loop)
 #endif
+#ifndef FFG_FIXED_SPLIT
+#define FFG_FIXED_SPLIT 1  // FP32E: fixed-point hi (exact hi*hi accumulation), two accumulators per item
+#endif
+#ifndef FFG_FIXED_LOLO
+#define FFG_FIXED_LOLO 1  // (with FFG_FIXED_SPLIT) the fourth product lo*lo into the cross accumulator
+#endif
 #ifndef FFG_EXACT_K16
 #define FFG_EXACT_K16 1  // K16 steps per chunk in exact-drain layers (1 or 2)
 #endif
@@ -136,11 +142,17 @@ __host__ __device__ constexpr int pair_chunks(int mode, int nk, bool exact) {
 }
 // K16 steps per chunk of layer l: FFG_EXACT_K16 in the exact-drain layers, 2 in the following
 // `semi_layers`, a whole K-block (4) after that
-__host__ __device__ constexpr int layer_kstep(int l, int exact_layers, int semi_layers) {
-    return l < exact_layers ? FFG_EXACT_K16 : (l < exact_layers + semi_layers ? 2 : kBK / kUK);
+__host__ __device__ constexpr int layer_kstep(int l, int exact_layers, int semi_layers, int normal_kstep) {
+    return l < exact_layers ? (FFG_FIXED_SPLIT ? 0 : FFG_EXACT_K16)
+                            : (l < exact_layers + semi_layers ? 2 : normal_kstep);
 }
 __host__ __device__ constexpr int layer_chunks(int mode, int nk, int kstep) {
-    return mode == kModeF32E ? nk * (kBK / kUK) / kstep : 1;
+    // kstep 0: fixed-point exact layer, two whole-K accumulators (hi*hi, cross terms); a chunk of
+    // several K-blocks ends early at the last K-block
+    return mode != kModeF32E ? 1
+           : kstep == 0      ? 2
+           : kstep <= kBK / kUK ? nk * (kBK / kUK) / kstep
+                                : (nk + kstep / (kBK / kUK) - 1) / (kstep / (kBK / kUK));
 }
 
 struct PairMaps {
@@ -165,6 +177,7 @@ struct PairParams {
     int l0, l1, n_layers;     // layers of this launch, model depth
     int exact_layers;
     int semi_layers;          // layers after the exact ones draining every 2 K16 steps
+    int normal_kstep;         // K16 steps per chunk in the remaining layers (4: one K-block, 8: two)
     int dbg;                  // measurement only: 1 skip epilogue math, 2 skip loads/MMAs,
                               // 4 skip dependency waits, 8 per-role wait cycles -> prof,
                               // 16 skip operand loads, 32 skip hi/lo stores, 64 skip X/A
@@ -258,7 +271,7 @@ __device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t t
     for (int item = pair_id; item < total; item += n_pairs) {
         const int l = l_first + (item - pair_id) / n_pairs;
         const bool last = (l == p.n_layers - 1);
-        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
+        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
         int ysl = 0;
         {
             float yacc[32];
@@ -295,7 +308,8 @@ __device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t t
             }
         }
         // ------------------------------------------------------------- epilogue of layer l
-        const EpiCoef k = load_coef(p.coef, l, last);
+        EpiCoef k = load_coef(p.coef, l, last);
+        k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
         EpiHealth hl;
         double tr = 0.0, sq = 0.0;
         const bool work = !skip && !(p.dbg & 1);
@@ -343,7 +357,7 @@ __device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t t
                 uint32_t hp[8], lp[8];
 #pragma unroll
                 for (int e = 0; e < 16; e += 2)
-                    split2<MODE>(__uint_as_float(xv[e]), __uint_as_float(xv[e + 1]), hp[e >> 1], lp[e >> 1]);
+                    split2<MODE>(__uint_as_float(xv[e]), __uint_as_float(xv[e + 1]), hp[e >> 1], lp[e >> 1], k.fixed);
                 // row segment into the staging pieces (hi at +0, lo at +2 KB; row = lane)
                 sts_v4(stg + sw64(lane, 2 * h + 0), hp[0], hp[1], hp[2], hp[3]);
                 sts_v4(stg + sw64(lane, 2 * h + 1), hp[4], hp[5], hp[6], hp[7]);
@@ -472,7 +486,7 @@ __device__ __forceinline__ void two_group_workers(const PairMaps& tm, const Pair
     for (int item = pair_id; item < total; item += n_pairs, ++u) {
         int m, l, pi;
         pair_decode(p, item, m, l, pi);
-        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
+        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
         if ((u & 1) != grp) {
             g += chunks;
             continue;
@@ -519,7 +533,8 @@ __device__ __forceinline__ void two_group_workers(const PairMaps& tm, const Pair
         const bool diag = R == C;
         const int gi = R * kBM + r;
         const bool c_on = gi < n;
-        const EpiCoef k = load_coef(p.coef, l, last);
+        EpiCoef k = load_coef(p.coef, l, last);
+        k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
         const int nxt = (l + 1) & 1;
         float* Xt = p.X + xa_tile_base(m, R, C, nb);
         float* At = p.A + xa_tile_base(m, R, C, nb);
@@ -649,7 +664,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
     for (int item = pair_id; item < total; item += n_pairs) {
         int m, l, pi;
         pair_decode(p, item, m, l, pi);
-        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
+        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
         float yacc[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) yacc[e] = 0.0f;
@@ -684,7 +699,8 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
         const bool dblk = diag && c == q;
         const int gi = R * kBM + r;
         const bool c_on = gi < n;
-        const EpiCoef k = load_coef(p.coef, l, last);
+        EpiCoef k = load_coef(p.coef, l, last);
+        k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
         const int nxt = (l + 1) & 1;
         float* Xt = p.X + xa_tile_base(m, R, C, nb);
         float* At = p.A + xa_tile_base(m, R, C, nb);
@@ -1010,8 +1026,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             for (int item = pair_id; item < total; item += n_pairs) {
                 int m, l, pi;
                 pair_decode(p, item, m, l, pi);
-                const int kst = layer_kstep(l, p.exact_layers, p.semi_layers);
-                const bool exact = kst < kBK / kUK;
+                const int kst = layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep);
+                const bool exact = kst != 0 && kst < kBK / kUK;
                 uint32_t t_slot = 0;
                 auto open_slot = [&]() {
                     const int sl = g % kSlots;
@@ -1026,13 +1042,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 };
                 // descriptor of (stage base + byte offset): the start address field is addr>>4
                 auto D = [&](uint64_t sbase, uint32_t off) { return sbase + (off >> 4); };
+                // FFG_FIXED_SPLIT: hi*hi over the whole K in one accumulator (exact: every product
+                // and partial sum lies on the 2^6 grid of the fixed-point hi, |sum| < 2^30), the cross
+                // terms in a second; the drain adds the two once
+                const bool kFixed = kDrain && kst == 0;
+                uint32_t t_hh = 0, t_x = 0;
+                if (kFixed) {
+                    const int s0 = g % kSlots, s1 = (g + 1) % kSlots;
+                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[s0], ((g / kSlots) & 1) ^ 1));
+                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[s1], (((g + 1) / kSlots) & 1) ^ 1));
+                    tc_fence_after();
+                    t_hh = tmem + s0 * 128;
+                    t_x = tmem + s1 * 128;
+                }
                 if (!kDrain) open_slot();
                 for (int kb = 0; kb < ((p.dbg & 2) ? 0 : nk); ++kb, ++it) {
                     const int s = it % S;
                     FFG_TIMED(w_full, mbar_wait(&full[s], (it / S) & 1));
                     tc_fence_after();
                     const uint64_t sb = desc0 + (uint64_t)((s * Cfg::kStageBytes) >> 4);
-                    if (!kDrain) {
+                    if (kFixed) {
+                        if (elect_one_sync()) {
+#pragma unroll
+                            for (int kk = 0; kk < kBK / kUK; ++kk) {
+                                const uint32_t koff = kk * kUK * 2;
+                                umma_f16_pair(t_x, D(sb, koff), D(sb, offBlo + koff), idesc, (kb | kk) != 0);
+                                umma_f16_pair(t_x, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
+                                if (FFG_FIXED_LOLO)  // lo*lo: the fixed-point lo is absolute (~2^-12), not negligible
+                                    umma_f16_pair(t_x, D(sb, offAlo + koff), D(sb, offBlo + koff), idesc, 1u);
+                                umma_f16_pair(t_hh, D(sb, koff), D(sb, offBhi + koff), idesc, (kb | kk) != 0);
+                            }
+                        }
+                        __syncwarp();
+                    } else if (!kDrain) {
 #pragma unroll
                         for (int kk = 0; kk < kBK / kUK; ++kk) {
                             const uint32_t koff = kk * kUK * 2;
@@ -1068,12 +1110,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         else
                             issue(std::integral_constant<int, 2>{});
                     } else {
-                        open_slot();
+                        const int kbc = kst / (kBK / kUK);  // K-blocks per chunk
+                        const bool first = kb % kbc == 0;
+                        if (first) open_slot();
                         if (elect_one_sync()) {
 #pragma unroll
                             for (int kk = 0; kk < kBK / kUK; ++kk) {
                                 const uint32_t koff = kk * kUK * 2;
-                                umma_f16_pair(t_slot, D(sb, koff), D(sb, offBlo + koff), idesc, kk != 0);
+                                umma_f16_pair(t_slot, D(sb, koff), D(sb, offBlo + koff), idesc, !(first && kk == 0));
                                 umma_f16_pair(t_slot, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
                             }
 #pragma unroll
@@ -1083,12 +1127,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                             }
                         }
                         __syncwarp();
-                        close_slot();
+                        if (kb % kbc == kbc - 1 || kb == nk - 1) close_slot();
                     }
                     if (elect_one_sync()) umma_commit_pair(&empty[s]);
                     __syncwarp();
                 }
-                if (!kDrain || (p.dbg & 2)) {
+                if (kFixed) {
+                    if (elect_one_sync()) {
+                        umma_commit_pair(&slot_full[g % kSlots]);
+                        umma_commit_pair(&slot_full[(g + 1) % kSlots]);
+                    }
+                    __syncwarp();
+                    g += 2;
+                } else if (!kDrain || (p.dbg & 2)) {
                     if (kDrain) open_slot();
                     close_slot();
                 }
@@ -1128,7 +1179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             for (int item = pair_id; item < total; item += n_pairs, ++u) {
                 int m, l, pi;
                 pair_decode(p, item, m, l, pi);
-                const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
+                const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
                 float yacc[kEpiCols];
     #pragma unroll
                 for (int e = 0; e < kEpiCols; ++e) yacc[e] = 0.0f;
@@ -1215,9 +1266,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const int C = (pr >> 20) & 1023;                     // block cols (B panel)
             const bool dummy = rank && ((pr >> 30) & 1);
             const bool last = (l == p.n_layers - 1);
-            const EpiCoef k = load_coef(p.coef, l, last);
+            EpiCoef k = load_coef(p.coef, l, last);
+        k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
             const int nxt = (l + 1) & 1;   // hi/lo parity written by this layer
-            g += (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers));
+            g += (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
             const int ysl = (g - 1) & 3;   // slot holding this item's Y
             const bool diag = R == C;
             const int gi = R * kBM + r;

@@ -80,14 +80,17 @@ constexpr int layer_smem_bytes() {
 }
 
 // 16-bit operand encodings (raw bits) -------------------------------------------------
+#ifndef FFG_FIXED_SPLIT
+#define FFG_FIXED_SPLIT 1  // FP32E exact layers: fixed-point hi instead of per-K16 drains (k2_pair.cuh)
+#endif
 template <int MODE>
-__device__ __forceinline__ void split16(float x, uint16_t& hi, uint16_t& lo) {
+__device__ __forceinline__ void split16(float x, uint16_t& hi, uint16_t& lo, bool fixed = false) {
     if constexpr (MODE == kModeBF16) {
         hi = __bfloat16_as_ushort(__float2bfloat16_rn(x));
         lo = 0;
     } else {
         const float xs = x * kHalfScale;
-        const __half h = __float2half_rn(xs);
+        const __half h = __float2half_rn((MODE == kModeF32E && fixed) ? rintf(xs * 0.125f) * 8.0f : xs);
         hi = __half_as_ushort(h);
         if constexpr (MODE == kModeF32E) {
             lo = __half_as_ushort(__float2half_rn(xs - __half2float(h)));
@@ -126,6 +129,7 @@ struct RescaleParams {
     int* flags;                 // [B][2] first bad X_k index: [0] non-finite, [1] half range
     int n, np, mode, write_operands;
     const uint8_t* xa_used;     // [nb][nb] blocks whose X/A K2 reads (null: all blocks)
+    int fixed;                  // FP32E: fixed-point hi split of X0 (layer 0 is an exact layer)
 };
 
 // One warp per row; 8 rows per CTA; grid (np/8, B).
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(256) rescale_gershgorin_kernel(const __grid_co
                 } else {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        split16<kModeF32E>(x[e], hb[e], lb[e]);
+                        split16<kModeF32E>(x[e], hb[e], lb[e], p.fixed != 0);
                         bad_hr |= half_range_bad<kModeF32E>(x[e]);
                     }
                 }
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
                 } else {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        split16<kModeF32E>(x[e], hb[e], lb[e]);
+                        split16<kModeF32E>(x[e], hb[e], lb[e], p.fixed != 0);
                         bad_hr |= half_range_bad<kModeF32E>(x[e]);
                     }
                 }
