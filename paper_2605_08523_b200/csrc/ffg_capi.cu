@@ -606,7 +606,7 @@ int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaS
 template <int V>
 int pair_capacity_mode(int mode, int* cap) {
     switch (mode) {
-        case kModeF32E: return pair_capacity<kModeF32E, V == 2 ? 0 : V>(cap);
+        case kModeF32E: return pair_capacity<kModeF32E, V>(cap);
         case kModeF16: return pair_capacity<kModeF16, V>(cap);
         default: return pair_capacity<kModeBF16, V>(cap);
     }
@@ -614,19 +614,21 @@ int pair_capacity_mode(int mode, int* cap) {
 template <int V>
 int launch_pair_mode(int mode, const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
     switch (mode) {
-        case kModeF32E: return launch_pair<kModeF32E, V == 2 ? 0 : V>(maps, pp, items, st);
+        case kModeF32E: return launch_pair<kModeF32E, V>(maps, pp, items, st);
         case kModeF16: return launch_pair<kModeF16, V>(maps, pp, items, st);
         default: return launch_pair<kModeBF16, V>(maps, pp, items, st);
     }
 }
 
-// Single-product modes at np <= 512: sixteen drain+epilogue workers (no separate drain pass
-// exists there, and each worker finishes one 32-column piece) measured 18% faster at 64 x N=512;
-// equal at N=1024, 6% slower at N=4096.  FFG_S16=0/1 overrides.
+// np <= 512: sixteen drain+epilogue workers, each finishing one 32-column piece straight from its
+// registers (Y never holds a TMEM slot).  Measured: 512 x N=512 BF16 -24%, FP32E -6%; 64 x N=256 FP32E
+// -18%; slower at N >= 1024 (the MMA starves while all sixteen warps are in the epilogue).  FFG_S16=0/1
+// overrides.
 bool use_s16(int mode, int64_t np) {
     const char* e = getenv("FFG_S16");
-    if (e) return mode != kModeF32E && atoi(e) != 0;
-    return mode != kModeF32E && np <= 512;
+    if (e) return atoi(e) != 0;
+    (void)mode;
+    return np <= 512;
 }
 
 // Resident K2 (one block per CTA for the whole recursion, k2_pair.cuh resident_workers) when
