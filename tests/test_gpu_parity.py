@@ -442,3 +442,22 @@ def test_schedule_invariance(model, monkeypatch):
         assert all(np.array_equal(a, b) for a, b in zip(Db, ref_b)), env
         assert [(s.trace, s.trace_square) for s in sb] == [(s.trace, s.trace_square) for s in st_b], env
         assert np.array_equal(D1, ref_1) and (s1.trace, s1.trace_square) == (st_1.trace, st_1.trace_square), env
+
+
+def test_fp32e_gates_at_n2048_vs_fp64_recursion(model):
+    """The FP32-emulated gates hold at a size where an absolute (fixed-point) lo error would show up
+    in the Frobenius norm: N=2048 vs the same MLSP2 recursion in fp64 (torch float64 GEMMs on the
+    device, test-side reference only)."""
+    import torch
+    n = 2048
+    H = tight_binding(n, seed=4242)
+    D, st, _ = E.compute_density_matrix(H, 0.0, 0.01, model, E.PrecisionMode.MIXED_EMULATED)
+    Hd = torch.from_numpy(H).cuda()
+    I = torch.eye(n, dtype=torch.float64, device=Hd.device)
+    X = (1.0 - model.mu0) * I - ((1.0 / 0.01) / model.beta0) * Hd
+    A = torch.zeros_like(X)
+    for a, b, c, d in model.abcd:
+        A = A + d * X
+        X = a * (X @ X) + b * X + c * I
+    R = (A + X).cpu().numpy()
+    check(D, R, E.PrecisionMode.MIXED_EMULATED)
