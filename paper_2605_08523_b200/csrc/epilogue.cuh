@@ -15,15 +15,18 @@ namespace ffg {
 
 struct EpiCoef {
     float a_hi, a_lo, b_hi, b_lo, c_hi, c_lo, d_hi, d_lo;
-    bool fixed;  // split X' with the fixed-point hi (the next layer accumulates hi*hi exactly)
+    float dc_hi, dc_lo;  // paired A updates: this layer's d, applied to the input X (0: none)
+    bool red;            // this layer adds (dc X + d X') into A
+    bool fixed;          // split X' with the fixed-point hi (the next layer accumulates hi*hi exactly)
 };
 
-// Layer l's coefficients as hi/lo fp32 pairs {a_hi, a_lo, b_hi, b_lo, c_hi, c_lo, d_hi, d_lo}, split on
-// the host from the fp64 model (hi = rn_f32(v), lo = rn_f32(v - hi)); d is the NEXT layer's d (0 after
-// the last layer), the accumulate that follows this layer's X'.
+// Layer l's coefficients as hi/lo fp32 pairs, split on the host from the fp64 model (hi = rn_f32(v),
+// lo = rn_f32(v - hi)): {a, b}, {c, d'}, {dc, red}.  d' multiplies the layer's output X', dc its input
+// X; with paired A updates (host: FFG_A_PAIR) only every other layer reduces into A, adding
+// d_l X_l + d_{l+1} X_{l+1} at once (dc = d' = 0 and red = 0 in the others).
 __device__ __forceinline__ EpiCoef load_coef(const float4* coef, int l, bool /*last*/) {
-    const float4 u = __ldg(coef + 2 * l), w = __ldg(coef + 2 * l + 1);
-    return EpiCoef{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w, false};
+    const float4 u = __ldg(coef + 3 * l), w = __ldg(coef + 3 * l + 1), z = __ldg(coef + 3 * l + 2);
+    return EpiCoef{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w, z.x, z.y, z.z != 0.0f, false};
 }
 
 #ifndef FFG_EPI_EFT
@@ -278,13 +281,13 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
                 xn = poly_step<false>(y, xs[e], k);
                 hl.add(xn);
             }
-            ts[e] = acc_term(xn, k);
+            ts[e] = acc_term(xn, k) + fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]);
             xs[e] = xn;
         }
         if (!nomem) {  // (measurement only: dbg & 64)
             if (store_x)
                 __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
-            red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
+            if (k.red) red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
         }
         split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
         split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
@@ -360,7 +363,7 @@ __device__ __forceinline__ void epi_sub_last_x(const uint32_t (&v)[16], const fl
             const bool own = !DIAG || cl >= r;
             if (own) hl.add(xn);
             if (own && gi < n && gj < n) {
-                const double dv = (double)as[e] + (double)xn;
+                const double dv = (double)as[e] + (double)fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]) + (double)xn;
                 if (Dm) {
                     Dm[(size_t)gi * n + gj] = dv;
                     if (!dg) Dm[(size_t)gj * n + gi] = dv;
@@ -467,7 +470,7 @@ __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const floa
             const bool own = !DIAG || cl >= r;
             if (own) hl.add(xn);
             if (own && gi < n && gj < n) {
-                const double dv = (double)as[e] + (double)xn;
+                const double dv = (double)as[e] + (double)fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]) + (double)xn;
                 if (Dm) {
                     Dm[(size_t)gi * n + gj] = dv;
                     if (!dg) Dm[(size_t)gj * n + gi] = dv;
@@ -568,7 +571,7 @@ __device__ __forceinline__ void epi_oct_last_y(const float (&y)[8], const float*
             const bool own = !DIAG || cl >= r;
             if (own) hl.add(xn);
             if (own && gi < n && gj < n) {
-                const double dv = (double)as[e] + (double)xn;
+                const double dv = (double)as[e] + (double)fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]) + (double)xn;
                 if (Dm) {
                     Dm[(size_t)gi * n + gj] = dv;
                     if (!dg) Dm[(size_t)gj * n + gi] = dv;

@@ -171,7 +171,7 @@ struct PairParams {
     uint32_t* bflags;         // [B][nb][nb] block completion counts, index min*nb+max (FFG_BLOCK_DEPS)
     int blockdeps;            // 1: producer waits per block while a panel is incomplete (host: G == 1)
     const uint32_t* pairs;    // [PT]  A0 | A1 << 10 | S << 20 | dummy << 30
-    const float4* coef;       // [n_layers][2] hi/lo fp32 a, b, c, d_next (host-split, epilogue.cuh)
+    const float4* coef;       // [n_layers][3] hi/lo fp32 a, b, c, d_next, d_cur, red (epilogue.cuh)
     int n, np, nb, PT;
     int B, G;                 // matrices, group size
     int l0, l1, n_layers;     // layers of this launch, model depth
