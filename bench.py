@@ -327,7 +327,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": {"MIXED_EMULATED": "f32-emulated (f16 hi/lo x3 products, f32 accumulate)",
+            "dtype": {"MIXED_EMULATED": "f32-emulated (binary16 hi/lo split, 3 tensor-core products; 4 with an exact fixed-point hi*hi accumulator in the first 10 layers; f32 accumulate)",
                       "BF16": "bf16 (f32 accumulate)", "FP16": "f16 (f32 accumulate)"}[args.mode],
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "n": n, "batch_per_gpu": B, "global_batch": B * world,
