@@ -163,87 +163,10 @@ struct EpiHealth {
     }
 };
 
-// One 16-column sub-block (columns c0..c0+15 of the 128x128 block) of this thread's row r,
-// mid-recursion layer: X/A in place, hi/lo into the warp's 32x32 direct staging piece
-// (`stg_d`: hi at +0, lo at +kPieceBytes; row = lane).  The mirrored piece is produced
-// afterwards by the warp (transpose_piece).  DIAG: the block is on the matrix diagonal; only
-// columns >= r are owned (the rest is the mirror of owned values) and the identity term is
-// added at column r.  dblk: the 32x32 piece itself is on the diagonal and is completed
-// symmetrically in place.
-template <int MODE, bool DIAG>
-__device__ __forceinline__ void epi_sub_mid(const uint32_t (&v)[16], float* Xt, float* At, int r,
-                                            int c0, int lane, int sub, bool c_on, const EpiCoef& k,
-                                            uint32_t stg_d, bool dblk, EpiHealth& hl,
-                                            bool nomem = false) {
-    using Tr = ModeTraits<MODE>;
-    float4 xq[4], aq[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (nomem) {  // measurement only
-            xq[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            aq[j] = xq[j];
-            continue;
-        }
-        xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
-        aq[j] = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
-    }
-    uint32_t hp[8], lp[8];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
-        float as[4] = {aq[j].x, aq[j].y, aq[j].z, aq[j].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float y = __uint_as_float(v[4 * j + e]);
-            float xn;
-            if constexpr (DIAG) {
-                const int cl = c0 + 4 * j + e;
-                xn = (cl == r && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
-                if (cl >= r) hl.add(xn);
-            } else {
-                xn = poly_step<false>(y, xs[e], k);
-                hl.add(xn);
-            }
-            as[e] = acc_step(as[e], xn, k);
-            xs[e] = xn;
-        }
-        if (!nomem) {
-            __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
-            __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
-        }
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
-    }
-    if (!dblk) {
-        sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
-        sts_v4(stg_d + sw64(lane, 2 * sub + 1), hp[4], hp[5], hp[6], hp[7]);
-        if (Tr::kHasLo) {
-            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 0), lp[0], lp[1], lp[2], lp[3]);
-            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 1), lp[4], lp[5], lp[6], lp[7]);
-        }
-    } else {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const uint32_t col = 16 * sub + e;
-            if ((int)col < lane) continue;
-            const uint16_t hb = (uint16_t)(hp[e >> 1] >> (16 * (e & 1)));
-            const uint16_t lb = (uint16_t)(lp[e >> 1] >> (16 * (e & 1)));
-            const uint32_t off = sw64(col, lane >> 3) + (lane & 7) * 2;
-            const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
-            sts_u16(stg_d + off, hb);
-            sts_u16(stg_d + doff, hb);
-            if (Tr::kHasLo) {
-                sts_u16(stg_d + kPieceBytes + off, lb);
-                sts_u16(stg_d + kPieceBytes + doff, lb);
-            }
-        }
-    }
-}
-
-// FFG_A_RED: A' = A + d'X' as a fire-and-forget vector reduction at L2 (no read of A, no round
-// trip; every element receives exactly one add per layer, so the result is deterministic).  The
-// sum d'X' is formed in fp32 from the hi/lo coefficient (one more rounding than acc_step's fused
-// form; both ~1 ulp).
+// A' = A + d'X' as a fire-and-forget vector reduction at L2 (no read of A, no round trip; every
+// element receives at most one add per layer, so the result is deterministic).  The sum d'X' is
+// formed in fp32 from the hi/lo coefficient (one more rounding than acc_step's fused form; both
+// ~1 ulp).
 __device__ __forceinline__ void red_add_v4(float* gp, float a, float b, float c, float d) {
     asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gp), "f"(a), "f"(b), "f"(c),
                  "f"(d)
@@ -257,12 +180,17 @@ __device__ __forceinline__ void epi_loadx16(const float* Xt, int r, int c0, floa
     for (int j = 0; j < 4; ++j) xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
 }
 
-// epi_sub_mid with X already in registers and A updated by reduction (FFG_A_RED)
+// One 16-column sub-block (columns c0..c0+15 of the 128x128 block) of this thread's row r,
+// mid-recursion layer, X already in registers: X stored, A updated by reduction, hi/lo into the warp's 32x32 direct staging piece
+// (`stg_d`: hi at +0, lo at +kPieceBytes; row = lane).  The mirrored piece is produced
+// afterwards by the warp (transpose_piece).  DIAG: the block is on the matrix diagonal; only
+// columns >= r are owned (the rest is the mirror of owned values) and the identity term is
+// added at column r.  dblk: the 32x32 piece itself is on the diagonal and is completed
+// symmetrically in place.
 template <int MODE, bool DIAG>
 __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const float4 (&xq)[4], float* Xt, float* At,
                                                 int r, int c0, int lane, int sub, bool c_on, const EpiCoef& k,
-                                                uint32_t stg_d, bool dblk, EpiHealth& hl, bool nomem = false,
-                                                bool store_x = true) {
+                                                uint32_t stg_d, bool dblk, EpiHealth& hl, bool nomem = false) {
     using Tr = ModeTraits<MODE>;
     uint32_t hp[8], lp[8];
 #pragma unroll
@@ -285,139 +213,9 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
             xs[e] = xn;
         }
         if (!nomem) {  // (measurement only: dbg & 64)
-            if (store_x)
-                __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
+            __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
             if (k.red) red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
         }
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
-    }
-    if (!dblk) {
-        sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
-        sts_v4(stg_d + sw64(lane, 2 * sub + 1), hp[4], hp[5], hp[6], hp[7]);
-        if (Tr::kHasLo) {
-            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 0), lp[0], lp[1], lp[2], lp[3]);
-            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 1), lp[4], lp[5], lp[6], lp[7]);
-        }
-    } else {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const uint32_t col = 16 * sub + e;
-            if ((int)col < lane) continue;
-            const uint16_t hb = (uint16_t)(hp[e >> 1] >> (16 * (e & 1)));
-            const uint16_t lb = (uint16_t)(lp[e >> 1] >> (16 * (e & 1)));
-            const uint32_t off = sw64(col, lane >> 3) + (lane & 7) * 2;
-            const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
-            sts_u16(stg_d + off, hb);
-            sts_u16(stg_d + doff, hb);
-            if (Tr::kHasLo) {
-                sts_u16(stg_d + kPieceBytes + off, lb);
-                sts_u16(stg_d + kPieceBytes + doff, lb);
-            }
-        }
-    }
-}
-
-// FFG_X_HILO (FP32-emulated): X of 16 columns rebuilt from the binary16 hi/lo operand row the previous
-// layer stored (x = (hi + lo) 2^-14, exact in fp32: ~22 significant bits, the same X the MMA squares), so
-// K2 never stores or reads the fp32 X blocks.  hrow/lrow point at column c0 of the thread's row.
-__device__ __forceinline__ void epi_loadx16_hilo(const uint16_t* hrow, const uint16_t* lrow, float4 (&xq)[4]) {
-    uint4 h[2], q[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        h[i] = __ldcg(reinterpret_cast<const uint4*>(hrow) + i);
-        q[i] = __ldcg(reinterpret_cast<const uint4*>(lrow) + i);
-    }
-    const uint32_t hw[8] = {h[0].x, h[0].y, h[0].z, h[0].w, h[1].x, h[1].y, h[1].z, h[1].w};
-    const uint32_t lw[8] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w};
-    float v[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&hw[i]));
-        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&lw[i]));
-        v[2 * i + 0] = (a.x + b.x) * (1.0f / kHalfScale);
-        v[2 * i + 1] = (a.y + b.y) * (1.0f / kHalfScale);
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) xq[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-}
-
-// last layer with X already in registers (FFG_X_HILO)
-template <bool DIAG>
-__device__ __forceinline__ void epi_sub_last_x(const uint32_t (&v)[16], const float4 (&xq)[4], const float* At,
-                                               int r, int c0, int gi, int gj0, int n, bool c_on,
-                                               const EpiCoef& k, double* Dm, EpiHealth& hl, double& tr,
-                                               double& sq) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const float4 aq = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
-        const float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
-        const float as[4] = {aq.x, aq.y, aq.z, aq.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int cl = c0 + 4 * j + e;
-            const int gj = gj0 + cl;
-            const float y = __uint_as_float(v[4 * j + e]);
-            const bool dg = DIAG && cl == r;
-            const float xn = (dg && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
-            const bool own = !DIAG || cl >= r;
-            if (own) hl.add(xn);
-            if (own && gi < n && gj < n) {
-                const double dv = (double)as[e] + (double)fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]) + (double)xn;
-                if (Dm) {
-                    Dm[(size_t)gi * n + gj] = dv;
-                    if (!dg) Dm[(size_t)gj * n + gi] = dv;
-                }
-                if (dg) {
-                    tr += dv;
-                    sq += dv * dv;
-                } else {
-                    sq += 2.0 * dv * dv;
-                }
-            }
-        }
-    }
-}
-
-// X/A of 16 columns (c0 .. c0+15) of row r: four float4 each.
-__device__ __forceinline__ void epi_load16(const float* Xt, const float* At, int r, int c0, float4 (&xq)[4],
-                                           float4 (&aq)[4]) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
-        aq[j] = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
-    }
-}
-
-// epi_sub_mid on X/A already in registers (the caller loads the next sub-block first)
-template <int MODE, bool DIAG>
-__device__ __forceinline__ void epi_sub_mid_pre(const uint32_t (&v)[16], const float4 (&xq)[4],
-                                                const float4 (&aq)[4], float* Xt, float* At, int r, int c0,
-                                                int lane, int sub, bool c_on, const EpiCoef& k, uint32_t stg_d,
-                                                bool dblk, EpiHealth& hl) {
-    using Tr = ModeTraits<MODE>;
-    uint32_t hp[8], lp[8];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
-        float as[4] = {aq[j].x, aq[j].y, aq[j].z, aq[j].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float y = __uint_as_float(v[4 * j + e]);
-            float xn;
-            if constexpr (DIAG) {
-                const int cl = c0 + 4 * j + e;
-                xn = (cl == r && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
-                if (cl >= r) hl.add(xn);
-            } else {
-                xn = poly_step<false>(y, xs[e], k);
-                hl.add(xn);
-            }
-            as[e] = acc_step(as[e], xn, k);
-            xs[e] = xn;
-        }
-        __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
-        __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
         split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
         split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
     }
@@ -486,105 +284,5 @@ __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const floa
     }
 }
 
-
-// Eight columns (c0..c0+7, c0 a multiple of 8) of row r from Y values already in registers
-// (two-group workers): X/A in place, hi/lo into the 16-byte chunk (c0 & 31) / 8 of the warp's
-// direct 32x32 pieces (hi at stg, lo at stg + kPieceBytes); dblk: symmetric completion of a
-// diagonal piece in place.
-template <int MODE, bool DIAG>
-__device__ __forceinline__ void epi_oct_mid_y(const float (&y)[8], float* Xt, float* At, int r, int c0, int lane,
-                                              bool c_on, const EpiCoef& k, uint32_t stg, bool dblk,
-                                              EpiHealth& hl) {
-    using Tr = ModeTraits<MODE>;
-    float4 xq[2], aq[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
-        aq[j] = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
-    }
-    uint32_t hp[4], lp[4];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
-        float as[4] = {aq[j].x, aq[j].y, aq[j].z, aq[j].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            float xn;
-            if constexpr (DIAG) {
-                const int cl = c0 + 4 * j + e;
-                xn = (cl == r && c_on) ? poly_step<true>(y[4 * j + e], xs[e], k)
-                                       : poly_step<false>(y[4 * j + e], xs[e], k);
-                if (cl >= r) hl.add(xn);
-            } else {
-                xn = poly_step<false>(y[4 * j + e], xs[e], k);
-                hl.add(xn);
-            }
-            as[e] = acc_step(as[e], xn, k);
-            xs[e] = xn;
-        }
-        __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
-        __stcg(reinterpret_cast<float4*>(At + xa_off(r, c0 / 4 + j)), make_float4(as[0], as[1], as[2], as[3]));
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
-    }
-    const int ch = (c0 & 31) >> 3;
-    if (!dblk) {
-        sts_v4(stg + sw64(lane, ch), hp[0], hp[1], hp[2], hp[3]);
-        if (Tr::kHasLo) sts_v4(stg + kPieceBytes + sw64(lane, ch), lp[0], lp[1], lp[2], lp[3]);
-    } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const uint32_t col = 8 * ch + e;
-            if ((int)col < lane) continue;
-            const uint16_t hb = (uint16_t)(hp[e >> 1] >> (16 * (e & 1)));
-            const uint16_t lb = (uint16_t)(lp[e >> 1] >> (16 * (e & 1)));
-            const uint32_t off = sw64(col, lane >> 3) + (lane & 7) * 2;
-            const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
-            sts_u16(stg + off, hb);
-            sts_u16(stg + doff, hb);
-            if (Tr::kHasLo) {
-                sts_u16(stg + kPieceBytes + off, lb);
-                sts_u16(stg + kPieceBytes + doff, lb);
-            }
-        }
-    }
-}
-
-// Last layer from register Y: D = A + X_L (fp64) and the owned elements' statistics; 8 columns.
-template <bool DIAG>
-__device__ __forceinline__ void epi_oct_last_y(const float (&y)[8], const float* Xt, const float* At, int r,
-                                               int c0, int gi, int gj0, int n, bool c_on, const EpiCoef& k,
-                                               double* Dm, EpiHealth& hl, double& tr, double& sq) {
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const float4 xq = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
-        const float4 aq = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
-        const float xs[4] = {xq.x, xq.y, xq.z, xq.w};
-        const float as[4] = {aq.x, aq.y, aq.z, aq.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int cl = c0 + 4 * j + e;
-            const int gj = gj0 + cl;
-            const bool dg = DIAG && cl == r;
-            const float xn = (dg && c_on) ? poly_step<true>(y[4 * j + e], xs[e], k)
-                                          : poly_step<false>(y[4 * j + e], xs[e], k);
-            const bool own = !DIAG || cl >= r;
-            if (own) hl.add(xn);
-            if (own && gi < n && gj < n) {
-                const double dv = (double)as[e] + (double)fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]) + (double)xn;
-                if (Dm) {
-                    Dm[(size_t)gi * n + gj] = dv;
-                    if (!dg) Dm[(size_t)gj * n + gi] = dv;
-                }
-                if (dg) {
-                    tr += dv;
-                    sq += dv * dv;
-                } else {
-                    sq += 2.0 * dv * dv;
-                }
-            }
-        }
-    }
-}
 
 }  // namespace ffg

@@ -179,8 +179,6 @@ struct Workspace {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // tensor-map cache over the operand arrays hi0 lo0 hi1 lo1: [0..3] 64x128 operand boxes
     // (SW128), [4..7] 32x32 epilogue pieces (SW64)
-    int tm_B = -1, tm_np = -1;
-    CUtensorMap tm[8];
     // pair kernel (k2_pair.cuh): panel counters, pair table, per-layer coefficients, maps
     uint32_t* counters = nullptr;
     size_t cap_cnt = 0;
@@ -286,7 +284,6 @@ int ensure(Workspace& w, int B, int64_t np, int64_t T, bool operands) {
         for (auto& p : w.op)
             if ((rc = grow(&p, dummy, elems))) return rc;
         w.cap_elems = elems;
-        w.tm_B = -1;
     }
     if (B > w.cap_B) {
         int rc;
@@ -459,13 +456,13 @@ int normal_kstep() {
 
 // Paired A updates (every other layer reduces d_l X_l + d_{l+1} X_{l+1} into A): only the streaming
 // epilogues that reduce A at L2 (epi_sub_mid_red) read the input-X term, so the resident variant
-// (FFG_RESIDENT) and the two-group workers keep one update per layer.
+// (FFG_RESIDENT) keeps one update per layer.
 bool a_pairing() {
     static bool v = [] {
         const char* e = getenv("FFG_A_PAIR");
         const char* r = getenv("FFG_RESIDENT");
         const bool on = e ? atoi(e) != 0 : true;
-        return on && FFG_A_RED && !FFG_TWO_GROUPS && !(r && atoi(r) != 0);
+        return on && !(r && atoi(r) != 0);
     }();
     return v;
 }
@@ -506,20 +503,6 @@ int num_sms() {
     return v;
 }
 
-template <int MODE>
-int launch_layer(const LayerMaps& maps, const LayerParams& p, int tiles, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        CK(cudaFuncSetAttribute(mlsp2_layer_persistent<MODE>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, kPersistSmem));
-        configured = true;
-    }
-    const int grid = std::min(tiles, num_sms());
-    mlsp2_layer_persistent<MODE><<<grid, kPersistThreads, kPersistSmem, st>>>(maps, p);
-    CK(cudaGetLastError());
-    return FFG_OK;
-}
-
 // Optional CUDA-event timing of every K2 launch, for the roofline figure.
 struct LayerProfile {
     bool on = false;
@@ -548,16 +531,6 @@ int prof_begin(cudaStream_t st, cudaEvent_t* stop, double flops) {
 
 unsigned long long* g_prof_buf = nullptr;  // FFG_DEBUG_K2 & 8: per-CTA role wait cycles
 
-// K2 implementation: 1 = per-layer single-CTA persistent kernel (kernels.cuh, kept for A/B
-// measurement), default = CTA-pair multi-layer kernel (k2_pair.cuh).
-int k2_impl() {
-    static int v = [] {
-        const char* e = getenv("FFG_K2");
-        // the per-layer kernel has no lo*lo product, which the fixed-point split needs
-        return (e && !FFG_FIXED_SPLIT) ? atoi(e) : 2;
-    }();
-    return v;
-}
 
 // Matrices per L2-resident group of the pair kernel.  Enough pair items per layer
 // (G * PT >= 2 * resident pairs) that a layer's first items find their panels complete while
@@ -586,11 +559,11 @@ int pair_capacity(int* out) {
     static int max_pairs = -1;
     if (max_pairs < 0) {
         CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                PairCfg<MODE, (V != 0)>::kSmem));
+                                PairCfg<MODE>::kSmem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * (num_sms() / 2));
         cfg.blockDim = dim3(kPairThreads);
-        cfg.dynamicSmemBytes = PairCfg<MODE, (V != 0)>::kSmem;
+        cfg.dynamicSmemBytes = PairCfg<MODE>::kSmem;
         int nc = 0;
         CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_pair_kernel<MODE, V>, &cfg));
         if (nc < 1) return set_err(FFG_ERR_CUDA, "pair kernel: no co-resident CTA pair fits");
@@ -610,7 +583,7 @@ int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaS
     // pair item of a layer (each keeps its block for all layers), `items` = pairs per layer
     if (RES && items > cap) return set_err(FFG_ERR_CUDA, "resident K2: %lld pairs > %d resident", (long long)items, cap);
     const int pairs = (int)std::min<int64_t>(cap, items);
-    mlsp2_pair_kernel<MODE, V><<<2 * pairs, kPairThreads, PairCfg<MODE, (V != 0)>::kSmem, st>>>(maps, pp);
+    mlsp2_pair_kernel<MODE, V><<<2 * pairs, kPairThreads, PairCfg<MODE>::kSmem, st>>>(maps, pp);
     CK(cudaGetLastError());
     return FFG_OK;
 }
@@ -732,7 +705,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     const int nb = (int)(np / kBM);
     const int64_t T = (int64_t)nb * (nb + 1) / 2;
     const ffg_model& md = *j.model;
-    const bool pair = k2_impl() != 1;
+    constexpr bool pair = true;  // the pair kernel (k2_pair.cuh) is the only K2
     int rc;
     if ((rc = ensure(w, B, np, pair ? 0 : T, true))) return rc;
     if (pair && (rc = ensure_pair(w, B, np, nb, md.n_layers))) return rc;
@@ -741,16 +714,6 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         size_t dummy = 0;
         if ((rc = grow(&w.partials, dummy, (size_t)B * Tpart))) return rc;
         w.cap_T = (size_t)B * Tpart;
-    }
-    if (!pair && (w.tm_B != B || w.tm_np != (int)np)) {
-        for (int k = 0; k < 4; ++k) {
-            if ((rc = make_map(&w.tm[k], w.op[k], (int64_t)B * np, np, 2, 64, 128))) return rc;
-            if ((rc = make_map(&w.tm[4 + k], w.op[k], (int64_t)B * np, np, 2, 32, 32,
-                               CU_TENSOR_MAP_SWIZZLE_64B)))
-                return rc;
-        }
-        w.tm_B = B;
-        w.tm_np = (int)np;
     }
     // per-matrix parameters
     std::vector<double> ph((size_t)4 * B);
@@ -808,7 +771,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     rp.mode = j.mode;
     rp.write_operands = 1;
     rp.fixed = (pair && FFG_FIXED_SPLIT && j.mode == kModeF32E && exact_drain_layers() > 0) ? 1 : 0;
-    rp.xa_used = pair ? w.xa_used : nullptr;   // the per-layer kernel reads every upper block
+    rp.xa_used = w.xa_used;   // X/A stores only for the blocks K2 reads
     rescale_tiles_kernel<<<dim3((unsigned)(np / kK1Rows), (unsigned)B), 256, 0, st>>>(rp);
     CK(cudaGetLastError());
 
@@ -876,47 +839,6 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
                 return rc;
         }
         if (stop) CK(cudaEventRecord(stop, st));
-    } else {
-        for (int l = 0; l < md.n_layers; ++l) {
-            const int par = l & 1;
-            LayerParams lp{};
-            lp.X = w.X;
-            lp.A = w.A;
-            lp.hi_dst = w.op[2 * (par ^ 1) + 0];
-            lp.lo_dst = w.op[2 * (par ^ 1) + 1];
-            lp.D = j.D_dev;
-            lp.partials = w.partials;
-            lp.flags = w.flags;
-            lp.a = md.abcd[4 * l + 0];
-            lp.b = md.abcd[4 * l + 1];
-            lp.c = md.abcd[4 * l + 2];
-            lp.last = (l == md.n_layers - 1);
-            lp.d_next = lp.last ? 0.0 : md.abcd[4 * (l + 1) + 3];
-            lp.n = (int)n;
-            lp.np = (int)np;
-            lp.nb = nb;
-            lp.T = (int)T;
-            lp.layer = l;
-            lp.n_layers = md.n_layers;
-            lp.exact_layers = exact_drain_layers();
-            lp.B = B;
-            lp.dbg = debug_flags();
-            LayerMaps maps;
-            maps.hi = w.tm[2 * par + 0];
-            maps.lo = w.tm[2 * par + 1];
-            maps.hip = w.tm[4 + 2 * (par ^ 1) + 0];
-            maps.lop = w.tm[4 + 2 * (par ^ 1) + 1];
-            const int tiles = (int)(B * T);
-            cudaEvent_t stop;
-            if ((rc = prof_begin(st, &stop, layer_flops))) return rc;
-            switch (j.mode) {
-                case kModeF32E: rc = launch_layer<kModeF32E>(maps, lp, tiles, st); break;
-                case kModeF16: rc = launch_layer<kModeF16>(maps, lp, tiles, st); break;
-                default: rc = launch_layer<kModeBF16>(maps, lp, tiles, st); break;
-            }
-            if (rc) return rc;
-            if (stop) CK(cudaEventRecord(stop, st));
-        }
     }
     FinalizeParams fp{};
     fp.partials = w.partials;
@@ -1596,7 +1518,7 @@ int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, in
     (void)n;
     (void)mode;
     if (!model) return 0;
-    if (k2_impl() != 1) return 4;            // reset + K1 + K2 (all layers) + K3
+    return 4;                                // reset + K1 + K2 (all layers) + K3
     return 3 + (int64_t)model->n_layers;    // reset + K1 + L x K2 + K3
 }
 

@@ -48,70 +48,39 @@ constexpr int kPRegsCtl = 48, kPRegsDrain = 104, kPRegsEpi = 112;
 constexpr int kPRegsCtl = 48, kPRegsDrain = 96, kPRegsEpi = 120;
 #endif
 static_assert(128 * kPRegsCtl + 256 * kPRegsDrain + 256 * kPRegsEpi <= 640 * 96, "setmaxnreg budget");
-#ifndef FFG_STREAM16
-#define FFG_STREAM16 0  // 16 worker warps: each drains and runs the epilogue of one 32-column piece
-#endif
-#ifndef FFG_TWO_GROUPS
-#define FFG_TWO_GROUPS 0  // streaming workers as two drain+epilogue groups on alternate items
-#endif
-#ifndef FFG_G_CTL
-#define FFG_G_CTL 32
-#define FFG_G_WORK 112
-#endif
-constexpr int kGRegsCtl = FFG_G_CTL, kGRegsWork = FFG_G_WORK;
-static_assert(128 * kGRegsCtl + 512 * kGRegsWork <= 640 * 96, "setmaxnreg budget (two groups)");
-// resident variant: 16 worker warps (drain + epilogue) own 32 columns each of the CTA's block
+// resident and 16-worker variants: 16 worker warps (drain + epilogue) own 32 columns each of the CTA's block
 constexpr int kResWorkers = 16;
 constexpr int kRRegsCtl = 40, kRRegsWork = 104;
 static_assert(128 * kRRegsCtl + 512 * kRRegsWork <= 640 * 96, "setmaxnreg budget (resident)");
 constexpr int kPairHalf = kBN / 2;                  // B rows supplied by each CTA
 constexpr int kPairOpA = kBM * kBK * 2;             // 16 KB
 constexpr int kPairOpB = kPairHalf * kBK * 2;       // 8 KB
-#ifndef FFG_STAGING_INPLACE
-#define FFG_STAGING_INPLACE 0  // epilogue staging: direct pieces only, mirrors transposed in place
-#endif
-constexpr int kStgPieces = FFG_STAGING_INPLACE ? 2 : 4;  // 2 KB pieces per epilogue warp
-constexpr int kPairStagingBytes = kEpiWarps2 * kStgPieces * kPieceBytes;  // 32 or 64 KB
+// epilogue staging: 64 KB = 8 epilogue warps x four 2 KB pieces (direct + mirrored hi/lo), or
+// 16 worker warps x two pieces (mirrors transposed in place)
+constexpr int kPairStagingBytes = kEpiWarps2 * 4 * kPieceBytes;
 
-// staging: 64 KB for the resident / two-group workers (16 warps x 4 KB) and the 4-piece
-// epilogue; 32 KB with in-place mirrors, which buys an extra operand stage (two for BF16)
-template <int MODE, bool WIDE = false>
+template <int MODE>
 struct PairCfg {
-    static constexpr bool kWide = WIDE || FFG_TWO_GROUPS || FFG_STREAM16 || !FFG_STAGING_INPLACE;
-    static constexpr int kStagingBytes = kWide ? kEpiWarps2 * 4 * kPieceBytes : kPairStagingBytes;
+    static constexpr int kStagingBytes = kPairStagingBytes;
     static constexpr int kStageBytes = ModeTraits<MODE>::kHasLo ? 2 * (kPairOpA + kPairOpB)
                                                                 : (kPairOpA + kPairOpB);
-    static constexpr int kStages = (ModeTraits<MODE>::kHasLo ? 3 : 6) + (kWide ? 0 : (ModeTraits<MODE>::kHasLo ? 1 : 2));
+    static constexpr int kStages = ModeTraits<MODE>::kHasLo ? 3 : 6;
     static constexpr int kStagingOff = kStages * kStageBytes;
     static constexpr int kBarOff = kStagingOff + kStagingBytes;
     static constexpr int kSmem = kBarOff + 1024 + 1024;  // barriers/scratch + alignment slack
 };
 static_assert(PairCfg<kModeF32E>::kSmem <= 227 * 1024, "pair kernel smem");
-static_assert(PairCfg<kModeF32E, true>::kSmem <= 227 * 1024, "pair kernel smem");
-static_assert(PairCfg<kModeBF16, true>::kSmem <= 227 * 1024, "pair kernel smem");
 static_assert(PairCfg<kModeBF16>::kSmem <= 227 * 1024, "pair kernel smem");
 static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue warps alike");
 
-// TMEM: 4 slots x 128 columns.  A CHUNK is accumulated into the next slot of the ring:
-// FP32-emulated: one K16 step (exact-drain layers) or one K-block, issued cross terms first
-// (hi*lo with accumulate=0, lo*hi) and hi*hi last, so hi*hi sees exactly one truncating
-// accumulate per K16 step into a chunk-sized partial (accumulation precision);
-// single-product modes: the whole K extent.  The drain warps sum chunks in registers with
-// round-to-nearest adds and write Y into the item's LAST slot, which the epilogue frees.
-#ifndef FFG_X_HILO
-#define FFG_X_HILO 0  // FP32E epilogue: X rebuilt from the hi/lo operands, no fp32 X traffic in K2
-#endif
+// TMEM: 4 slots x 128 columns.  A CHUNK is accumulated into the next slot of the ring.
+// FP32-emulated: in the exact layers two whole-K chunks (hi*hi on the fixed-point split, exact;
+// the cross terms), afterwards one chunk per two K-blocks with the cross terms issued first (hi*lo
+// with accumulate=0, lo*hi) and hi*hi last (accumulation precision); single-product
+// modes: the whole K extent.  The drain warps sum chunks in registers with round-to-nearest adds
+// and write Y into the item's LAST slot, which the epilogue frees.
 #ifndef FFG_BLOCK_DEPS
 #define FFG_BLOCK_DEPS 1  // producer waits per 128-column block when a panel is incomplete (runtime: p.blockdeps)
-#endif
-#ifndef FFG_WARP_PUBLISH
-#define FFG_WARP_PUBLISH 0  // every epilogue warp publishes its part of a block (no block barrier)
-#endif
-#ifndef FFG_A_RED
-#define FFG_A_RED 1  // epilogue: A += d'X' by L2 vector reduction; X prefetched one sub-block ahead
-#endif
-#ifndef FFG_EPI_PREFETCH
-#define FFG_EPI_PREFETCH 0  // epilogue loads sub-block 1's X/A before computing sub-block 0
 #endif
 #ifndef FFG_EPI_SPIN
 #define FFG_EPI_SPIN 0  // epilogue warps spin on y_full instead of sleeping
@@ -459,188 +428,7 @@ __device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t t
     }
 }
 
-// Two-group streaming workers (FFG_TWO_GROUPS): warps 4-19 form two groups of 8 that take
-// alternate items of this CTA pair.  A group drains the item's chunks into REGISTER sums (each
-// TMEM slot is released as soon as it is read, so all four slots keep rotating) and then runs
-// the epilogue straight from those registers, while the other group drains the next item: two
-// epilogues are in flight per CTA.  Warp w of a group: TMEM lane quarter q = w & 3 (rows
-// 32q..32q+31), column half h (columns 64h..64h+63, quarters 2h and 2h + 1); thread = one row.
-template <int MODE>
-__device__ __forceinline__ void two_group_workers(const PairMaps& tm, const PairParams& p, uint32_t tmem,
-                                                  int warp, int lane, uint32_t rank, int pair_id,
-                                                  int n_pairs, int total, int nk, uint64_t* slot_full,
-                                                  uint64_t* slot_empty, uint64_t* hand, uint8_t* staging,
-                                                  double* red) {
-    using Tr = ModeTraits<MODE>;
-    const int wk = warp - 4, grp = wk >> 3, wq = wk & 7;
-    const int q = warp & 3, h = wq >> 2;
-    const int r = q * 32 + lane;
-    const int nb = p.nb, n = p.n, np = p.np;
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + 64 * h;  // + slot * 128
-    const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
-    const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
-    uint8_t* stg = staging + wk * 2 * kPieceBytes;  // direct hi piece, lo piece (mirrors in place)
-    const uint32_t stg_a = smem_u32(stg);
-    double* gred = red + 16 * grp;
-    int g = 0, u = 0;
-    for (int item = pair_id; item < total; item += n_pairs, ++u) {
-        int m, l, pi;
-        pair_decode(p, item, m, l, pi);
-        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
-        if ((u & 1) != grp) {
-            g += chunks;
-            continue;
-        }
-        // the other group has seen every chunk of the previous item: slot_full phases are then
-        // at most one ahead of this group's waits (no parity aliasing)
-        if (u > 0) mbar_wait(&hand[grp ^ 1], ((u - 1) >> 1) & 1);
-        float yacc[64];
-#pragma unroll
-        for (int e = 0; e < 64; ++e) yacc[e] = 0.0f;
-#pragma unroll 1
-        for (int f = 0; f < chunks; ++f, ++g) {
-            const int sl = g & 3;
-            mbar_wait(&slot_full[sl], (g >> 2) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int ch = 0; ch < 4; ch += 2) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x16(tl + sl * 128 + ch * 16, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
-                tmem_ld_32x32b_x16(tl + sl * 128 + ch * 16 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
-                tmem_ld_wait();
-                if (ch == 2) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
-                }
-#pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    const float2 acc = add_f32x2(make_float2(yacc[16 * ch + e], yacc[16 * ch + e + 1]),
-                                                 make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
-                    yacc[16 * ch + e] = acc.x;
-                    yacc[16 * ch + e + 1] = acc.y;
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&hand[grp]);
-        // ------------------------------------------------------------- epilogue of the item
-        const uint32_t pr = __ldg(p.pairs + pi);
-        const int R = rank ? (pr >> 10) & 1023 : pr & 1023;
-        const int C = (pr >> 20) & 1023;
-        const bool dummy = rank && ((pr >> 30) & 1);
-        const bool last = (l == p.n_layers - 1);
-        const bool diag = R == C;
-        const int gi = R * kBM + r;
-        const bool c_on = gi < n;
-        EpiCoef k = load_coef(p.coef, l, last);
-        k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
-        const int nxt = (l + 1) & 1;
-        float* Xt = p.X + xa_tile_base(m, R, C, nb);
-        float* At = p.A + xa_tile_base(m, R, C, nb);
-        double* Dm = (last && p.D) ? p.D + (size_t)m * n * n : nullptr;
-        EpiHealth hl;
-        double tr = 0.0, sq = 0.0;
-#pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-            const int qc = 2 * h + qi;  // column quarter (32 columns)
-            if (dummy || (p.dbg & 1) || (diag && qc < q)) continue;
-            const bool dblk = diag && qc == q;
-            if (!last) {
-                if (lane == 0) tma_store_wait_read();  // the staging pieces are free again
-                __syncwarp();
-            }
-#pragma unroll
-            for (int rd = 0; rd < 4; ++rd) {
-                const int c0 = 32 * qc + 8 * rd;
-                float y[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) y[e] = yacc[32 * qi + 8 * rd + e] * inv_s2;
-                if (!last) {
-                    if (diag)
-                        epi_oct_mid_y<MODE, true>(y, Xt, At, r, c0, lane, c_on, k, stg_a, dblk, hl);
-                    else
-                        epi_oct_mid_y<MODE, false>(y, Xt, At, r, c0, lane, c_on, k, stg_a, false, hl);
-                } else {
-                    if (diag)
-                        epi_oct_last_y<true>(y, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
-                    else
-                        epi_oct_last_y<false>(y, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
-                }
-            }
-            if (!last && !(p.dbg & 32)) {
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    const int prow = m * np + R * kBM + 32 * q;  // direct piece origin
-                    const int pcol = C * kBN + 32 * qc;
-                    tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
-                    if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
-                    tma_store_commit();
-                }
-                if (!dblk) {  // mirrored pieces: transpose the direct pieces in place once read
-                    if (lane == 0) tma_store_wait_read();
-                    __syncwarp();
-                    transpose_piece_inplace(stg_a, lane);
-                    if (Tr::kHasLo) transpose_piece_inplace(stg_a + kPieceBytes, lane);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        const int mrow = m * np + C * kBN + 32 * qc;
-                        const int mcol = R * kBM + 32 * q;
-                        tma_store_2d(&tm.p_hi[nxt], stg, mcol, mrow);
-                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, mcol, mrow);
-                        tma_store_commit();
-                    }
-                }
-            }
-        }
-        if (!dummy) {
-            const bool any_nf = __any_sync(0xffffffffu, hl.nonfinite());
-            const bool any_hr = !last && __any_sync(0xffffffffu, hl.template half_range<MODE>());
-            if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], l + 1);
-            if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], l + 1);
-        }
-        if (last) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                tr += __shfl_xor_sync(0xffffffffu, tr, o);
-                sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            }
-            named_bar_sync(3 + grp, 8 * 32);  // the group's previous partial consumed
-            if (lane == 0) {
-                gred[2 * wq + 0] = tr;
-                gred[2 * wq + 1] = sq;
-            }
-            named_bar_sync(3 + grp, 8 * 32);
-            if (wq == 0 && lane == 0) {
-                double T0 = 0.0, T1 = 0.0;
-                for (int w = 0; w < 8; ++w) {  // fixed order
-                    T0 += gred[2 * w + 0];
-                    T1 += gred[2 * w + 1];
-                }
-                p.partials[(size_t)m * 2 * p.PT + 2 * pi + rank] = make_double2(T0, T1);
-            }
-        } else if (!dummy && l + 1 < p.l1) {
-            // publish the block: hi/lo stores landed, X/A stores visible -> panel counters
-            if (lane == 0) {
-                tma_store_wait_all();
-                fence_proxy_async_global();
-            }
-            __syncwarp();
-            named_bar_sync(5 + grp, 8 * 32);
-            if (wq == 0 && lane == 0) {
-                __threadfence();
-                uint32_t* cm = p.counters + (size_t)m * nb;
-                red_release_gpu_add(cm + R, 1u);
-                if (C != R) red_release_gpu_add(cm + C, 1u);
-            }
-        }
-    }
-    if (lane == 0) tma_store_wait_all();
-}
-
-// Streaming 16-worker epilogue (FFG_STREAM16): warps 4-19 all work on every item.  Warp w:
+// Streaming 16-worker epilogue (kernel variant V = 2): warps 4-19 all work on every item.  Warp w:
 // TMEM lane quarter q = w & 3 (rows 32q..32q+31), column quarter c = (w - 4) >> 2 (32 columns).
 // The warp drains its 32 columns of every chunk into register sums and releases each TMEM slot
 // as soon as it is read (Y never holds a slot, so the MMA always has the four-slot ring), then
@@ -847,15 +635,12 @@ template <int MODE, int V = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     mlsp2_pair_kernel(const __grid_constant__ PairMaps tm, const __grid_constant__ PairParams p) {
     constexpr bool RES = V == 1;
-    constexpr bool S16 = V == 2 || (V == 0 && FFG_STREAM16);
+    constexpr bool S16 = V == 2;
     constexpr int kSlots = RES ? 3 : 4;  // TMEM chunk ring (resident: slot 3 holds the X block)
-    // panel-counter increments per published block (per-warp publication: one per epilogue warp)
-    constexpr uint32_t kPub = (!RES && !FFG_TWO_GROUPS && FFG_WARP_PUBLISH) ? kEpiWarps2 : 1;
     using Tr = ModeTraits<MODE>;
-    using Cfg = PairCfg<MODE, (V != 0)>;
+    using Cfg = PairCfg<MODE>;
     // (FP32-emulated only: a K-block pair there is 1.5K MMA cycles, enough to hide the polls)
-    constexpr bool kXHilo = FFG_X_HILO && MODE == kModeF32E;
-    constexpr bool kBlockDeps = FFG_BLOCK_DEPS && !RES && !FFG_TWO_GROUPS && !FFG_WARP_PUBLISH && Tr::kHasLo;
+    constexpr bool kBlockDeps = FFG_BLOCK_DEPS && !RES && Tr::kHasLo;
     constexpr bool kDrain = Tr::kProducts == 3;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -899,7 +684,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"((RES || S16) ? kRRegsCtl : (FFG_TWO_GROUPS ? kGRegsCtl : kPRegsCtl)) : "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"((RES || S16) ? kRRegsCtl : kPRegsCtl) : "memory");
         if (warp == 0 && lane == 0) {
             // ================================================= TMA producer (both CTAs)
             for (int i = 0; i < 2; ++i) {
@@ -926,12 +711,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 // loaded, so the item's first K-blocks overlap the previous layer's tail
                 bool blockwise = false;
                 if (kBlockDeps && p.blockdeps && l > p.l0 && !(p.dbg & 4)) {
-                    const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
+                    const uint32_t need = (uint32_t)(nb * (l - p.l0));
                     const uint32_t* cm = p.counters + (size_t)m * nb;
                     blockwise = ld_acquire_gpu(cm + ap) < need || ld_acquire_gpu(cm + sp) < need;
                     if (!blockwise) fence_proxy_async_global();
                 } else if (l > p.l0 && !(p.dbg & 4)) {
-                    const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
+                    const uint32_t need = (uint32_t)(nb * (l - p.l0));
                     const uint32_t* cm = p.counters + (size_t)m * nb;
                     const long long t0 = clock64();
                     while (ld_acquire_gpu(cm + ap) < need && (FFG_DEP_BACKOFF ? (__nanosleep(FFG_DEP_BACKOFF), 1) : 1))
@@ -972,7 +757,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         const uint32_t* fa = bf + (ap < blk ? ap * nb + blk : blk * nb + ap);
                         const uint32_t* fs = bf + (sp < blk ? sp * nb + blk : blk * nb + sp);
                         const uint32_t* cm = p.counters + (size_t)m * nb;
-                        const uint32_t needp = (uint32_t)(kPub * nb * (l - p.l0));
+                        const uint32_t needp = (uint32_t)(nb * (l - p.l0));
                         const long long t0 = clock64();
                         // the four polls in flight together; complete panels end the blockwise mode
                         uint32_t va = ld_acquire_gpu(fa), vs = ld_acquire_gpu(fs);
@@ -1160,10 +945,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRRegsWork) : "memory");
         stream16_workers<MODE>(tm, p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk, slot_full,
                                slot_empty, smem + Cfg::kStagingOff, red);
-    } else if (FFG_TWO_GROUPS) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kGRegsWork) : "memory");
-        two_group_workers<MODE>(tm, p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk, slot_full,
-                                slot_empty, y_full, smem + Cfg::kStagingOff, red);
     } else if (warp < 4 + kEpiWarps) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsDrain) : "memory");
         // ===================================================== chunk drain -> Y (both CTAs)
@@ -1251,7 +1032,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int r = q * 32 + lane;       // block row of this thread
         const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
         const int np = p.np, n = p.n;
-        uint8_t* stg = smem + Cfg::kStagingOff + ew * kStgPieces * kPieceBytes;
+        uint8_t* stg = smem + Cfg::kStagingOff + ew * 4 * kPieceBytes;
         const uint32_t stg_a = smem_u32(stg);
         const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
         int g = 0;
@@ -1277,19 +1058,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const uint32_t tacc = tlane + ysl * 128;
             float* Xt = p.X + xa_tile_base(m, R, C, nb);
             float* At = p.A + xa_tile_base(m, R, C, nb);
-            // X of layer l: fp32 block, or (FFG_X_HILO, FP32E) rebuilt from the hi/lo operand row
-            const size_t xrow = ((size_t)m * np + R * kBM + r) * np + C * kBN;
-            const uint16_t* hrow = p.hi[l & 1] + xrow;
-            const uint16_t* lrow = p.lo[l & 1] + xrow;
-            auto loadx = [&](int c0, float4(&x)[4]) {
-                if constexpr (kXHilo)
-                    epi_loadx16_hilo(hrow + c0, lrow + c0, x);
-                else
-                    epi_loadx16(Xt, r, c0, x);
-            };
             EpiHealth hl;
             double tr = 0.0, sq = 0.0;
-#if FFG_A_RED
             // X of this warp's first sub-block is requested before the wait for Y; every
             // sub-block then requests the next one's X before computing (software pipeline)
             const bool ok0 = !(dummy || (p.dbg & 1) || (diag && s < q));
@@ -1305,16 +1075,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                             while (ld_acquire_gpu(f) < (uint32_t)(l - p.l0)) {
                             }
                         } else {
-                            const uint32_t need = (uint32_t)(kPub * nb * (l - p.l0));
+                            const uint32_t need = (uint32_t)(nb * (l - p.l0));
                             while (ld_acquire_gpu(p.counters + (size_t)m * nb + R) < need) {
                             }
                         }
                     }
                     __syncwarp();
                 }
-                if (!(p.dbg & 128)) loadx(32 * (ok0 ? s : s + 2), xq);
+                if (!(p.dbg & 128)) epi_loadx16(Xt, r, 32 * (ok0 ? s : s + 2), xq);
             }
-#endif
             if constexpr (!kDrain) {
                 // single-product modes: the slot holds the whole-K accumulator, read directly
                 // (no drain pass); the 1/scale^2 is applied as it is loaded
@@ -1342,10 +1111,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 }
                 const bool dblk = diag && qc == q;  // 32x32 piece on the matrix diagonal
                 const long long t_c0 = (p.dbg & 8) ? clock64() : 0;
-#if FFG_EPI_PREFETCH
-                float4 xq[4], aq[4];
-                if (!last) epi_load16(Xt, At, r, 32 * qc, xq, aq);
-#endif
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     const int c0 = 32 * qc + 16 * sub;
@@ -1358,92 +1123,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                             v[e] = __float_as_uint(__uint_as_float(v[e]) * (1.0f / (Tr::kScale * Tr::kScale)));
                     }
                     if (!last) {
-#if FFG_A_RED
                         float4 xn[4];
                         const bool more = sub == 0 || (qi == 0 && ok1);
-                        if (more && !(p.dbg & 128)) loadx(sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
+                        if (more && !(p.dbg & 128)) epi_loadx16(Xt, r, sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
                         if (diag)
                             epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
-                                                        p.dbg & 64, !kXHilo);
+                                                        p.dbg & 64);
                         else
                             epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
-                                                         p.dbg & 64, !kXHilo);
+                                                         p.dbg & 64);
                         if (more) {
 #pragma unroll
                             for (int j = 0; j < 4; ++j) xq[j] = xn[j];
                         }
-#elif FFG_EPI_PREFETCH
-                        // software pipeline: the next sub-block's X/A are in flight during this one
-                        float4 xn[4], an[4];
-                        if (sub == 0) epi_load16(Xt, At, r, c0 + 16, xn, an);
-                        if (diag)
-                            epi_sub_mid_pre<MODE, true>(v, xq, aq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl);
-                        else
-                            epi_sub_mid_pre<MODE, false>(v, xq, aq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl);
-                        if (sub == 0) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                xq[j] = xn[j];
-                                aq[j] = an[j];
-                            }
-                        }
-#else
-                        const bool nomem = p.dbg & 64;
-                        if (diag)
-                            epi_sub_mid<MODE, true>(v, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl, nomem);
-                        else
-                            epi_sub_mid<MODE, false>(v, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl, nomem);
-#endif
                     } else {
                         double* Dm = p.D ? p.D + (size_t)m * n * n : nullptr;
-                        if constexpr (kXHilo) {
-                            float4 xl[4];
-                            loadx(c0, xl);
-                            if (diag)
-                                epi_sub_last_x<true>(v, xl, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
-                            else
-                                epi_sub_last_x<false>(v, xl, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
-                        } else if (diag) {
+                        if (diag)
                             epi_sub_last<true>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
-                        } else {
+                        else
                             epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
-                        }
                     }
                 }
                 const long long t_c1 = (p.dbg & 8) ? clock64() : 0;
                 if (p.dbg & 8) w_cmp += (unsigned long long)(t_c1 - t_c0);
-#if FFG_STAGING_INPLACE
-                if (!last && !(p.dbg & 32)) {
-                    // direct pieces out, then the mirrored pieces transposed in place once the
-                    // direct stores have read the staging
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        const int prow = m * np + R * kBM + 32 * q;
-                        const int pcol = C * kBN + 32 * qc;
-                        tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
-                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
-                        tma_store_commit();
-                    }
-                    if (!dblk) {
-                        if (lane == 0) tma_store_wait_read();
-                        __syncwarp();
-                        transpose_piece_inplace(stg_a, lane);
-                        if (Tr::kHasLo) transpose_piece_inplace(stg_a + kPieceBytes, lane);
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            const int mrow = m * np + C * kBN + 32 * qc;
-                            const int mcol = R * kBM + 32 * q;
-                            tma_store_2d(&tm.p_hi[nxt], stg, mcol, mrow);
-                            if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, mcol, mrow);
-                        }
-                    }
-                }
-                if (false) {
-#else
                 if (!last) {
-#endif
                     if (!dblk) {  // mirrored pieces: warp transpose of the direct pieces
                         __syncwarp();
                         transpose_piece(stg_a, stg_a + 2 * kPieceBytes, lane);
@@ -1513,13 +1216,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         if (C != R) red_relaxed_gpu_add(cm + C, 1u);
                     }
                 } else {
-#if FFG_WARP_PUBLISH
-                    // per warp: no wait for the block's slowest warp (consumers count 8 per block)
-                    if (lane == 0) {
-#else
                     named_bar_sync(4, kEpiWarps2 * 32);
                     if (ew == 0 && lane == 0) {
-#endif
                         __threadfence();
                         uint32_t* cm = p.counters + (size_t)m * nb;
                         // the fence above orders this block's writes before all three increments

@@ -5,7 +5,7 @@ import numpy as np
 from paper_2605_08523_b200 import engine as E
 from paper_2605_08523_b200.hamiltonians import tight_binding, batch_params
 from oracle import oracle as O
-print("dev", E.device_available(), "K2", os.environ.get("FFG_K2", "2"), flush=True)
+print("dev", E.device_available(), flush=True)
 Y = E.mixed_square(np.eye(256, dtype=np.float32)); print("I ok", np.array_equal(Y, np.eye(256)), flush=True)
 m = E.load_model("M1500")
 for n in (100, 128, 256, 384, 512, 1024):
