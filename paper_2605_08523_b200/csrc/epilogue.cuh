@@ -21,12 +21,25 @@ struct EpiCoef {
 };
 
 // Layer l's coefficients as hi/lo fp32 pairs, split on the host from the fp64 model (hi = rn_f32(v),
-// lo = rn_f32(v - hi)): {a, b}, {c, d'}, {dc, red}.  d' multiplies the layer's output X', dc its input
-// X; with paired A updates (host: FFG_A_PAIR) only every other layer reduces into A, adding
-// d_l X_l + d_{l+1} X_{l+1} at once (dc = d' = 0 and red = 0 in the others).
-__device__ __forceinline__ EpiCoef load_coef(const float4* coef, int l, bool /*last*/) {
-    const float4 u = __ldg(coef + 3 * l), w = __ldg(coef + 3 * l + 1), z = __ldg(coef + 3 * l + 2);
-    return EpiCoef{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w, z.x, z.y, z.z != 0.0f, false};
+// lo = rn_f32(v - hi)): table row l = {a, b}, {c, d_{l+1}} (d_L = 0).  d' multiplies the layer's output
+// X', dc its input X.  With paired A updates only the odd layers reduce into A, adding d_l X_l +
+// d_{l+1} X_{l+1} at once (d_l is row l-1's d'); K1 wrote A = d_0 X_0.  The table stays at 8 floats
+// per layer (under 1 KB for 30 layers) so its per-call upload travels inline with the launch stream
+// instead of queueing on a copy engine behind the host path's matrix transfers.
+__device__ __forceinline__ EpiCoef load_coef(const float4* coef, int l, int n_layers, bool paired) {
+    const float4 u = __ldg(coef + 2 * l), w = __ldg(coef + 2 * l + 1);
+    EpiCoef k{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w, 0.0f, 0.0f, l + 1 < n_layers, false};
+    if (paired) {
+        if (l & 1) {
+            const float4 wp = __ldg(coef + 2 * (l - 1) + 1);
+            k.dc_hi = wp.z;
+            k.dc_lo = wp.w;
+        } else {
+            k.d_hi = k.d_lo = 0.0f;
+            k.red = false;
+        }
+    }
+    return k;
 }
 
 #ifndef FFG_EPI_EFT

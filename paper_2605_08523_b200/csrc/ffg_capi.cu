@@ -187,7 +187,7 @@ struct Workspace {
     size_t cap_used = 0;
     int pairs_nb = -1, PT = 0;
     size_t cap_pairs = 0;
-    float* coef = nullptr;              // [L][12] hi/lo fp32 coefficients (load_coef)
+    float* coef = nullptr;              // [L][8] hi/lo fp32 coefficients (load_coef)
     size_t cap_coef = 0;
     int pm_B = -1, pm_np = -1;
     PairMaps pmaps;
@@ -672,9 +672,9 @@ int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L) {
         w.pairs_nb = nb;
         w.PT = (int)t.size();
     }
-    if ((size_t)12 * L > w.cap_coef) {
-        if ((rc = grow(&w.coef, dummy, (size_t)12 * L))) return rc;
-        w.cap_coef = (size_t)12 * L;
+    if ((size_t)8 * L > w.cap_coef) {
+        if ((rc = grow(&w.coef, dummy, (size_t)8 * L))) return rc;
+        w.cap_coef = (size_t)8 * L;
     }
     if (w.pm_B != B || w.pm_np != (int)np) {
         for (int par = 0; par < 2; ++par) {
@@ -725,29 +725,19 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     }
     if ((rc = upload_small(w, w.params, ph.data(), sizeof(double) * 4 * B, st))) return rc;
     if (pair) {
-        // hi/lo fp32 split of a, b, c, the d of the layer's output and (paired A updates) of its input,
-        // plus the reduce flag, per layer (epilogue.cuh load_coef)
-        const bool paired = a_pairing();
-        std::vector<float> cf((size_t)12 * md.n_layers, 0.0f);
+        // hi/lo fp32 split of a, b, c and the next layer's d per layer (epilogue.cuh load_coef; the
+        // paired A updates are derived in the kernel from the same 8-float rows)
+        std::vector<float> cf((size_t)8 * md.n_layers);
         auto split = [](double v, float* o) {
             o[0] = (float)v;
             o[1] = (float)(v - (double)o[0]);
         };
-        const int L = md.n_layers;
-        for (int l = 0; l < L; ++l) {
-            float* o = cf.data() + 12 * l;
+        for (int l = 0; l < md.n_layers; ++l) {
+            float* o = cf.data() + 8 * l;
             split(md.abcd[4 * l + 0], o + 0);
             split(md.abcd[4 * l + 1], o + 2);
             split(md.abcd[4 * l + 2], o + 4);
-            const double dnext = l + 1 < L ? md.abcd[4 * (l + 1) + 3] : 0.0;
-            if (!paired) {
-                split(dnext, o + 6);
-                o[10] = (l + 1 < L) ? 1.0f : 0.0f;
-            } else if (l & 1) {  // odd layers add d_l X_l + d_{l+1} X_{l+1}; K1 wrote A = d_0 X_0
-                split(dnext, o + 6);
-                split(md.abcd[4 * l + 3], o + 8);
-                o[10] = (l + 1 < L) ? 1.0f : 0.0f;  // the last layer adds d_l X_l into D directly
-            }
+            split(l + 1 < md.n_layers ? md.abcd[4 * (l + 1) + 3] : 0.0, o + 6);
         }
         if ((rc = upload_small(w, w.coef, cf.data(), sizeof(float) * cf.size(), st))) return rc;
     }
@@ -787,6 +777,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         pp.bflags = w.counters + (size_t)B * nb;
         pp.pairs = w.pairs;
         pp.coef = reinterpret_cast<const float4*>(w.coef);
+        pp.a_pair = a_pairing() ? 1 : 0;
         pp.n = (int)n;
         pp.np = (int)np;
         pp.nb = nb;

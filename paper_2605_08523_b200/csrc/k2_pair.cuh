@@ -140,7 +140,8 @@ struct PairParams {
     uint32_t* bflags;         // [B][nb][nb] block completion counts, index min*nb+max (FFG_BLOCK_DEPS)
     int blockdeps;            // 1: producer waits per block while a panel is incomplete (host: G == 1)
     const uint32_t* pairs;    // [PT]  A0 | A1 << 10 | S << 20 | dummy << 30
-    const float4* coef;       // [n_layers][3] hi/lo fp32 a, b, c, d_next, d_cur, red (epilogue.cuh)
+    const float4* coef;       // [n_layers][2] hi/lo fp32 a, b, c, d_next (epilogue.cuh load_coef)
+    int a_pair;               // paired A updates (odd layers reduce d_l X_l + d_{l+1} X_{l+1})
     int n, np, nb, PT;
     int B, G;                 // matrices, group size
     int l0, l1, n_layers;     // layers of this launch, model depth
@@ -277,7 +278,7 @@ __device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t t
             }
         }
         // ------------------------------------------------------------- epilogue of layer l
-        EpiCoef k = load_coef(p.coef, l, last);
+        EpiCoef k = load_coef(p.coef, l, p.n_layers, p.a_pair != 0);
         k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
         EpiHealth hl;
         double tr = 0.0, sq = 0.0;
@@ -487,7 +488,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
         const bool dblk = diag && c == q;
         const int gi = R * kBM + r;
         const bool c_on = gi < n;
-        EpiCoef k = load_coef(p.coef, l, last);
+        EpiCoef k = load_coef(p.coef, l, p.n_layers, p.a_pair != 0);
         k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
         const int nxt = (l + 1) & 1;
         float* Xt = p.X + xa_tile_base(m, R, C, nb);
@@ -1047,7 +1048,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const int C = (pr >> 20) & 1023;                     // block cols (B panel)
             const bool dummy = rank && ((pr >> 30) & 1);
             const bool last = (l == p.n_layers - 1);
-            EpiCoef k = load_coef(p.coef, l, last);
+            EpiCoef k = load_coef(p.coef, l, p.n_layers, p.a_pair != 0);
         k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
             const int nxt = (l + 1) & 1;   // hi/lo parity written by this layer
             g += (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
