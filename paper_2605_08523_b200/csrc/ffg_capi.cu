@@ -559,11 +559,11 @@ int pair_capacity(int* out) {
     static int max_pairs = -1;
     if (max_pairs < 0) {
         CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                PairCfg<MODE>::kSmem));
+                                PairCfg<MODE, pair_narrow<MODE, V>()>::kSmem));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * (num_sms() / 2));
         cfg.blockDim = dim3(kPairThreads);
-        cfg.dynamicSmemBytes = PairCfg<MODE>::kSmem;
+        cfg.dynamicSmemBytes = PairCfg<MODE, pair_narrow<MODE, V>()>::kSmem;
         int nc = 0;
         CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_pair_kernel<MODE, V>, &cfg));
         if (nc < 1) return set_err(FFG_ERR_CUDA, "pair kernel: no co-resident CTA pair fits");
@@ -583,7 +583,7 @@ int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaS
     // pair item of a layer (each keeps its block for all layers), `items` = pairs per layer
     if (RES && items > cap) return set_err(FFG_ERR_CUDA, "resident K2: %lld pairs > %d resident", (long long)items, cap);
     const int pairs = (int)std::min<int64_t>(cap, items);
-    mlsp2_pair_kernel<MODE, V><<<2 * pairs, kPairThreads, PairCfg<MODE>::kSmem, st>>>(maps, pp);
+    mlsp2_pair_kernel<MODE, V><<<2 * pairs, kPairThreads, PairCfg<MODE, pair_narrow<MODE, V>()>::kSmem, st>>>(maps, pp);
     CK(cudaGetLastError());
     return FFG_OK;
 }

@@ -59,18 +59,25 @@ constexpr int kPairOpB = kPairHalf * kBK * 2;       // 8 KB
 // 16 worker warps x two pieces (mirrors transposed in place)
 constexpr int kPairStagingBytes = kEpiWarps2 * 4 * kPieceBytes;
 
-template <int MODE>
+#ifndef FFG_NARROW_STAGING
+#define FFG_NARROW_STAGING 1  // streaming FP32E: two staging pieces per epilogue warp (mirrors in place), 4 stages
+#endif
+// NARROW (streaming kernel, FP32E, FFG_NARROW_STAGING): 32 KB of staging buys a fourth operand stage
+template <int MODE, bool NARROW = false>
 struct PairCfg {
-    static constexpr int kStagingBytes = kPairStagingBytes;
+    static constexpr int kStagingBytes = NARROW ? kPairStagingBytes / 2 : kPairStagingBytes;
     static constexpr int kStageBytes = ModeTraits<MODE>::kHasLo ? 2 * (kPairOpA + kPairOpB)
                                                                 : (kPairOpA + kPairOpB);
-    static constexpr int kStages = ModeTraits<MODE>::kHasLo ? 3 : 6;
+    static constexpr int kStages = (ModeTraits<MODE>::kHasLo ? 3 : 6) + (NARROW ? 1 : 0);
     static constexpr int kStagingOff = kStages * kStageBytes;
     static constexpr int kBarOff = kStagingOff + kStagingBytes;
     static constexpr int kSmem = kBarOff + 1024 + 1024;  // barriers/scratch + alignment slack
 };
 static_assert(PairCfg<kModeF32E>::kSmem <= 227 * 1024, "pair kernel smem");
 static_assert(PairCfg<kModeBF16>::kSmem <= 227 * 1024, "pair kernel smem");
+static_assert(PairCfg<kModeF32E, true>::kSmem <= 227 * 1024, "pair kernel smem");
+template <int MODE, int V>
+constexpr bool pair_narrow() { return FFG_NARROW_STAGING && V == 0 && ModeTraits<MODE>::kHasLo; }
 static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue warps alike");
 
 // TMEM: 4 slots x 128 columns.  A CHUNK is accumulated into the next slot of the ring.
@@ -639,7 +646,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     constexpr bool S16 = V == 2;
     constexpr int kSlots = RES ? 3 : 4;  // TMEM chunk ring (resident: slot 3 holds the X block)
     using Tr = ModeTraits<MODE>;
-    using Cfg = PairCfg<MODE>;
+    constexpr bool kNarrow = pair_narrow<MODE, V>();
+    using Cfg = PairCfg<MODE, kNarrow>;
     // (FP32-emulated only: a K-block pair there is 1.5K MMA cycles, enough to hide the polls)
     constexpr bool kBlockDeps = FFG_BLOCK_DEPS && !RES && Tr::kHasLo;
     constexpr bool kDrain = Tr::kProducts == 3;
@@ -1033,7 +1041,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const int r = q * 32 + lane;       // block row of this thread
         const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
         const int np = p.np, n = p.n;
-        uint8_t* stg = smem + Cfg::kStagingOff + ew * 4 * kPieceBytes;
+        uint8_t* stg = smem + Cfg::kStagingOff + ew * (kNarrow ? 2 : 4) * kPieceBytes;
         const uint32_t stg_a = smem_u32(stg);
         const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
         int g = 0;
@@ -1147,7 +1155,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 }
                 const long long t_c1 = (p.dbg & 8) ? clock64() : 0;
                 if (p.dbg & 8) w_cmp += (unsigned long long)(t_c1 - t_c0);
-                if (!last) {
+                if (kNarrow && !last && !(p.dbg & 32)) {
+                    // direct pieces out, then the mirrors transposed in place once the direct stores
+                    // have read the staging
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tm.p_hi[nxt], stg, C * kBN + 32 * qc, m * np + R * kBM + 32 * q);
+                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, C * kBN + 32 * qc, m * np + R * kBM + 32 * q);
+                        tma_store_commit();
+                    }
+                    if (!dblk) {
+                        if (lane == 0) tma_store_wait_read();
+                        __syncwarp();
+                        transpose_piece_inplace(stg_a, lane);
+                        if (Tr::kHasLo) transpose_piece_inplace(stg_a + kPieceBytes, lane);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tm.p_hi[nxt], stg, R * kBM + 32 * q, m * np + C * kBN + 32 * qc);
+                            if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, R * kBM + 32 * q, m * np + C * kBN + 32 * qc);
+                        }
+                    }
+                } else if (!last) {
                     if (!dblk) {  // mirrored pieces: warp transpose of the direct pieces
                         __syncwarp();
                         transpose_piece(stg_a, stg_a + 2 * kPieceBytes, lane);
