@@ -17,16 +17,22 @@
 // also order the WAR hazard on the hi/lo parity a layer overwrites: every reader of panels
 // A_c and S at layer l-1 is one of the blocks those counters wait for.
 //
-// Per CTA (640 threads, warp-specialised, setmaxnreg 32/104/120):
+// Single-matrix groups also track per-block completion (bflags) and a producer whose panels are
+// not complete yet waits per 128-column block just before loading it.
+//
+// Per CTA (640 threads, warp-specialised, setmaxnreg 48/104/112):
 //   warp 0        TMA producer: A_hi, A_lo (128 x 64) of panel A_c and this CTA's half
 //                 (64 x 64) of B_hi, B_lo of panel S; complete_tx on the LEADER's full barrier
 //   warp 1        TMEM allocator (both CTAs) / UMMA issuer (leader only)
-//   warps 4-11    drain the hi*hi TMEM ring (round-to-nearest register sums) -> Y in TMEM
-//   warps 12-19   epilogue (unchanged arithmetic, kernels.cuh): X' = aY + bX + cI,
-//                 A += d'X', binary16 split, direct + mirrored 32x32 pieces by TMA store;
+//   warps 4-11    drain the chunk ring (round-to-nearest register sums) -> Y in TMEM
+//   warps 12-19   epilogue (epilogue.cuh): X' = aY + bX + cI, A += d'X' (L2 reductions, paired
+//                 over two layers), binary16 split, direct + mirrored 32x32 pieces by TMA store;
 //                 last layer: D = A + X_L and the per-block statistics.
-// Accumulation precision: hi*hi is drained after every MMA for the first
-// `exact_layers` layers and after every K-block afterwards; hi*lo + lo*hi accumulate apart.
+// Variants (template V): 1 resident (one block per CTA for all layers), 2 sixteen workers that
+// drain and finish one 32-column piece each (np <= 512).
+// Accumulation precision: in the first `exact_layers` layers hi is a fixed-point split
+// and hi*hi accumulates EXACTLY over the whole K in its own TMEM accumulator (cross terms and
+// lo*lo in a second); later layers drain every two K-blocks into round-to-nearest registers.
 #pragma once
 #include <type_traits>
 
