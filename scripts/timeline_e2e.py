@@ -37,3 +37,10 @@ print("span", (ev[-1]["ts"] + ev[-1]["dur"] - t0), "us for 4 calls")
 if os.environ.get("TL_DUMP"):
     for e in ev:
         print(f"{e['ts'] - t0:9.1f} {e['dur']:8.1f} s{e.get('args', {}).get('stream', '?')} {e['name'][:50]}")
+# copy-engine utilisation over the captured span
+span = ev[-1]["ts"] + ev[-1]["dur"] - t0
+for tag in ("HtoD", "DtoH"):
+    busy = sum(e["dur"] for e in ev if e["cat"] == "gpu_memcpy" and tag in e["name"])
+    print(f"{tag} engine busy {busy / span:.2f} of the span")
+kb = sum(e["dur"] for e in ev if e["cat"] == "kernel")
+print(f"kernels busy {kb / span:.2f} of the span")
