@@ -606,15 +606,14 @@ int launch_pair_mode(int mode, const PairMaps& maps, const PairParams& pp, int64
     }
 }
 
-// np <= 512: sixteen drain+epilogue workers, each finishing one 32-column piece straight from its
-// registers (Y never holds a TMEM slot).  Measured: 512 x N=512 BF16 -24%, FP32E -6%; 64 x N=256 FP32E
-// -18%; slower at N >= 1024 (the MMA starves while all sixteen warps are in the epilogue).  FFG_S16=0/1
-// overrides.
+// np <= 512 (single-product modes: np <= 1024): sixteen drain+epilogue workers, each finishing one
+// 32-column piece straight from its registers (Y never holds a TMEM slot).  Measured: 512 x N=512 BF16
+// -24%, FP32E -6%; 64 x N=256 FP32E -18%; 16 x N=1024 BF16 -6%, FP32E +13%; N=4096 BF16 +10% (the MMA
+// starves while all sixteen warps are in the epilogue).  FFG_S16=0/1 overrides.
 bool use_s16(int mode, int64_t np) {
     const char* e = getenv("FFG_S16");
     if (e) return atoi(e) != 0;
-    (void)mode;
-    return np <= 512;
+    return np <= 512 || (mode != kModeF32E && np <= 1024);
 }
 
 // Resident K2 (one block per CTA for the whole recursion, k2_pair.cuh resident_workers) when
