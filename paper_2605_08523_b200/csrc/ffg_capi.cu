@@ -608,12 +608,13 @@ int launch_pair_mode(int mode, const PairMaps& maps, const PairParams& pp, int64
 
 // np <= 512 (single-product modes: np <= 1024): sixteen drain+epilogue workers, each finishing one
 // 32-column piece straight from its registers (Y never holds a TMEM slot).  Measured: 512 x N=512 BF16
-// -24%, FP32E -6%; 64 x N=256 FP32E -18%; 16 x N=1024 BF16 -6%, FP32E +13%; N=4096 BF16 +10% (the MMA
-// starves while all sixteen warps are in the epilogue).  FFG_S16=0/1 overrides.
-bool use_s16(int mode, int64_t np) {
+// -24%, FP32E -6%; 64 x N=256 FP32E -18%; 16 x N=1024 BF16 -6%, FP32E +13%; one N=1024 matrix FP32E -10%,
+// BF16 -19%; N=4096 BF16 +10% (the MMA starves while all sixteen warps are in the epilogue).  FFG_S16=0/1
+// overrides.
+bool use_s16(int mode, int64_t np, int B) {
     const char* e = getenv("FFG_S16");
     if (e) return atoi(e) != 0;
-    return np <= 512 || (mode != kModeF32E && np <= 1024);
+    return np <= 512 || (np <= 1024 && (mode != kModeF32E || B == 1));
 }
 
 // Resident K2 (one block per CTA for the whole recursion, k2_pair.cuh resident_workers) when
@@ -814,7 +815,7 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
                 if ((rc = launch_pair_mode<1>(j.mode, w.pmaps, gp, (int64_t)gp.B * w.PT, st))) return rc;
             }
         } else {
-            const bool s16 = use_s16(j.mode, np);
+            const bool s16 = use_s16(j.mode, np, B);
             if ((rc = s16 ? pair_capacity_mode<2>(j.mode, &cap) : pair_capacity_mode<0>(j.mode, &cap))) return rc;
             pp.G = group_size(B, np, w.PT, cap, j.mode);
             // single-matrix groups: a layer is one matrix, so its items wait on each other;
