@@ -608,13 +608,15 @@ int launch_pair_mode(int mode, const PairMaps& maps, const PairParams& pp, int64
 
 // np <= 512 (single-product modes: np <= 1024): sixteen drain+epilogue workers, each finishing one
 // 32-column piece straight from its registers (Y never holds a TMEM slot).  Measured: 512 x N=512 BF16
-// -24%, FP32E -6%; 64 x N=256 FP32E -18%; 16 x N=1024 BF16 -6%, FP32E +13%; one N=1024 matrix FP32E -10%,
-// BF16 -19%; N=4096 BF16 +10% (the MMA starves while all sixteen warps are in the epilogue).  FFG_S16=0/1
-// overrides.
-bool use_s16(int mode, int64_t np, int B) {
+// -24%, FP32E -6%; 64 x N=256 FP32E -18%; 16 x N=1024 BF16 -6%, FP32E +13%; 1-4 x N=1024 FP32E -10%,
+// BF16 -19%; one N=2048 matrix BF16 -13%, FP32E -4%; 8 x N=1024 FP32E +2%; N=4096 BF16 +10% (the MMA
+// starves while all sixteen warps are in the epilogue).  FFG_S16=0/1 overrides.
+bool use_s16(int mode, int64_t np, int64_t items_per_layer, int pairs) {
     const char* e = getenv("FFG_S16");
     if (e) return atoi(e) != 0;
-    return np <= 512 || (np <= 1024 && (mode != kModeF32E || B == 1));
+    // a layer with no more items than resident pairs is latency-bound: more epilogue parallelism
+    // pays; with two or more items per pair the MMA must keep running through the epilogues
+    return np <= 512 || (np <= 1024 && mode != kModeF32E) || items_per_layer <= pairs;
 }
 
 // Resident K2 (one block per CTA for the whole recursion, k2_pair.cuh resident_workers) when
@@ -815,9 +817,10 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
                 if ((rc = launch_pair_mode<1>(j.mode, w.pmaps, gp, (int64_t)gp.B * w.PT, st))) return rc;
             }
         } else {
-            const bool s16 = use_s16(j.mode, np, B);
-            if ((rc = s16 ? pair_capacity_mode<2>(j.mode, &cap) : pair_capacity_mode<0>(j.mode, &cap))) return rc;
+            if ((rc = pair_capacity_mode<0>(j.mode, &cap))) return rc;
             pp.G = group_size(B, np, w.PT, cap, j.mode);
+            const bool s16 = use_s16(j.mode, np, (int64_t)pp.G * w.PT, cap);
+            if (s16 && (rc = pair_capacity_mode<2>(j.mode, &cap))) return rc;
             // single-matrix groups: a layer is one matrix, so its items wait on each other;
             // block-granular waits let a next-layer item start on its completed blocks
             // (measured: N=4096 -8%; in multi-matrix groups other matrices fill the gaps and
