@@ -425,23 +425,31 @@ def test_bitwise_deterministic(model):
 
 def test_schedule_invariance(model, monkeypatch):
     """The schedule changes only the order of independent work, never the arithmetic: results are
-    bit-identical across L2 group sizes (FFG_GROUP) and with block-granular dependency waits
-    forced on or off (FFG_BLOCKDEPS), for a batch and for a single matrix."""
+    bit-identical across L2 group sizes (FFG_GROUP), with block-granular dependency waits forced on
+    or off (FFG_BLOCKDEPS) and with the 16-worker epilogue forced on or off (FFG_S16; D bit-identical,
+    the fp64 block statistics to 1e-13), for a batch and for a single matrix."""
     mu, kT = batch_params(6)
     Hs = [tight_binding(512, seed=500 + k) for k in range(6)]
     ref_b, st_b, _ = E.compute_density_matrices(Hs, mu, kT, model)
     H1 = tight_binding(1024, seed=9)
     ref_1, st_1, _ = E.compute_density_matrix(H1, 0.0, 0.01, model)
     for env in ({"FFG_GROUP": "1"}, {"FFG_GROUP": "4"}, {"FFG_BLOCKDEPS": "1"}, {"FFG_BLOCKDEPS": "0"},
-                {"FFG_GROUP": "2", "FFG_BLOCKDEPS": "1"}):
+                {"FFG_GROUP": "2", "FFG_BLOCKDEPS": "1"}, {"FFG_S16": "0"}, {"FFG_S16": "1"}):
         with monkeypatch.context() as mp:
             for k, v in env.items():
                 mp.setenv(k, v)
             Db, sb, _ = E.compute_density_matrices(Hs, mu, kT, model)
             D1, s1, _ = E.compute_density_matrix(H1, 0.0, 0.01, model)
         assert all(np.array_equal(a, b) for a, b in zip(Db, ref_b)), env
-        assert [(s.trace, s.trace_square) for s in sb] == [(s.trace, s.trace_square) for s in st_b], env
-        assert np.array_equal(D1, ref_1) and (s1.trace, s1.trace_square) == (st_1.trace, st_1.trace_square), env
+        assert np.array_equal(D1, ref_1), env
+        got = [(s.trace, s.trace_square) for s in sb] + [(s1.trace, s1.trace_square)]
+        want = [(s.trace, s.trace_square) for s in st_b] + [(st_1.trace, st_1.trace_square)]
+        if "FFG_S16" in env:
+            # the two epilogues reduce a block's statistics over different warp splits (each in a
+            # fixed order), so the fp64 sums may differ in the last bits
+            np.testing.assert_allclose(np.array(got), np.array(want), rtol=1e-13, err_msg=str(env))
+        else:
+            assert got == want, env
 
 
 def test_fp32e_gates_at_n2048_vs_fp64_recursion(model):
