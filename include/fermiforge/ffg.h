@@ -24,6 +24,9 @@
  *                              counterpart)
  *   ffg_density_matrices_dev   the same on device-resident buffers, asynchronous
  *                              on a caller stream
+ *   ffg_rowblock_*             one large H row-block sharded over `world` GPUs, one rank per
+ *                              process (the reference permits data-parallel
+ *                              matmul with deterministic reductions)
  *
  * Coefficients are the reference's Mlsp2Coefficients rows
  * (proj/core/include/fermiforge/scalar_models.hpp:80-88: a, b, c, d per layer)
@@ -92,7 +95,11 @@ typedef struct ffg_provenance {
                                  x = mu0 + (beta/beta0)(eps - mu); valid iff in [0,1]    */
     int32_t mode;
     int32_t n_layers;
-    int64_t half_products;    /* tensor-core products per density matrix: 3L / L / L   */
+    int64_t half_products;    /* tensor-core products per square summed over the layers,
+                                 counted by the K2 issuer: each covers the
+                                 upper-triangle blocks; FP32-emulated 3 per square (4 in the
+                                 fixed-point exact layers), BF16/FP16 1; 0 when no recursion
+                                 ran (out of region)                                     */
     int32_t diverged_layer;   /* first X_k (k = 0..L) non-finite, -1 if none              */
     int32_t half_range_layer; /* first X_k whose binary16 split overflowed, -1 if none    */
     int32_t status;           /* ffg_status of this matrix                                */
@@ -130,7 +137,8 @@ int ffg_density_matrix(const double* H, int64_t n, double mu, double kT, const f
 
 /* Batched: `batch` independent H (host pointers), per-matrix mu / kT.
  * D_out may be NULL or hold NULL entries; stats_out batch*2; prov batch entries or NULL.
- * Returns FFG_OK when every matrix succeeded, else the first failing status. */
+ * Returns FFG_OK when every matrix succeeded, else the first failing status.  A matrix outside
+ * the region of validity runs no recursion and its D is NaN. */
 int ffg_density_matrices(int32_t batch, const double* const* H, int64_t n, const double* mu,
                          const double* kT, const ffg_model* model, int32_t mode,
                          double* const* D_out, double* stats_out, ffg_provenance* prov);
@@ -154,6 +162,41 @@ int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, cons
                              const double* kT, const ffg_model* model, int32_t mode,
                              double* D_dev, double* stats_dev, int32_t* status_dev,
                              double* bounds_dev, void* stream);
+
+/* ---------------------------------------------------------------- row-block sharding
+ * One H of size n split by block rows (128-row blocks, nb = ceil(n/128), nb % world == 0) over
+ * `world` ranks, one process per GPU.  Rank r owns block rows [r nb/world, (r+1) nb/world) of X,
+ * A and D and computes those rows against ALL columns each layer; between layers every rank needs
+ * every rank's rows of the binary16 operands X_{l+1} (hi / lo): the caller all-gathers them
+ * in place (NCCL) -- the operand buffers are [np][np] row-major with this rank's rows at
+ * [row0, row0 + rows) and the same layout on every rank.  Each block is computed with the exact
+ * arithmetic of the single-GPU path (pair-table cross-order bit), so the assembled D equals the
+ * single-GPU D bit for bit.
+ *
+ *   h = ffg_rowblock_begin(...)        K1 on the whole (replicated) H: operands of X_0 for every
+ *                                      row, X_0 / A_1 for this rank's rows, Gershgorin bounds
+ *   for l in 0 .. L-1:
+ *       ffg_rowblock_layer(h, l, ...)  layer l on this rank's rows (reads operand parity l & 1,
+ *                                      writes this rank's rows of parity (l + 1) & 1; the last
+ *                                      layer writes D_rows and the statistics partials)
+ *       all-gather parity (l + 1) & 1  (caller; not after the last layer)
+ *   ffg_rowblock_end(h, ...)           this rank's partial {sum_i D_ii, sum_ij D_ij^2} over its
+ *                                      rows, status; frees the handle
+ * All calls are asynchronous on `stream` except end (synchronises). */
+typedef struct ffg_rowblock ffg_rowblock;
+int ffg_rowblock_begin(const double* H_dev, int64_t n, double mu, double kT, const ffg_model* model,
+                       int32_t mode, int32_t rank, int32_t world, void* stream, ffg_rowblock** handle);
+/* this rank's element rows [row0, row0 + rows) (rows of D_rows: min(row0 + rows, n) - row0), np */
+int ffg_rowblock_rows(const ffg_rowblock* h, int64_t* row0, int64_t* rows, int64_t* np);
+/* device pointers of operand parity `parity` (0/1): hi and lo ([np][np] uint16; lo NULL in
+ * BF16 / FP16 mode) */
+int ffg_rowblock_operands(ffg_rowblock* h, int32_t parity, void** hi, void** lo);
+/* layer `layer` (0 .. n_layers-1, in order); D_rows [rows][n] fp64 device, used by the last layer */
+int ffg_rowblock_layer(ffg_rowblock* h, int32_t layer, double* D_rows, void* stream);
+/* partial_stats: {sum over this rank's rows of D_ii, of D_ij^2}; status: ffg_status of the matrix
+ * (out of region, diverged, half range); prov may be NULL. */
+int ffg_rowblock_end(ffg_rowblock* h, double* partial_stats, int32_t* status, ffg_provenance* prov,
+                     void* stream);
 
 /* ---------------------------------------------------------------- workflow
  * Callers of the density-matrix path built on the same pipeline: every call below runs
@@ -210,10 +253,12 @@ int ffg_profile_read(double* total_ms, int64_t* launches);
  * the profiled launches. */
 int ffg_profile_read_ex(double* total_ms, int64_t* launches, double* algorithmic_flops);
 /* Introspection of the K2 work decomposition (pure host): the pair table for an nb x nb
- * grid of 128-blocks, entries A0 | A1 << 10 | S << 20 | dummy << 30 (blocks (A0,S) and
- * (A1,S) share B panel S).  Writes min(count, capacity) entries; returns count, -1 on a
- * bad nb. */
+ * grid of 128-blocks, entries A0 | A1 << 10 | S << 20 | dummy << 30 | swap << 31 (blocks
+ * (A0,S) and (A1,S) share B panel S; swap: cross terms in swapped order).  Writes
+ * min(count, capacity) entries; returns count, -1 on bad arguments.  ffg_rowblock_table: rank
+ * `rank` of `world`'s row-block table. */
 int32_t ffg_pair_table(int32_t nb, uint32_t* out, int32_t capacity);
+int32_t ffg_rowblock_table(int32_t nb, int32_t rank, int32_t world, uint32_t* out, int32_t capacity);
 
 /* Release cached device workspaces of the calling process. */
 void ffg_release_workspaces(void);

@@ -41,6 +41,11 @@ def g17(v: float) -> str:
     return "%.17g" % float(v)
 
 
+def now_utc() -> str:
+    import datetime
+    return datetime.datetime.now(datetime.timezone.utc).strftime("%Y-%m-%dT%H:%M:%SZ")
+
+
 def train(name: str) -> dict:
     c = CONFIGS[name]
     R = O.ref()
@@ -51,6 +56,7 @@ def train(name: str) -> dict:
     if L < 0:
         raise RuntimeError(R.ffr_last_error().decode())
     return {
+        "schema_version": 1, "created": now_utc(),
         "name": name, "architecture": "mlsp2", "beta0": g17(c["beta0"]), "mu0": g17(c["mu0"]),
         "training": {k: c[k] for k in ("layers", "samples", "max_iter", "seed")} | {"weighting": "derivative"},
         "report": {"final_max_error": rep[0], "final_rms_error": rep[1], "iterations": int(rep[2]),
@@ -74,6 +80,7 @@ def train_entropy(name: str) -> dict:
     if rc < 0:
         raise RuntimeError(R.ffr_last_error().decode())
     return {
+        "schema_version": 1, "created": now_utc(),
         "name": name, "architecture": "entropy", "base": c["base"], "beta0": g17(m["beta0"]),
         "mu0": g17(m["mu0"]), "alpha": g17(alpha.value),
         "training": {k: c[k] for k in ("samples", "max_iter", "seed")} | {"weighting": "derivative"},
@@ -101,6 +108,7 @@ def main():
             with open(path) as f:
                 old = json.load(f)
             assert old["layers"] == d["layers"], f"{name}: trainer no longer bit-identical"
+            d["created"] = old.get("created", d["created"])
         with open(path, "w") as f:
             json.dump(d, f, indent=1)
         print(name, d["report"])
@@ -126,6 +134,7 @@ def main():
                     old = json.load(f)
                 assert old["layers"] == d["layers"] and old["alpha"] == d["alpha"], \
                     f"{name}: trainer no longer bit-identical"
+                d["created"] = old.get("created", d["created"])
             with open(path, "w") as f:
                 json.dump(d, f, indent=1)
             print(name, d["report"])

@@ -18,6 +18,8 @@ struct EpiCoef {
     float dc_hi, dc_lo;  // paired A updates: this layer's d, applied to the input X (0: none)
     bool red;            // this layer adds (dc X + d X') into A
     bool fixed;          // split X' with the fixed-point hi (the next layer accumulates hi*hi exactly)
+    bool sr;             // ... and round its lo stochastically (the first sr_layers layers)
+    uint32_t layer;      // the layer whose operands the split produces (stochastic-rounding hash)
 };
 
 // Layer l's coefficients as hi/lo fp32 pairs, split on the host from the fp64 model (hi = rn_f32(v),
@@ -28,7 +30,7 @@ struct EpiCoef {
 // instead of queueing on a copy engine behind the host path's matrix transfers.
 __device__ __forceinline__ EpiCoef load_coef(const float4* coef, int l, int n_layers, bool paired) {
     const float4 u = __ldg(coef + 2 * l), w = __ldg(coef + 2 * l + 1);
-    EpiCoef k{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w, 0.0f, 0.0f, l + 1 < n_layers, false};
+    EpiCoef k{u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w, 0.0f, 0.0f, l + 1 < n_layers, false, false, (uint32_t)(l + 1)};
     if (paired) {
         if (l & 1) {
             const float4 wp = __ldg(coef + 2 * (l - 1) + 1);
@@ -91,11 +93,13 @@ __device__ __forceinline__ float acc_step(float a, float x, const EpiCoef& k) {
 
 // packed binary16 split of two values: hi = rn(x * 2^14), lo = rn(x * 2^14 - hi)
 // (bf16 mode: hi = rn_bf16(x), lo = 0).  fixed (FP32E, the layers before `exact_layers`): hi is
-// rounded to a multiple of 8 in the 2^14-scaled domain (x on a 2^-11 grid; exact in binary16 for
-// |x| < 2), so the next layer's hi*hi products and all their partial sums lie on the 2^6 grid and
-// an fp32 accumulator adds them exactly (|sums| < 2^30 for a spectrum in [0, 1]).
+// rounded to a multiple of 8 in the 2^14-scaled domain (x on a 2^-11 grid, or 2^-10 where binary16
+// rounds it again for |x| >= 1), so the next layer's hi*hi products and all their partial sums lie on
+// the 2^6 grid and an fp32 accumulator adds them exactly (|sums| < 2^30 for a spectrum in [0, 1]);
+// lo is then rounded stochastically with the element hashes h0, h1 (kernels.cuh sr_hash).
 template <int MODE>
-__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo, bool fixed = false) {
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo, bool fixed = false,
+                                       bool sr = false, uint32_t h0 = 0, uint32_t h1 = 0) {
     if constexpr (MODE == kModeBF16) {
         const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
         hi = *reinterpret_cast<const uint32_t*>(&h);
@@ -108,7 +112,12 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
         hi = *reinterpret_cast<const uint32_t*>(&h);
         if constexpr (MODE == kModeF32E) {
             const float2 f = __half22float2(h);
-            const __half2 r = __floats2half2_rn(s0 - f.x, s1 - f.y);
+            float r0 = s0 - f.x, r1 = s1 - f.y;  // exact
+            if (FFG_SR_LO && fixed && sr) {
+                r0 = sr_f16_grid(r0, h0);
+                r1 = sr_f16_grid(r1, h1);
+            }
+            const __half2 r = __floats2half2_rn(r0, r1);
             lo = *reinterpret_cast<const uint32_t*>(&r);
         } else {
             lo = 0u;
@@ -200,10 +209,13 @@ __device__ __forceinline__ void epi_loadx16(const float* Xt, int r, int c0, floa
 // columns >= r are owned (the rest is the mirror of owned values) and the identity term is
 // added at column r.  dblk: the 32x32 piece itself is on the diagonal and is completed
 // symmetrically in place.
+// gi / gj0: global row of this thread and first global column of the block (stochastic-rounding
+// hashes of the fixed-point split).
 template <int MODE, bool DIAG>
 __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const float4 (&xq)[4], float* Xt, float* At,
                                                 int r, int c0, int lane, int sub, bool c_on, const EpiCoef& k,
-                                                uint32_t stg_d, bool dblk, EpiHealth& hl, bool nomem = false) {
+                                                uint32_t stg_d, bool dblk, EpiHealth& hl, int gi, int gj0,
+                                                bool nomem = false) {
     using Tr = ModeTraits<MODE>;
     uint32_t hp[8], lp[8];
 #pragma unroll
@@ -229,8 +241,20 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
             __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
             if (k.red) red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
         }
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed);
+        uint32_t hh[4] = {0u, 0u, 0u, 0u};
+        if (MODE == kModeF32E && FFG_SR_LO && k.sr) {
+            // sr_hash(gi, gj, layer) incrementally: the key of {i, j} is (min << 16) | max; a block
+            // below the diagonal has j < i for all elements (a diagonal block's j < i elements are
+            // mirrors, their values unused)
+            const bool lower = gi >= gj0 + kBN;
+            const uint32_t kb = lower ? ((uint32_t)(gj0 + c0) << 16) + (uint32_t)gi
+                                      : ((uint32_t)gi << 16) + (uint32_t)(gj0 + c0);
+            const uint32_t ks = lower ? 65536u : 1u;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hh[e] = sr_mix(kb + (uint32_t)(4 * j + e) * ks, k.layer);
+        }
+        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed, k.sr, hh[0], hh[1]);
+        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed, k.sr, hh[2], hh[3]);
     }
     if (!dblk) {
         sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
@@ -259,12 +283,14 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
 }
 
 // Last layer: D = A + X_L (fp64, full symmetric storage) and the statistics of the owned
-// elements (Tr D, sum D^2 with off-diagonal elements counted twice); sixteen columns.
+// elements (Tr D, sum D^2 with off-diagonal elements counted twice); sixteen columns.  mir = false
+// (row-block table, off the diagonal blocks): only the direct entry, counted once -- the mirrored
+// entry belongs to another rank's rows, which computes it itself.
 template <bool DIAG>
 __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const float* Xt, const float* At,
                                              int r, int c0, int gi, int gj0, int n, bool c_on,
                                              const EpiCoef& k, double* Dm, EpiHealth& hl, double& tr,
-                                             double& sq) {
+                                             double& sq, bool mir = true) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const float4 xq = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
@@ -284,13 +310,13 @@ __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const floa
                 const double dv = (double)as[e] + (double)fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]) + (double)xn;
                 if (Dm) {
                     Dm[(size_t)gi * n + gj] = dv;
-                    if (!dg) Dm[(size_t)gj * n + gi] = dv;
+                    if (!dg && (DIAG || mir)) Dm[(size_t)gj * n + gi] = dv;
                 }
                 if (dg) {
                     tr += dv;
                     sq += dv * dv;
                 } else {
-                    sq += 2.0 * dv * dv;
+                    sq += ((DIAG || mir) ? 2.0 : 1.0) * dv * dv;
                 }
             }
         }

@@ -2,8 +2,8 @@
 //
 // Validation mirrors the reference (ModelCoefficients::validate
 // scalar_models.cpp:133-171, FermiParams::validate :27-34); then the device
-// pipeline  reset -> K1 rescale_gershgorin -> L x K2 mlsp2_layer -> K3 finalize
-// is enqueued on one stream.  No CPU fallback: without an sm_100 device every
+// pipeline  reset -> K1 rescale_tiles -> K2 mlsp2_pair_kernel (all layers) -> K3 finalize
+// is enqueued on the caller's stream, with K2 forked to the device's K2 stream (DevState).  No CPU fallback: without an sm_100 device every
 // compute entry point fails with FFG_ERR_CUDA.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -134,6 +134,10 @@ int make_map(CUtensorMap* tm, void* base, int64_t rows, int64_t np, int elem, in
 }
 
 // --------------------------------------------------------------------- workspace
+// Per-matrix record read back by the host paths: stats {Tr D, Tr D^2}, widened bounds
+// {eps_min, eps_max, x_min, x_max}, status, flags {non-finite layer, half-range layer}, products.
+constexpr size_t kRecordBytes = 2 * 8 + 4 * 8 + 4 + 2 * 4 + 4;
+
 // One in-flight batch of the host-buffer path: device staging, pinned per-matrix records,
 // events, and the call parameters provenance needs at wait time.
 struct HostSlot {
@@ -149,6 +153,7 @@ struct HostSlot {
     int64_t ticket = 0;
     int B = 0;
     int64_t n = 0;
+    int PT = 0;
     int mode_api = 0;
     ffg_model model{};
     std::vector<double> mu, kT;
@@ -170,6 +175,7 @@ struct Workspace {
     double* params_host = nullptr;  // pinned mirror
     unsigned long long* bounds = nullptr;
     int* flags = nullptr;
+    uint32_t* products = nullptr;   // [B] instrumented tensor-core product passes (K2 issuer)
     double2* partials = nullptr;
     double* stats = nullptr;
     double* bounds_out = nullptr;
@@ -177,6 +183,7 @@ struct Workspace {
     void* host_small = nullptr;     // pinned readback: stats, bounds, status, flags
     size_t host_small_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // K2 runs on the device's K2 stream
     // tensor-map cache over the operand arrays hi0 lo0 hi1 lo1: [0..3] 64x128 operand boxes
     // (SW128), [4..7] 32x32 epilogue pieces (SW64)
     // pair kernel (k2_pair.cuh): panel counters, pair table, per-layer coefficients, maps
@@ -185,7 +192,8 @@ struct Workspace {
     uint32_t* pairs = nullptr;
     uint8_t* xa_used = nullptr;      // [nb][nb] blocks in the pair table's orientation
     size_t cap_used = 0;
-    int pairs_nb = -1, PT = 0;
+    int64_t pairs_nb = -1;  // key of the cached pair table (nb, row-block rank / world)
+    int PT = 0;
     size_t cap_pairs = 0;
     float* coef = nullptr;              // [L][8] hi/lo fp32 coefficients (load_coef)
     size_t cap_coef = 0;
@@ -232,6 +240,7 @@ void free_ws(Workspace* w) {
     cudaFreeHost(w->params_host);
     cudaFree(w->bounds);
     cudaFree(w->flags);
+    cudaFree(w->products);
     cudaFree(w->partials);
     cudaFree(w->stats);
     cudaFree(w->bounds_out);
@@ -257,8 +266,8 @@ void free_ws(Workspace* w) {
     }
     for (auto& e : w->ring_ev)
         if (e) cudaEventDestroy(e);
-    if (w->ev0) cudaEventDestroy(w->ev0);
-    if (w->ev1) cudaEventDestroy(w->ev1);
+    for (cudaEvent_t e : {w->ev0, w->ev1, w->ev_fork, w->ev_join})
+        if (e) cudaEventDestroy(e);
 }
 
 template <typename T>
@@ -275,6 +284,8 @@ int ensure(Workspace& w, int B, int64_t np, int64_t T, bool operands) {
     if (!w.ev0) {
         CK(cudaEventCreate(&w.ev0));
         CK(cudaEventCreate(&w.ev1));
+        CK(cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming));
     }
     const size_t elems = (size_t)B * np * np;
     if (operands && elems > w.cap_elems) {
@@ -292,11 +303,12 @@ int ensure(Workspace& w, int B, int64_t np, int64_t T, bool operands) {
         CK(cudaMallocHost(&w.params_host, sizeof(double) * 4 * B));
         if ((rc = grow(&w.bounds, dummy, (size_t)2 * B))) return rc;
         if ((rc = grow(&w.flags, dummy, (size_t)2 * B))) return rc;
+        if ((rc = grow(&w.products, dummy, (size_t)B))) return rc;
         if ((rc = grow(&w.stats, dummy, (size_t)2 * B))) return rc;
         if ((rc = grow(&w.bounds_out, dummy, (size_t)4 * B))) return rc;
         if ((rc = grow(&w.status, dummy, (size_t)B))) return rc;
         cudaFreeHost(w.host_small);
-        w.host_small_bytes = (size_t)B * (2 * 8 + 4 * 8 + 4 + 8);
+        w.host_small_bytes = (size_t)B * kRecordBytes;
         CK(cudaMallocHost(&w.host_small, w.host_small_bytes));
         w.cap_B = B;
     }
@@ -385,7 +397,7 @@ std::vector<uint32_t> pair_table(int nb) {
 
 // --------------------------------------------------------------------- small kernels
 __global__ void reset_kernel(unsigned long long* bounds, int* flags, int B,
-                             uint32_t* counters = nullptr, int n_counters = 0) {
+                             uint32_t* counters = nullptr, int n_counters = 0, uint32_t* products = nullptr) {
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m < n_counters) counters[m] = 0u;
     if (m < B) {
@@ -393,6 +405,7 @@ __global__ void reset_kernel(unsigned long long* bounds, int* flags, int B,
         bounds[2 * m + 1] = 0ull;
         flags[2 * m + 0] = INT_MAX;
         flags[2 * m + 1] = INT_MAX;
+        if (products) products[m] = 0u;
     }
 }
 
@@ -435,11 +448,20 @@ int exact_drain_layers() {
     return v;
 }
 
-// Layers after the exact ones that drain every 2 K16 steps (default 0: measurement knob)
+// Layers (from the first) whose fixed-point split rounds lo stochastically (kernels.cuh sr_hash)
+int sr_layers() {
+    static int v = [] {
+        const char* e = getenv("FFG_SR_LAYERS");
+        return e ? atoi(e) : FFG_SR_LAYERS;
+    }();
+    return v;
+}
+
+// Layers after the exact ones that drain every 2 K16 steps (measurement knob; FFG_SEMI_DRAIN builds)
 int semi_drain_layers() {
     static int v = [] {
         const char* e = getenv("FFG_SEMI_DRAIN_LAYERS");
-        return e ? atoi(e) : 0;
+        return (FFG_SEMI_DRAIN && e) ? atoi(e) : 0;
     }();
     return v;
 }
@@ -454,15 +476,11 @@ int normal_kstep() {
     return v;
 }
 
-// Paired A updates (every other layer reduces d_l X_l + d_{l+1} X_{l+1} into A): only the streaming
-// epilogues that reduce A at L2 (epi_sub_mid_red) read the input-X term, so the resident variant
-// (FFG_RESIDENT) keeps one update per layer.
+// Paired A updates (every other layer reduces d_l X_l + d_{l+1} X_{l+1} into A at L2, epi_sub_mid_red)
 bool a_pairing() {
     static bool v = [] {
         const char* e = getenv("FFG_A_PAIR");
-        const char* r = getenv("FFG_RESIDENT");
-        const bool on = e ? atoi(e) != 0 : true;
-        return on && !(r && atoi(r) != 0);
+        return e ? atoi(e) != 0 : true;
     }();
     return v;
 }
@@ -475,32 +493,59 @@ int debug_flags() {
     return v;
 }
 
+// Per-device library state (each entry is set up on first use with that device current):
+//  * `lib`  the stream of the host-buffer entry points on this device;
+//  * `k2`   the ONE stream every K2 launch of the library on this device goes to.  K2 is a
+//           persistent kernel whose CTA pairs wait on each other's layer results, so it needs all
+//           of its CTAs co-resident: two K2 grids running side by side (two caller streams, two
+//           threads) could each hold part of the SMs and wait forever.  Serialising them on one
+//           stream (fork/join events from the caller's stream) makes that impossible;
+//  * the pair kernels' shared-memory attribute and co-resident capacity, the SM count and the
+//    watchdog buffer, all of which are per-device properties.
+struct DevState {
+    bool init = false;
+    cudaStream_t lib = nullptr, k2 = nullptr;
+    int sms = 148;
+    int cap[3][3] = {{-1, -1, -1}, {-1, -1, -1}, {-1, -1, -1}};  // [mode][V] co-resident CTA pairs
+    bool watch = false;
+};
+std::mutex g_dev_mu;
+std::map<int, DevState> g_dev;
+
 // Host-mapped watchdog record (ptx.cuh watchdog_fire): [0] fired count, [1] block,
-// [2] thread, [3] site tag, [4..5] site data.  Survives a trapped context.
+// [2] thread, [3] site tag, [4..5] site data.  Survives a trapped context.  One host record
+// shared by all devices (the first trap wins).
 unsigned long long* g_watch_host = nullptr;
-int install_watchdog() {
-    static int rc = [] {
-        void* h = nullptr;
-        if (cudaHostAlloc(&h, 16 * sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess)
-            return (int)FFG_ERR_CUDA;
-        memset(h, 0, 16 * sizeof(unsigned long long));
-        void* d = nullptr;
-        if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return (int)FFG_ERR_CUDA;
-        if (cudaMemcpyToSymbol(ffg_watch_buf, &d, sizeof(d)) != cudaSuccess) return (int)FFG_ERR_CUDA;
-        g_watch_host = static_cast<unsigned long long*>(h);
-        return (int)FFG_OK;
-    }();
-    return rc;
+
+int dev_state(DevState** out) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DevState& d = g_dev[dev];
+    if (!d.init) {
+        CK(cudaStreamCreateWithFlags(&d.lib, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&d.k2, cudaStreamNonBlocking));
+        CK(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+        d.init = true;
+    }
+    *out = &d;
+    return FFG_OK;
 }
 
-int num_sms() {
-    static int v = [] {
-        int dev = 0, n = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n;
-    }();
-    return v;
+int install_watchdog(DevState& d) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (d.watch) return FFG_OK;
+    if (!g_watch_host) {
+        void* h = nullptr;
+        CK(cudaHostAlloc(&h, 16 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable));
+        memset(h, 0, 16 * sizeof(unsigned long long));
+        g_watch_host = static_cast<unsigned long long*>(h);
+    }
+    void* dp = nullptr;
+    CK(cudaHostGetDevicePointer(&dp, g_watch_host, 0));
+    CK(cudaMemcpyToSymbol(ffg_watch_buf, &dp, sizeof(dp)));
+    d.watch = true;
+    return FFG_OK;
 }
 
 // Optional CUDA-event timing of every K2 launch, for the roofline figure.
@@ -552,16 +597,19 @@ int group_size(int B, int64_t np, int PT, int resident_pairs, int mode) {
     return (B + ng - 1) / ng;
 }
 
-// Co-resident CTA pairs of the pair kernel (all pairs must be resident: the layer
-// dependencies are waited for inside the kernel).
+// Co-resident CTA pairs of the pair kernel on the current device (all pairs must be resident:
+// the layer dependencies are waited for inside the kernel).
 template <int MODE, int V>
 int pair_capacity(int* out) {
-    static int max_pairs = -1;
+    DevState* d;
+    int rc;
+    if ((rc = dev_state(&d))) return rc;
+    int& max_pairs = d->cap[MODE][V];
     if (max_pairs < 0) {
         CK(cudaFuncSetAttribute(mlsp2_pair_kernel<MODE, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PairCfg<MODE, pair_narrow<MODE, V>()>::kSmem));
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * (num_sms() / 2));
+        cfg.gridDim = dim3(2 * (d->sms / 2));
         cfg.blockDim = dim3(kPairThreads);
         cfg.dynamicSmemBytes = PairCfg<MODE, pair_narrow<MODE, V>()>::kSmem;
         int nc = 0;
@@ -573,22 +621,22 @@ int pair_capacity(int* out) {
     return FFG_OK;
 }
 
+// Launch on `st`, which must be the device's K2 stream (enqueue forks to it).
 template <int MODE, int V>
 int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
-    constexpr bool RES = V == 1;
+    DevState* d;
     int cap, rc;
     if ((rc = pair_capacity<MODE, V>(&cap))) return rc;
-    if ((rc = install_watchdog())) return set_err(FFG_ERR_CUDA, "watchdog buffer");
-    // streaming: persistent pairs walk all items round-robin; resident: exactly one CTA pair per
-    // pair item of a layer (each keeps its block for all layers), `items` = pairs per layer
-    if (RES && items > cap) return set_err(FFG_ERR_CUDA, "resident K2: %lld pairs > %d resident", (long long)items, cap);
+    if ((rc = dev_state(&d))) return rc;
+    if ((rc = install_watchdog(*d))) return rc;
+    // persistent pairs walk all items round-robin
     const int pairs = (int)std::min<int64_t>(cap, items);
     mlsp2_pair_kernel<MODE, V><<<2 * pairs, kPairThreads, PairCfg<MODE, pair_narrow<MODE, V>()>::kSmem, st>>>(maps, pp);
     CK(cudaGetLastError());
     return FFG_OK;
 }
 
-// V: 0 streaming, 1 resident, 2 streaming with 16 workers (single-product modes only)
+// V: 0 streaming, 2 streaming with 16 workers
 template <int V>
 int pair_capacity_mode(int mode, int* cap) {
     switch (mode) {
@@ -619,15 +667,6 @@ bool use_s16(int mode, int64_t np, int64_t items_per_layer, int pairs) {
     return np <= 512 || (np <= 1024 && mode != kModeF32E) || items_per_layer <= pairs;
 }
 
-// Resident K2 (one block per CTA for the whole recursion, k2_pair.cuh resident_workers) when
-// a matrix's pair table fits the co-resident CTA pairs and FFG_RESIDENT=1.
-bool use_resident(int PT, int cap) {
-    static int v = [] {
-        const char* e = getenv("FFG_RESIDENT");
-        return e ? atoi(e) : 0;  // measured slower than streaming; opt-in
-    }();
-    return v != 0 && PT <= cap;
-}
 
 struct Job {
     int B = 0;
@@ -643,9 +682,50 @@ struct Job {
     double* stats_dev = nullptr;        // [B][2] or null (-> workspace)
     int* status_dev = nullptr;          // [B] or null (-> workspace)
     double* bounds_dev = nullptr;       // [B][4] or null (-> workspace)
+    int exact_layers = -1;              // fixed-point exact layers (FP32E); -1: the default
+    int rb_world = 0, rb_rank = 0;      // row-block mode (B = 1): this rank's block rows of `world`
 };
 
-int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L) {
+// Block rows [r0, r1) of rank `rank` of `world` (nb % world == 0, checked by the caller).
+void rowblock_rows(int nb, int rank, int world, int* r0, int* r1) {
+    *r0 = nb / world * rank;
+    *r1 = nb / world * (rank + 1);
+}
+
+// Row-block table: every block (R, C) of block rows [r0, r1) and ALL columns,
+// as pair items (R, R+1, C).  Each block gets exactly the values the symmetric table gives it: a
+// block the symmetric table computes in the other orientation, (C, R), is computed here with the
+// cross terms in swapped order (bit 31; k2_pair.cuh), which makes it the exact transpose.  A row pair
+// whose two blocks disagree on that bit runs as two half items (dummy partner, bit 30).
+std::vector<uint32_t> rowblock_table(int nb, int r0, int r1) {
+    const std::vector<uint32_t> sym = pair_table(nb);
+    std::vector<int> arow((size_t)nb * nb, -1);  // [min * nb + max] -> the A-panel row computing it
+    auto key = [nb](int a, int b) { return (size_t)std::min(a, b) * nb + std::max(a, b); };
+    for (uint32_t e : sym) {
+        const int a0 = e & 1023, a1 = (e >> 10) & 1023, sp = (e >> 20) & 1023;
+        arow[key(a0, sp)] = a0;
+        if (!((e >> 30) & 1)) arow[key(a1, sp)] = a1;
+    }
+    auto swp = [&](int R, int C) -> uint32_t { return (R != C && arow[key(R, C)] != R) ? 1u : 0u; };
+    std::vector<uint32_t> out;
+    for (int R = r0; R < r1; R += 2) {
+        const bool two = R + 1 < r1;
+        for (int C = 0; C < nb; ++C) {
+            const uint32_t s0 = swp(R, C);
+            if (two && s0 == swp(R + 1, C)) {
+                out.push_back((uint32_t)R | ((uint32_t)(R + 1) << 10) | ((uint32_t)C << 20) | (s0 << 31));
+            } else {
+                out.push_back((uint32_t)R | ((uint32_t)R << 10) | ((uint32_t)C << 20) | (1u << 30) | (s0 << 31));
+                if (two)
+                    out.push_back((uint32_t)(R + 1) | ((uint32_t)(R + 1) << 10) | ((uint32_t)C << 20) | (1u << 30) |
+                                  (swp(R + 1, C) << 31));
+            }
+        }
+    }
+    return out;
+}
+
+int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L, int rb_rank = 0, int rb_world = 0) {
     size_t dummy = 0;
     int rc;
     const size_t ncnt = (size_t)B * nb * (1 + nb);  // panel counters, then block flags
@@ -653,8 +733,16 @@ int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L) {
         if ((rc = grow(&w.counters, dummy, ncnt))) return rc;
         w.cap_cnt = ncnt;
     }
-    if (w.pairs_nb != nb) {
-        const std::vector<uint32_t> t = pair_table(nb);
+    const int64_t pkey = (int64_t)nb | ((int64_t)rb_rank << 24) | ((int64_t)rb_world << 44);
+    if (w.pairs_nb != pkey) {
+        std::vector<uint32_t> t;
+        if (rb_world > 0) {
+            int r0, r1;
+            rowblock_rows(nb, rb_rank, rb_world, &r0, &r1);
+            t = rowblock_table(nb, r0, r1);
+        } else {
+            t = pair_table(nb);
+        }
         if (t.size() > w.cap_pairs) {
             if ((rc = grow(&w.pairs, dummy, t.size()))) return rc;
             w.cap_pairs = t.size();
@@ -671,7 +759,7 @@ int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L) {
             w.cap_used = used.size();
         }
         CK(cudaMemcpy(w.xa_used, used.data(), used.size(), cudaMemcpyHostToDevice));
-        w.pairs_nb = nb;
+        w.pairs_nb = pkey;
         w.PT = (int)t.size();
     }
     if ((size_t)8 * L > w.cap_coef) {
@@ -699,19 +787,26 @@ int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L) {
 }
 
 // Enqueue the full pipeline for one batch on `st` (asynchronous; the small per-call host
-// arrays go through the pinned upload ring).
-int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
+// arrays go through the pinned upload ring): enqueue_k1 (uploads, reset, K1), enqueue_k2 (layers
+// [l0, l1) on the device's K2 stream), enqueue_k3.  The row-block entry points run them separately.
+struct EnqueueCtx {
+    int64_t np = 0;
+    int nb = 0;
+    int64_t Tpart = 0;
+    int exact_layers = 0;
+    RegionCheck region{};
+};
+
+int enqueue_k1(Workspace& w, const Job& j, cudaStream_t st, EnqueueCtx& cx) {
     const int B = j.B;
     const int64_t n = j.n;
     const int64_t np = (n + kBM - 1) / kBM * kBM;
     const int nb = (int)(np / kBM);
-    const int64_t T = (int64_t)nb * (nb + 1) / 2;
     const ffg_model& md = *j.model;
-    constexpr bool pair = true;  // the pair kernel (k2_pair.cuh) is the only K2
     int rc;
-    if ((rc = ensure(w, B, np, pair ? 0 : T, true))) return rc;
-    if (pair && (rc = ensure_pair(w, B, np, nb, md.n_layers))) return rc;
-    const int64_t Tpart = pair ? 2 * (int64_t)w.PT : T;  // statistics partials per matrix
+    if ((rc = ensure(w, B, np, 0, true))) return rc;
+    if ((rc = ensure_pair(w, B, np, nb, md.n_layers, j.rb_rank, j.rb_world))) return rc;
+    const int64_t Tpart = 2 * (int64_t)w.PT;  // statistics partials per matrix
     if ((size_t)B * Tpart > w.cap_T) {
         size_t dummy = 0;
         if ((rc = grow(&w.partials, dummy, (size_t)B * Tpart))) return rc;
@@ -726,26 +821,30 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
         ph[3 * B + m] = j.mu ? j.mu[m] : 0.0;
     }
     if ((rc = upload_small(w, w.params, ph.data(), sizeof(double) * 4 * B, st))) return rc;
-    if (pair) {
-        // hi/lo fp32 split of a, b, c and the next layer's d per layer (epilogue.cuh load_coef; the
-        // paired A updates are derived in the kernel from the same 8-float rows)
-        std::vector<float> cf((size_t)8 * md.n_layers);
-        auto split = [](double v, float* o) {
-            o[0] = (float)v;
-            o[1] = (float)(v - (double)o[0]);
-        };
-        for (int l = 0; l < md.n_layers; ++l) {
-            float* o = cf.data() + 8 * l;
-            split(md.abcd[4 * l + 0], o + 0);
-            split(md.abcd[4 * l + 1], o + 2);
-            split(md.abcd[4 * l + 2], o + 4);
-            split(l + 1 < md.n_layers ? md.abcd[4 * (l + 1) + 3] : 0.0, o + 6);
-        }
-        if ((rc = upload_small(w, w.coef, cf.data(), sizeof(float) * cf.size(), st))) return rc;
+    // hi/lo fp32 split of a, b, c and the next layer's d per layer (epilogue.cuh load_coef; the
+    // paired A updates are derived in the kernel from the same 8-float rows)
+    std::vector<float> cf((size_t)8 * md.n_layers);
+    auto split = [](double v, float* o) {
+        o[0] = (float)v;
+        o[1] = (float)(v - (double)o[0]);
+    };
+    for (int l = 0; l < md.n_layers; ++l) {
+        float* o = cf.data() + 8 * l;
+        split(md.abcd[4 * l + 0], o + 0);
+        split(md.abcd[4 * l + 1], o + 2);
+        split(md.abcd[4 * l + 2], o + 4);
+        split(l + 1 < md.n_layers ? md.abcd[4 * (l + 1) + 3] : 0.0, o + 6);
     }
-    const int ncnt = pair ? B * nb * (1 + nb) : 0;
-    reset_kernel<<<(std::max(B, ncnt) + 127) / 128, 128, 0, st>>>(w.bounds, w.flags, B, w.counters, ncnt);
+    if ((rc = upload_small(w, w.coef, cf.data(), sizeof(float) * cf.size(), st))) return rc;
+    const int ncnt = B * nb * (1 + nb);
+    reset_kernel<<<(std::max(B, ncnt) + 127) / 128, 128, 0, st>>>(w.bounds, w.flags, B, w.counters, ncnt,
+                                                                 w.products);
     CK(cudaGetLastError());
+    cx.np = np;
+    cx.nb = nb;
+    cx.Tpart = Tpart;
+    cx.exact_layers = j.exact_layers >= 0 ? j.exact_layers : exact_drain_layers();
+    cx.region = RegionCheck{w.bounds, j.scale ? w.params + 2 * B : nullptr, w.params + 3 * B, md.mu0};
 
     RescaleParams rp{};
     rp.H = j.H_dev;
@@ -761,105 +860,139 @@ int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
     rp.n = (int)n;
     rp.np = (int)np;
     rp.mode = j.mode;
-    rp.write_operands = 1;
-    rp.fixed = (pair && FFG_FIXED_SPLIT && j.mode == kModeF32E && exact_drain_layers() > 0) ? 1 : 0;
+    rp.fixed = (FFG_FIXED_SPLIT && j.mode == kModeF32E && cx.exact_layers > 0) ? 1 : 0;
+    rp.sr = (rp.fixed && sr_layers() > 0) ? 1 : 0;
     rp.xa_used = w.xa_used;   // X/A stores only for the blocks K2 reads
     rescale_tiles_kernel<<<dim3((unsigned)(np / kK1Rows), (unsigned)B), 256, 0, st>>>(rp);
-    CK(cudaGetLastError());
-
-    const double layer_flops = (double)B * ((j.mode == kModeF32E) ? 3.0 : 1.0) * (double)n * n * (n + 1);
-    if (pair) {
-        PairParams pp{};
-        pp.X = w.X;
-        pp.A = w.A;
-        pp.D = j.D_dev;
-        pp.partials = w.partials;
-        pp.flags = w.flags;
-        pp.counters = w.counters;
-        pp.bflags = w.counters + (size_t)B * nb;
-        pp.pairs = w.pairs;
-        pp.coef = reinterpret_cast<const float4*>(w.coef);
-        pp.a_pair = a_pairing() ? 1 : 0;
-        pp.n = (int)n;
-        pp.np = (int)np;
-        pp.nb = nb;
-        pp.PT = w.PT;
-        pp.B = B;
-        pp.hi[0] = w.op[0];
-        pp.lo[0] = w.op[1];
-        pp.hi[1] = w.op[2];
-        pp.lo[1] = w.op[3];
-        pp.l0 = 0;
-        pp.l1 = md.n_layers;
-        pp.n_layers = md.n_layers;
-        pp.exact_layers = exact_drain_layers();
-        pp.semi_layers = semi_drain_layers();
-        pp.normal_kstep = normal_kstep();
-        pp.dbg = debug_flags();
-        if (pp.dbg & 8) {
-            static unsigned long long* prof = nullptr;
-            if (!prof) CK(cudaMallocManaged(&prof, sizeof(unsigned long long) * 16 * 2 * 512));
-            pp.prof = prof;
-            g_prof_buf = prof;
-        }
-        int cap_res = 0, cap = 0;
-        if ((rc = pair_capacity_mode<1>(j.mode, &cap_res))) return rc;
-        cudaEvent_t stop;
-        if ((rc = prof_begin(st, &stop, layer_flops * md.n_layers))) return rc;
-        if (use_resident(w.PT, cap_res)) {
-            // resident: groups of G matrices, one CTA pair per pair item for all layers
-            const int G = std::max(1, cap_res / w.PT);
-            for (int m0 = 0; m0 < B; m0 += G) {
-                PairParams gp = pp;
-                gp.m0 = m0;
-                gp.B = std::min(G, B - m0);
-                gp.G = gp.B;
-                if ((rc = launch_pair_mode<1>(j.mode, w.pmaps, gp, (int64_t)gp.B * w.PT, st))) return rc;
-            }
-        } else {
-            if ((rc = pair_capacity_mode<0>(j.mode, &cap))) return rc;
-            pp.G = group_size(B, np, w.PT, cap, j.mode);
-            const bool s16 = use_s16(j.mode, np, (int64_t)pp.G * w.PT, cap);
-            if (s16 && (rc = pair_capacity_mode<2>(j.mode, &cap))) return rc;
-            // single-matrix groups: a layer is one matrix, so its items wait on each other;
-            // block-granular waits let a next-layer item start on its completed blocks
-            // (measured: N=4096 -8%; in multi-matrix groups other matrices fill the gaps and
-            // the extra polls cost 2-5%)
-            const char* bd = getenv("FFG_BLOCKDEPS");
-            pp.blockdeps = bd ? atoi(bd) : (pp.G == 1);
-            const int64_t items = (int64_t)md.n_layers * B * w.PT;
-            if ((rc = s16 ? launch_pair_mode<2>(j.mode, w.pmaps, pp, items, st)
-                          : launch_pair_mode<0>(j.mode, w.pmaps, pp, items, st)))
-                return rc;
-        }
-        if (stop) CK(cudaEventRecord(stop, st));
-    }
-    FinalizeParams fp{};
-    fp.partials = w.partials;
-    fp.bounds = w.bounds;
-    fp.flags = w.flags;
-    fp.scale = j.scale ? w.params + 2 * B : nullptr;
-    fp.mu = w.params + 3 * B;
-    fp.mu0 = md.mu0;
-    fp.T = (int)Tpart;
-    fp.B = B;
-    fp.stats = j.stats_dev ? j.stats_dev : w.stats;
-    fp.bounds_out = j.bounds_dev ? j.bounds_dev : w.bounds_out;
-    fp.status = j.status_dev ? j.status_dev : w.status;
-    finalize_stats_kernel<<<B, 256, 0, st>>>(fp);
     CK(cudaGetLastError());
     return FFG_OK;
 }
 
-cudaStream_t lib_stream() {
-    static cudaStream_t s = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] { cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); });
-    return s;
+// K2 over layers [l0, l1): forked from `st` to the device's K2 stream (DevState) and joined back.
+int enqueue_k2(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx, int l0, int l1) {
+    const int B = j.B;
+    const int64_t n = j.n;
+    const ffg_model& md = *j.model;
+    const bool rowblock = j.rb_world > 0;
+    int rc;
+    PairParams pp{};
+    pp.X = w.X;
+    pp.A = w.A;
+    pp.D = (l1 == md.n_layers) ? j.D_dev : nullptr;
+    pp.partials = w.partials;
+    pp.flags = w.flags;
+    pp.counters = w.counters;
+    pp.bflags = w.counters + (size_t)B * cx.nb;
+    pp.pairs = w.pairs;
+    pp.coef = reinterpret_cast<const float4*>(w.coef);
+    pp.a_pair = a_pairing() ? 1 : 0;
+    pp.n = (int)n;
+    pp.np = (int)cx.np;
+    pp.nb = cx.nb;
+    pp.PT = w.PT;
+    pp.products = w.products;
+    pp.region = cx.region;
+    pp.l0 = l0;
+    pp.l1 = l1;
+    pp.n_layers = md.n_layers;
+    pp.exact_layers = cx.exact_layers;
+    pp.sr_layers = sr_layers();
+    pp.semi_layers = semi_drain_layers();
+    pp.normal_kstep = normal_kstep();
+    pp.rowblock = rowblock ? 1 : 0;
+    // algorithmic flops per layer: c N^2 (N+1) for the symmetric square; a row-block
+    // rank computes its rows x all columns, 2 c rows N^2
+    const double cmode = (j.mode == kModeF32E) ? 3.0 : 1.0;
+    double layer_flops = (double)B * cmode * (double)n * n * (n + 1);
+    if (rowblock) {
+        int r0, r1;
+        rowblock_rows(cx.nb, j.rb_rank, j.rb_world, &r0, &r1);
+        pp.drow0 = r0 * kBM;
+        const double rows = (double)(std::min<int64_t>((int64_t)r1 * kBM, n) - (int64_t)r0 * kBM);
+        layer_flops = 2.0 * cmode * rows * (double)n * n;
+    }
+    pp.dbg = debug_flags();
+    if (pp.dbg & 8) {
+        static unsigned long long* prof = nullptr;
+        if (!prof) CK(cudaMallocManaged(&prof, sizeof(unsigned long long) * 16 * 2 * 512));
+        pp.prof = prof;
+        g_prof_buf = prof;
+    }
+    DevState* d;
+    if ((rc = dev_state(&d))) return rc;
+    cudaStream_t k2s = d->k2;
+    CK(cudaEventRecord(w.ev_fork, st));
+    CK(cudaStreamWaitEvent(k2s, w.ev_fork, 0));
+    cudaEvent_t stop;
+    if ((rc = prof_begin(k2s, &stop, layer_flops * (l1 - l0)))) return rc;
+    // one persistent launch per kValidBits matrices (the kernel's validity bitmap)
+    for (int m0 = 0; m0 < B; m0 += kValidBits) {
+        const int Bl = std::min(B - m0, kValidBits);
+        PairParams lp = pp;
+        lp.m0 = m0;
+        lp.B = Bl;
+        int cap = 0;
+        if ((rc = pair_capacity_mode<0>(j.mode, &cap))) return rc;
+        lp.G = group_size(Bl, cx.np, w.PT, cap, j.mode);
+        const bool s16 = use_s16(j.mode, cx.np, (int64_t)lp.G * w.PT, cap);
+        if (s16 && (rc = pair_capacity_mode<2>(j.mode, &cap))) return rc;
+        // single-matrix groups: a layer is one matrix, so its items wait on each other;
+        // block-granular waits let a next-layer item start on its completed blocks
+        // (measured: N=4096 -8%; in multi-matrix groups other matrices fill the gaps and
+        // the extra polls cost 2-5%)
+        const char* bd = getenv("FFG_BLOCKDEPS");
+        lp.blockdeps = bd ? atoi(bd) : (lp.G == 1 && l1 - l0 > 1);
+        const int64_t items = (int64_t)(l1 - l0) * Bl * w.PT;
+        if ((rc = s16 ? launch_pair_mode<2>(j.mode, w.pmaps, lp, items, k2s)
+                      : launch_pair_mode<0>(j.mode, w.pmaps, lp, items, k2s)))
+            return rc;
+    }
+    if (stop) CK(cudaEventRecord(stop, k2s));
+    CK(cudaEventRecord(w.ev_join, k2s));
+    CK(cudaStreamWaitEvent(st, w.ev_join, 0));
+    return FFG_OK;
 }
 
+// K3: statistics, validity status, NaN D for out-of-region matrices (d_rows: rows of D per matrix
+// the kernel owns -- n, or a row-block rank's rows).
+int enqueue_k3(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx, int64_t d_rows) {
+    FinalizeParams fp{};
+    fp.partials = w.partials;
+    fp.flags = w.flags;
+    fp.region = cx.region;
+    fp.T = (int)cx.Tpart;
+    fp.B = j.B;
+    fp.D = j.D_dev;
+    fp.d_elems = d_rows * j.n;
+    fp.stats = j.stats_dev ? j.stats_dev : w.stats;
+    fp.bounds_out = j.bounds_dev ? j.bounds_dev : w.bounds_out;
+    fp.status = j.status_dev ? j.status_dev : w.status;
+    finalize_stats_kernel<<<j.B, 256, 0, st>>>(fp);
+    CK(cudaGetLastError());
+    return FFG_OK;
+}
+
+int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
+    EnqueueCtx cx;
+    int rc;
+    if ((rc = enqueue_k1(w, j, st, cx))) return rc;
+    if ((rc = enqueue_k2(w, j, st, cx, 0, j.model->n_layers))) return rc;
+    return enqueue_k3(w, j, st, cx, j.n);
+}
+
+// The host-buffer entry points' stream on the current device (null on failure: ffg_last_error).
+cudaStream_t lib_stream() {
+    DevState* d;
+    return dev_state(&d) == FFG_OK ? d->lib : nullptr;
+}
+
+// products: the K2 issuer's instrumented count of product passes for this matrix (all layers, all
+// pair items); PT: pair items per layer, so products / PT = tensor-core products per square summed
+// over the layers (SPEC.md:404 multiplication accounting; each product covers the upper-triangle
+// blocks: 3 per FP32-emulated square, 4 in the fixed-point exact layers, 1 in BF16/FP16).
 void fill_prov(ffg_provenance* pv, const double* bnd, const double* kT, double mu, int status,
-               const int* flags, const ffg_model* md, int mode_api, int n, double ms) {
+               const int* flags, const ffg_model* md, int mode_api, int n, double ms, uint32_t products,
+               int PT) {
     pv->eps_min = bnd[0];
     pv->eps_max = bnd[1];
     pv->x_min = bnd[2];
@@ -869,7 +1002,7 @@ void fill_prov(ffg_provenance* pv, const double* bnd, const double* kT, double m
     pv->mu_prime = W > 0 ? (bnd[1] - mu) / W : 0.0;
     pv->mode = mode_api;
     pv->n_layers = md->n_layers;
-    pv->half_products = (int64_t)md->n_layers * (mode_api == FFG_MODE_MIXED_EMULATED ? 3 : 1);
+    pv->half_products = PT > 0 ? (int64_t)(products / (uint32_t)PT) : 0;
     pv->diverged_layer = flags[0] == INT_MAX ? -1 : flags[0];
     pv->half_range_layer = flags[1] == INT_MAX ? -1 : flags[1];
     pv->status = status;
@@ -907,7 +1040,7 @@ int e2e_chunks(int B, bool async) {
 int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, int64_t n, const double* alpha,
                 const double* gamma, const double* scale, const double* mu, const double* kT,
                 const ffg_model* md, int mode_api, int mode, double* const* D_out, int* slot_out,
-                bool async = false) {
+                bool async = false, int exact_layers = -1) {
     int rc;
     int si = -1;
     for (int k = 0; k < Workspace::kSlots; ++k)
@@ -921,7 +1054,7 @@ int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, in
         if ((rc = grow(&hsl.Ds, dummy, (size_t)B * nn))) return rc;
         hsl.cap = (size_t)B * nn;
     }
-    const size_t small = (size_t)B * (2 * 8 + 4 * 8 + 4 + 8);
+    const size_t small = (size_t)B * kRecordBytes;
     if (small > hsl.host_small_bytes) {
         cudaFreeHost(hsl.host_small);
         CK(cudaMallocHost(&hsl.host_small, small));
@@ -951,6 +1084,7 @@ int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, in
     double* h_bounds = h_stats + 2 * B;
     int* h_status = reinterpret_cast<int*>(h_bounds + 4 * B);
     int* h_flags = h_status + B;
+    uint32_t* h_prod = reinterpret_cast<uint32_t*>(h_flags + 2 * B);
     const int nchunk = e2e_chunks(B, async);
     auto chunk_range = [&](int k, int& m0, int& mb) {
         m0 = (int)((int64_t)B * k / nchunk);
@@ -979,12 +1113,14 @@ int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, in
         j.model = md;
         j.mode = mode;
         j.D_dev = want_D ? hsl.Ds + m0 * nn : nullptr;
+        j.exact_layers = exact_layers;
         if ((rc = enqueue(w, j, st))) return rc;
         // per-matrix records of this chunk (the next chunk's reset reuses the workspace)
         CK(cudaMemcpyAsync(h_stats + 2 * m0, w.stats, sizeof(double) * 2 * mb, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(h_bounds + 4 * m0, w.bounds_out, sizeof(double) * 4 * mb, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(h_status + m0, w.status, sizeof(int) * mb, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(h_flags + 2 * m0, w.flags, sizeof(int) * 2 * mb, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h_prod + m0, w.products, sizeof(uint32_t) * mb, cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(hsl.ev_done[k], st));
         if (want_D) {
             CK(cudaStreamWaitEvent(w.s_d2h, hsl.ev_done[k], 0));
@@ -1000,6 +1136,7 @@ int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, in
     hsl.ticket = ++w.next_ticket;
     hsl.B = B;
     hsl.n = n;
+    hsl.PT = w.PT;
     hsl.mode_api = mode_api;
     hsl.model = *md;
     hsl.mu.assign(mu ? mu : alpha, (mu ? mu : alpha) + B);
@@ -1024,6 +1161,7 @@ int finish_host(Workspace& w, int si, double* stats_out, ffg_provenance* prov) {
     double* h_bounds = h_stats + 2 * B;
     int* h_status = reinterpret_cast<int*>(h_bounds + 4 * B);
     int* h_flags = h_status + B;
+    const uint32_t* h_prod = reinterpret_cast<const uint32_t*>(h_flags + 2 * B);
     int first = FFG_OK, first_m = -1;
     for (int m = 0; m < B; ++m) {
         if (stats_out) {
@@ -1033,7 +1171,7 @@ int finish_host(Workspace& w, int si, double* stats_out, ffg_provenance* prov) {
         if (prov)
             fill_prov(&prov[m], h_bounds + 4 * m, hsl.has_kT ? &hsl.kT[m] : nullptr,
                       hsl.has_mu ? hsl.mu[m] : 0.0, h_status[m], h_flags + 2 * m, &hsl.model, hsl.mode_api,
-                      (int)hsl.n, ms);
+                      (int)hsl.n, ms, h_prod[m], hsl.PT);
         if (h_status[m] != FFG_OK && first == FFG_OK) {
             first = h_status[m];
             first_m = m;
@@ -1069,14 +1207,17 @@ int validate_host_call(int B, const double* const* H, int64_t n, const ffg_model
 // Host-buffer driver shared by density_matrix(ces) / apply_model / mixed_square: submit + wait.
 int run_host(int B, const double* const* H, int64_t n, const double* alpha, const double* gamma,
              const double* scale, const double* mu, const double* kT, const ffg_model* md,
-             int mode_api, double* const* D_out, double* stats_out, ffg_provenance* prov) {
+             int mode_api, double* const* D_out, double* stats_out, ffg_provenance* prov,
+             int exact_layers = -1) {
     int rc, dev, mode;
     if ((rc = validate_host_call(B, H, n, md, mode_api, &mode, &dev))) return rc;
     cudaStream_t st = lib_stream();
+    if (!st) return FFG_ERR_CUDA;
     Workspace& w = *get_ws(dev, st);
     std::lock_guard<std::mutex> lk(w.mu);
     int si;
-    if ((rc = submit_host(w, st, B, H, n, alpha, gamma, scale, mu, kT, md, mode_api, mode, D_out, &si)))
+    if ((rc = submit_host(w, st, B, H, n, alpha, gamma, scale, mu, kT, md, mode_api, mode, D_out, &si, false,
+                          exact_layers)))
         return rc;
     return finish_host(w, si, stats_out, prov);
 }
@@ -1110,7 +1251,7 @@ void rescale_coeffs(int B, const double* mu, const double* kT, const ffg_model* 
 // status, flags.  D goes to w.Ds when want_D.
 int eval_single(Workspace& w, cudaStream_t st, int64_t n, double alpha, double gamma, double scale,
                 double mu, const ffg_model* md, int mode, bool want_D, double stats[2], double bounds[4],
-                int* status, int flags[2]) {
+                int* status, int flags[2], uint32_t* products = nullptr) {
     Job j;
     j.B = 1;
     j.n = n;
@@ -1129,13 +1270,30 @@ int eval_single(Workspace& w, cudaStream_t st, int64_t n, double alpha, double g
     CK(cudaMemcpyAsync(hs + 16, w.bounds_out, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hs + 48, w.status, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hs + 52, w.flags, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs + 60, w.products, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     memcpy(stats, hs, 16);
     memcpy(bounds, hs + 16, 32);
     memcpy(status, hs + 48, 4);
     memcpy(flags, hs + 52, 8);
+    if (products) memcpy(products, hs + 60, 4);
     return FFG_OK;
 }
+
+// Row-block session (ffg_rowblock_*): one rank's own workspace and job over the whole run.
+struct RowBlockState {
+    Workspace* w = nullptr;
+    int device = -1;
+    Job job;
+    EnqueueCtx cx;
+    std::vector<double> abcd;
+    ffg_model model{};
+    double alpha = 0, gamma = 0, scale = 0, mu = 0, kT = 0;
+    int mode_api = 0;
+    int64_t n = 0, np = 0;
+    int nb = 0, rank = 0, world = 1, r0 = 0, r1 = 0;
+    int next_layer = 0;
+};
 
 int status_error(int code, const double* b, const int* f) {
     if (code == FFG_ERR_OUT_OF_REGION)
@@ -1145,6 +1303,10 @@ int status_error(int code, const double* b, const int* f) {
 }
 
 }  // namespace
+
+struct ffg_rowblock {
+    RowBlockState s;
+};
 
 // ===================================================================== C ABI
 extern "C" {
@@ -1171,6 +1333,7 @@ int ffg_spectral_bounds(const double* H, int64_t n, double* eps_min, double* eps
     if (!H || !eps_min || !eps_max) return set_err(FFG_ERR_VALIDATION, "null argument");
     if ((rc = check_device(&dev))) return rc;
     cudaStream_t st = lib_stream();
+    if (!st) return FFG_ERR_CUDA;
     Workspace& w = *get_ws(dev, st);
     std::lock_guard<std::mutex> lk(w.mu);
     const size_t nn = (size_t)n * n;
@@ -1178,20 +1341,7 @@ int ffg_spectral_bounds(const double* H, int64_t n, double* eps_min, double* eps
     if ((rc = ensure(w, 1, 128, 1, false))) return rc;
     CK(cudaMemcpyAsync(w.Hs, H, nn * 8, cudaMemcpyHostToDevice, st));
     reset_kernel<<<1, 32, 0, st>>>(w.bounds, w.flags, 1);
-    RescaleParams rp{};
-    double* ag = w.params_host;
-    ag[0] = 1.0;
-    ag[1] = 0.0;
-    CK(cudaMemcpyAsync(w.params, ag, 16, cudaMemcpyHostToDevice, st));
-    rp.H = w.Hs;
-    rp.alpha = w.params;
-    rp.gamma = w.params + 1;
-    rp.bounds = w.bounds;
-    rp.flags = w.flags;
-    rp.n = (int)n;
-    rp.np = (int)((n + 7) / 8 * 8);
-    rp.write_operands = 0;
-    rescale_gershgorin_kernel<<<dim3((unsigned)(rp.np / 8), 1), 256, 0, st>>>(rp);
+    gershgorin_kernel<<<dim3((unsigned)((n + 7) / 8), 1), 256, 0, st>>>(w.Hs, (int)n, w.bounds);
     CK(cudaGetLastError());
     unsigned long long k[2];
     CK(cudaMemcpyAsync(k, w.bounds, 16, cudaMemcpyDeviceToHost, st));
@@ -1211,22 +1361,43 @@ int ffg_apply_model(const double* H0, int64_t n, const ffg_model* model, int32_t
                     nullptr, prov);
 }
 
+// X0 = half(X), X1 = half(X - X0), Y = X0 X0 + X0 X1 + (X0 X1)^T accumulated in
+// single precision, over the whole binary16 range.  The kernels split x * 2^14; a call picks the
+// power of two 2^e that puts max|X| just below 65504 (e <= 40: small inputs keep their lo parts out
+// of the binary16 subnormals) and feeds X * 2^(e-14), then scales Y back by 2^(28-2e) -- exact
+// power-of-two scalings, so the split is that of X at scale 2^e.  One layer of the identity model
+// (a=1, b=c=d=0) on the floating split (no fixed-point exact layer): the three upper-triangle
+// products hi*hi + hi*lo + lo*hi of Eq. 48, i.e. 1.5 full-GEMM equivalents against SPEC's "2 half
+// multiplications".  |X| beyond the binary16 range -> FFG_ERR_HALF_RANGE (overflow error).
 int ffg_mixed_square(const float* X, int64_t n, float* Y_out) {
     int rc;
     if ((rc = validate_n(n))) return rc;
     if (!X || !Y_out) return set_err(FFG_ERR_VALIDATION, "null argument");
     const size_t nn = (size_t)n * n;
+    float amax = 0.0f;
+    for (size_t e = 0; e < nn; ++e) {
+        if (!std::isfinite(X[e])) return set_err(FFG_ERR_VALIDATION, "mixed_square: non-finite entry %zu", e);
+        amax = std::max(amax, std::fabs(X[e]));
+    }
+    if (!(amax < 65504.0f))
+        return set_err(FFG_ERR_HALF_RANGE, "mixed_square: max|X| = %.9g exceeds the binary16 range (65504)",
+                       (double)amax);
+    int e = 40;
+    if (amax > 0.0f) {
+        e = std::min(40, (int)std::floor(std::log2(65504.0 / (double)amax)));
+        while (e > -30 && !((double)amax * std::ldexp(1.0, e) < 65504.0)) --e;
+    }
     std::vector<double> Xd(nn), Yd(nn);
-    for (size_t e = 0; e < nn; ++e) Xd[e] = X[e];
+    for (size_t k = 0; k < nn; ++k) Xd[k] = (double)std::ldexp(X[k], e - 14);  // exact in fp32 and fp64
     const double abcd[4] = {1.0, 0.0, 0.0, 0.0};
     ffg_model m{abcd, 1, 1.0, 0.5};
     const double alpha = 1.0, gamma = 0.0;
     const double* Hp[1] = {Xd.data()};
     double* Dp[1] = {Yd.data()};
-    rc = run_host(1, Hp, n, &alpha, &gamma, nullptr, nullptr, nullptr, &m,
-                  FFG_MODE_MIXED_EMULATED, Dp, nullptr, nullptr);
+    rc = run_host(1, Hp, n, &alpha, &gamma, nullptr, nullptr, nullptr, &m, FFG_MODE_MIXED_EMULATED, Dp, nullptr,
+                  nullptr, /*exact_layers=*/0);
     if (rc) return rc;
-    for (size_t e = 0; e < nn; ++e) Y_out[e] = (float)Yd[e];
+    for (size_t k = 0; k < nn; ++k) Y_out[k] = (float)std::ldexp(Yd[k], 28 - 2 * e);
     return FFG_OK;
 }
 
@@ -1236,6 +1407,7 @@ int ffg_expectation(const double* D, const double* A, int64_t n, double* out) {
     if (!D || !A || !out) return set_err(FFG_ERR_VALIDATION, "null argument");
     if ((rc = check_device(&dev))) return rc;
     cudaStream_t st = lib_stream();
+    if (!st) return FFG_ERR_CUDA;
     Workspace& w = *get_ws(dev, st);
     std::lock_guard<std::mutex> lk(w.mu);
     const size_t nn = (size_t)n * n;
@@ -1247,7 +1419,7 @@ int ffg_expectation(const double* D, const double* A, int64_t n, double* out) {
     reset_kernel<<<1, 32, 0, st>>>(w.bounds, w.flags, 1);
     FinalizeParams fp{};
     fp.partials = w.partials;
-    fp.bounds = w.bounds;
+    fp.region = RegionCheck{w.bounds, nullptr, nullptr, 0.0};
     fp.flags = w.flags;
     fp.T = (int)n;
     fp.B = 1;
@@ -1276,6 +1448,7 @@ int ffg_entropy_trace(const double* H, int64_t n, double mu, double kT, const ff
     if (!H || !entropy_trace) return set_err(FFG_ERR_VALIDATION, "null argument");
     if ((rc = check_device(&dev))) return rc;
     cudaStream_t st = lib_stream();
+    if (!st) return FFG_ERR_CUDA;
     Workspace& w = *get_ws(dev, st);
     std::lock_guard<std::mutex> lk(w.mu);
     const size_t nn = (size_t)n * n;
@@ -1286,9 +1459,11 @@ int ffg_entropy_trace(const double* H, int64_t n, double mu, double kT, const ff
     const double a = em->alpha * s, g = em->inner.mu0 - em->alpha * s * mu;
     double stats[2], bounds[4];
     int status, flags[2];
-    if ((rc = eval_single(w, st, n, a, g, s, mu, &em->inner, mode, false, stats, bounds, &status, flags)))
+    uint32_t products = 0;
+    if ((rc = eval_single(w, st, n, a, g, s, mu, &em->inner, mode, false, stats, bounds, &status, flags,
+                          &products)))
         return rc;
-    if (prov) fill_prov(prov, bounds, &kT, mu, status, flags, &em->inner, mode_api, (int)n, 0.0);
+    if (prov) fill_prov(prov, bounds, &kT, mu, status, flags, &em->inner, mode_api, (int)n, 0.0, products, w.PT);
     if (status != FFG_OK) return status_error(status, bounds, flags);
     *entropy_trace = 4.0 * std::log(2.0) * (stats[0] - stats[1]);
     return FFG_OK;
@@ -1309,6 +1484,7 @@ int ffg_solve_chemical_potential(const double* H, int64_t n, double kT, double n
     if (!(tol > 0.0) || max_iter < 1) return set_err(FFG_ERR_VALIDATION, "tol > 0 and max_iter >= 1 required");
     if ((rc = check_device(&dev))) return rc;
     cudaStream_t st = lib_stream();
+    if (!st) return FFG_ERR_CUDA;
     Workspace& w = *get_ws(dev, st);
     std::lock_guard<std::mutex> lk(w.mu);
     const size_t nn = (size_t)n * n;
@@ -1396,6 +1572,7 @@ int ffg_density_statistics(const double* D, int64_t n, double* stats_out) {
     if (!D || !stats_out) return set_err(FFG_ERR_VALIDATION, "null argument");
     if ((rc = check_device(&dev))) return rc;
     cudaStream_t st = lib_stream();
+    if (!st) return FFG_ERR_CUDA;
     Workspace& w = *get_ws(dev, st);
     std::lock_guard<std::mutex> lk(w.mu);
     const size_t nn = (size_t)n * n;
@@ -1406,10 +1583,8 @@ int ffg_density_statistics(const double* D, int64_t n, double* stats_out) {
     reset_kernel<<<1, 32, 0, st>>>(w.bounds, w.flags, 1);
     FinalizeParams fp{};
     fp.partials = w.partials;
-    fp.bounds = w.bounds;
+    fp.region = RegionCheck{w.bounds, nullptr, nullptr, 0.0};
     fp.flags = w.flags;
-    fp.scale = nullptr;
-    fp.mu = nullptr;
     fp.T = (int)n;
     fp.B = 1;
     fp.stats = w.stats;
@@ -1452,6 +1627,7 @@ int ffg_density_matrices_async(int32_t batch, const double* const* H, int64_t n,
     std::vector<double> alpha, gamma, scale;
     rescale_coeffs(batch, mu, kT, model, alpha, gamma, scale);
     cudaStream_t st = lib_stream();
+    if (!st) return FFG_ERR_CUDA;
     Workspace& w = *get_ws(dev, st);
     std::lock_guard<std::mutex> lk(w.mu);
     int si;
@@ -1466,6 +1642,7 @@ int ffg_wait(int64_t ticket, double* stats_out, ffg_provenance* prov) {
     int rc, dev;
     if ((rc = check_device(&dev))) return rc;
     cudaStream_t st = lib_stream();
+    if (!st) return FFG_ERR_CUDA;
     Workspace& w = *get_ws(dev, st);
     std::lock_guard<std::mutex> lk(w.mu);
     for (int k = 0; k < Workspace::kSlots; ++k)
@@ -1512,8 +1689,7 @@ int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, in
     (void)n;
     (void)mode;
     if (!model) return 0;
-    return 4;                                // reset + K1 + K2 (all layers) + K3
-    return 3 + (int64_t)model->n_layers;    // reset + K1 + L x K2 + K3
+    return 4;  // reset + K1 + K2 (all layers, one persistent launch) + K3
 }
 
 int ffg_profile_layers(int enable) {
@@ -1558,6 +1734,155 @@ int64_t ffg_debug_watchdog(uint64_t* out6) {
     if (!g_watch_host) return 0;
     for (int i = 0; i < 6; ++i) out6[i] = g_watch_host[i];
     return (int64_t)g_watch_host[0];
+}
+
+int32_t ffg_rowblock_table(int32_t nb, int32_t rank, int32_t world, uint32_t* out, int32_t capacity) {
+    if (nb < 1 || nb > 1023 || world < 1 || rank < 0 || rank >= world || nb % world) return -1;
+    int r0, r1;
+    rowblock_rows(nb, rank, world, &r0, &r1);
+    const std::vector<uint32_t> t = rowblock_table(nb, r0, r1);
+    if (out)
+        for (int32_t i = 0; i < (int32_t)t.size() && i < capacity; ++i) out[i] = t[i];
+    return (int32_t)t.size();
+}
+
+int ffg_rowblock_begin(const double* H_dev, int64_t n, double mu, double kT, const ffg_model* model,
+                       int32_t mode_api, int32_t rank, int32_t world, void* stream, ffg_rowblock** handle) {
+    int rc, dev, mode;
+    if (!H_dev || !handle) return set_err(FFG_ERR_VALIDATION, "H_dev / handle is null");
+    *handle = nullptr;
+    if ((rc = validate_model(model))) return rc;
+    if ((rc = mode_to_internal(mode_api, &mode))) return rc;
+    if ((rc = validate_n(n))) return rc;
+    if ((rc = check_mu_kT(1, &mu, &kT))) return rc;
+    if (world < 1 || rank < 0 || rank >= world)
+        return set_err(FFG_ERR_VALIDATION, "row-block rank %d of world %d", rank, world);
+    const int nb = (int)((n + kBM - 1) / kBM);
+    if (nb % world)
+        return set_err(FFG_ERR_DIMENSION, "row-block sharding needs the %d blocks of 128 rows to divide evenly "
+                       "over %d ranks (n = %lld)", nb, world, (long long)n);
+    if ((rc = check_device(&dev))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ffg_rowblock* h = new ffg_rowblock();
+    RowBlockState& S = h->s;
+    S.w = new Workspace();
+    S.w->device = dev;
+    S.device = dev;
+    S.abcd.assign(model->abcd, model->abcd + 4 * model->n_layers);
+    S.model = *model;
+    S.model.abcd = S.abcd.data();
+    S.kT = kT;
+    S.mu = mu;
+    S.scale = (1.0 / kT) / model->beta0;
+    S.alpha = -S.scale;
+    S.gamma = (1.0 - model->mu0) + S.scale * mu;
+    S.mode_api = mode_api;
+    S.n = n;
+    S.nb = nb;
+    S.np = (int64_t)nb * kBM;
+    S.rank = rank;
+    S.world = world;
+    rowblock_rows(nb, rank, world, &S.r0, &S.r1);
+    Job& j = S.job;
+    j.B = 1;
+    j.n = n;
+    j.H_dev = H_dev;
+    j.alpha = &S.alpha;
+    j.gamma = &S.gamma;
+    j.scale = &S.scale;
+    j.mu = &S.mu;
+    j.model = &S.model;
+    j.mode = mode;
+    j.rb_world = world;
+    j.rb_rank = rank;
+    if ((rc = enqueue_k1(*S.w, j, st, S.cx))) {
+        free_ws(S.w);
+        delete S.w;
+        delete h;
+        return rc;
+    }
+    *handle = h;
+    return FFG_OK;
+}
+
+int ffg_rowblock_rows(const ffg_rowblock* h, int64_t* row0, int64_t* rows, int64_t* np) {
+    if (!h) return set_err(FFG_ERR_VALIDATION, "null handle");
+    const RowBlockState& S = h->s;
+    if (row0) *row0 = (int64_t)S.r0 * kBM;
+    if (rows) *rows = (int64_t)(S.r1 - S.r0) * kBM;
+    if (np) *np = S.np;
+    return FFG_OK;
+}
+
+int ffg_rowblock_operands(ffg_rowblock* h, int32_t parity, void** hi, void** lo) {
+    if (!h || parity < 0 || parity > 1) return set_err(FFG_ERR_VALIDATION, "bad handle / parity");
+    RowBlockState& S = h->s;
+    if (hi) *hi = S.w->op[2 * parity];
+    if (lo) *lo = S.job.mode == kModeF32E ? S.w->op[2 * parity + 1] : nullptr;
+    return FFG_OK;
+}
+
+int ffg_rowblock_layer(ffg_rowblock* h, int32_t layer, double* D_rows, void* stream) {
+    if (!h) return set_err(FFG_ERR_VALIDATION, "null handle");
+    RowBlockState& S = h->s;
+    if (layer != S.next_layer || layer >= S.model.n_layers)
+        return set_err(FFG_ERR_VALIDATION, "row-block layer %d out of order (next %d of %d)", layer, S.next_layer,
+                       S.model.n_layers);
+    int cur = -1;
+    CK(cudaGetDevice(&cur));
+    if (cur != S.device) return set_err(FFG_ERR_VALIDATION, "row-block handle belongs to device %d", S.device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool last = layer + 1 == S.model.n_layers;
+    S.job.D_dev = last ? D_rows : nullptr;
+    int rc;
+    if ((rc = enqueue_k2(*S.w, S.job, st, S.cx, layer, layer + 1))) return rc;
+    if (last) {
+        const int64_t d_rows = std::min<int64_t>((int64_t)S.r1 * kBM, S.n) - (int64_t)S.r0 * kBM;
+        if ((rc = enqueue_k3(*S.w, S.job, st, S.cx, std::max<int64_t>(d_rows, 0)))) return rc;
+    }
+    ++S.next_layer;
+    return FFG_OK;
+}
+
+int ffg_rowblock_end(ffg_rowblock* h, double* partial_stats, int32_t* status, ffg_provenance* prov,
+                     void* stream) {
+    if (!h) return set_err(FFG_ERR_VALIDATION, "null handle");
+    RowBlockState& S = h->s;
+    Workspace& w = *S.w;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc = FFG_OK;
+    if (S.next_layer != S.model.n_layers) {
+        rc = set_err(FFG_ERR_VALIDATION, "row-block ended after %d of %d layers", S.next_layer, S.model.n_layers);
+    } else {
+        double stats[2], bounds[4];
+        int st_code = 0, flags[2];
+        uint32_t products = 0;
+        cudaError_t e = cudaSuccess;
+        e = e ? e : cudaMemcpyAsync(stats, w.stats, 16, cudaMemcpyDeviceToHost, st);
+        e = e ? e : cudaMemcpyAsync(bounds, w.bounds_out, 32, cudaMemcpyDeviceToHost, st);
+        e = e ? e : cudaMemcpyAsync(&st_code, w.status, 4, cudaMemcpyDeviceToHost, st);
+        e = e ? e : cudaMemcpyAsync(flags, w.flags, 8, cudaMemcpyDeviceToHost, st);
+        e = e ? e : cudaMemcpyAsync(&products, w.products, 4, cudaMemcpyDeviceToHost, st);
+        e = e ? e : cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            rc = set_err(FFG_ERR_CUDA, "row-block readback: %s", cudaGetErrorString(e));
+        } else {
+            if (partial_stats) {
+                partial_stats[0] = stats[0];
+                partial_stats[1] = stats[1];
+            }
+            if (status) *status = st_code;
+            if (prov)
+                fill_prov(prov, bounds, &S.kT, S.mu, st_code, flags, &S.model, S.mode_api, (int)S.n, 0.0, products,
+                          w.PT);
+            if (st_code != FFG_OK) rc = status_error(st_code, bounds, flags);
+        }
+    }
+    cudaStreamSynchronize(st);
+    free_ws(S.w);
+    delete S.w;
+    delete h;
+    return rc;
 }
 
 int32_t ffg_pair_table(int32_t nb, uint32_t* out, int32_t capacity) {

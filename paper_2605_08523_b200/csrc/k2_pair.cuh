@@ -28,8 +28,13 @@
 //   warps 12-19   epilogue (epilogue.cuh): X' = aY + bX + cI, A += d'X' (L2 reductions, paired
 //                 over two layers), binary16 split, direct + mirrored 32x32 pieces by TMA store;
 //                 last layer: D = A + X_L and the per-block statistics.
-// Variants (template V): 1 resident (one block per CTA for all layers), 2 sixteen workers that
-// drain and finish one 32-column piece each (np <= 512).
+// Variants (template V): 0 the above, 2 sixteen workers that drain and finish one 32-column
+// piece each (latency-bound layers; ffg_capi.cu use_s16).
+// Matrices outside the model's region of validity (K1's Gershgorin bounds, the K3 formula
+// matrix_in_region) never enter the item space: the prologue compacts the launch's matrices to
+// the valid ones (MatrixMap) and the items walk only those -- no loads, no MMAs, no epilogue for an
+// out-of-region matrix (K3 then writes its D as NaN).  The MMA issuer counts the products it issues
+// per matrix (p.products).
 // Accumulation precision: in the first `exact_layers` layers hi is a fixed-point split
 // and hi*hi accumulates EXACTLY over the whole K in its own TMEM accumulator (cross terms and
 // lo*lo in a second); later layers drain every two K-blocks into round-to-nearest registers.
@@ -54,10 +59,10 @@ constexpr int kPRegsCtl = 48, kPRegsDrain = 104, kPRegsEpi = 112;
 constexpr int kPRegsCtl = 48, kPRegsDrain = 96, kPRegsEpi = 120;
 #endif
 static_assert(128 * kPRegsCtl + 256 * kPRegsDrain + 256 * kPRegsEpi <= 640 * 96, "setmaxnreg budget");
-// resident and 16-worker variants: 16 worker warps (drain + epilogue) own 32 columns each of the CTA's block
+// 16-worker variant: 16 worker warps (drain + epilogue) own 32 columns each of the CTA's block
 constexpr int kResWorkers = 16;
 constexpr int kRRegsCtl = 40, kRRegsWork = 104;
-static_assert(128 * kRRegsCtl + 512 * kRRegsWork <= 640 * 96, "setmaxnreg budget (resident)");
+static_assert(128 * kRRegsCtl + 512 * kRRegsWork <= 640 * 96, "setmaxnreg budget (16 workers)");
 constexpr int kPairHalf = kBN / 2;                  // B rows supplied by each CTA
 constexpr int kPairOpA = kBM * kBK * 2;             // 16 KB
 constexpr int kPairOpB = kPairHalf * kBK * 2;       // 8 KB
@@ -68,6 +73,9 @@ constexpr int kPairStagingBytes = kEpiWarps2 * 4 * kPieceBytes;
 #ifndef FFG_NARROW_STAGING
 #define FFG_NARROW_STAGING 1  // streaming FP32E: two staging pieces per epilogue warp (mirrors in place), 4 stages
 #endif
+// Validity bitmap of a launch's matrices (at most kValidBits per launch; the host splits larger
+// batches) in shared memory, filled in the prologue
+constexpr int kValidBits = 8192;
 // NARROW (streaming kernel, FP32E, FFG_NARROW_STAGING): 32 KB of staging buys a fourth operand stage
 template <int MODE, bool NARROW = false>
 struct PairCfg {
@@ -77,7 +85,8 @@ struct PairCfg {
     static constexpr int kStages = (ModeTraits<MODE>::kHasLo ? 3 : 6) + (NARROW ? 1 : 0);
     static constexpr int kStagingOff = kStages * kStageBytes;
     static constexpr int kBarOff = kStagingOff + kStagingBytes;
-    static constexpr int kSmem = kBarOff + 1024 + 1024;  // barriers/scratch + alignment slack
+    static constexpr int kValidOff = kBarOff + 1024;           // validity bitmap (kValidBits matrices)
+    static constexpr int kSmem = kValidOff + kValidBits / 8 + 1024;  // + alignment slack
 };
 static_assert(PairCfg<kModeF32E>::kSmem <= 227 * 1024, "pair kernel smem");
 static_assert(PairCfg<kModeBF16>::kSmem <= 227 * 1024, "pair kernel smem");
@@ -119,6 +128,9 @@ static_assert(kEpiWarps == kEpiWarps2, "slot_empty counts drain and epilogue war
 #ifndef FFG_EXACT_K16
 #define FFG_EXACT_K16 1  // K16 steps per chunk in exact-drain layers (1 or 2)
 #endif
+#ifndef FFG_SEMI_DRAIN
+#define FFG_SEMI_DRAIN 0  // compile the drain-every-2-K16 layers (FFG_SEMI_DRAIN_LAYERS, measurement)
+#endif
 __host__ __device__ constexpr int pair_chunks(int mode, int nk, bool exact) {
     return mode == kModeF32E ? (exact ? nk * (kBK / kUK) / FFG_EXACT_K16 : nk) : 1;
 }
@@ -159,6 +171,7 @@ struct PairParams {
     int B, G;                 // matrices, group size
     int l0, l1, n_layers;     // layers of this launch, model depth
     int exact_layers;
+    int sr_layers;            // layers whose fixed-point split rounds lo stochastically (kernels.cuh)
     int semi_layers;          // layers after the exact ones draining every 2 K16 steps
     int normal_kstep;         // K16 steps per chunk in the remaining layers (4: one K-block, 8: two)
     int dbg;                  // measurement only: 1 skip epilogue math, 2 skip loads/MMAs,
@@ -166,281 +179,54 @@ struct PairParams {
                               // 16 skip operand loads, 32 skip hi/lo stores, 64 skip X/A
                               // stores (A: reductions), 128 skip X loads (all measurement only: results are wrong)
     unsigned long long* prof; // [gridDim][16] (dbg & 8)
-    int m0;                   // first matrix of this launch (resident groups)
-    uint16_t* hi[2];          // hi/lo parity buffers [B][np][np] (resident epilogue stores)
-    uint16_t* lo[2];
+    int m0;                   // first matrix of this launch
     uint32_t zero;            // always 0: an opaque operand for scheduling dependencies (drain)
+    uint32_t* products;       // [B] tensor-core product passes issued per matrix (instrumented count)
+    RegionCheck region;       // validity of each matrix from K1's bounds (kernels.cuh)
+    int rowblock;             // row-block table (a rank's block rows x all columns): no mirrored
+                              // hi/lo pieces or D entries off the diagonal blocks, each element counted once
+    int drow0;                // row-block: first global row of D's row slab (D indexed (gi - drow0) * n + gj)
 };
 
-__device__ __forceinline__ void pair_decode(const PairParams& p, int item, int& m, int& l, int& pi) {
+// The launch's matrices that are inside the region of validity: nvalid of the B, bit m of `valid`
+// set for matrix m0 + m.  All valid (the normal case): item matrix index = position.  Otherwise
+// position -> the position-th set bit (every role computes the same map).
+struct MatrixMap {
+    const uint32_t* valid;
+    int nvalid;
+    bool remap;
+    __device__ __forceinline__ int matrix(int pos) const {
+        if (!remap) return pos;
+        int w = 0;
+        for (;; ++w) {
+            const int c = __popc(valid[w]);
+            if (pos < c) break;
+            pos -= c;
+        }
+        uint32_t bits = valid[w];
+        for (int k = 0; k < pos; ++k) bits &= bits - 1;  // drop the lowest set bits
+        return 32 * w + (__ffs(bits) - 1);
+    }
+};
+
+__device__ __forceinline__ void pair_decode(const PairParams& p, const MatrixMap& mm, int item, int& m, int& l,
+                                            int& pi) {
     const int L = p.l1 - p.l0;
     const int per_group = L * p.G * p.PT;
     const int g = item / per_group;
     const int base = g * p.G;
-    const int Gg = min(p.G, p.B - base);
+    const int Gg = min(p.G, mm.nvalid - base);
     int r = item - g * per_group;
     const int per_layer = Gg * p.PT;
     const int dl = r / per_layer;
     r -= dl * per_layer;
     const int mi = r / p.PT;
     pi = r - mi * p.PT;
-    m = p.m0 + base + mi;
+    m = p.m0 + mm.matrix(base + mi);
     l = p.l0 + dl;
 }
 
 
-__device__ __forceinline__ void stg_v4(uint16_t* gp, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    *reinterpret_cast<uint4*>(gp) = make_uint4(a, b, c, d);
-}
-__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(addr) : "memory");
-    return v;
-}
-
-// Resident K2 workers (RES): warps 4-19 of each CTA own its block (R, C) of one matrix for
-// the whole recursion.  Warp w: TMEM lane quarter q = w & 3 (rows 32q..32q+31), column quarter
-// c = (w - 4) >> 2 (32 columns); thread = one row.  X_l lives in TMEM slot 3, A_l and the
-// per-layer Y in registers; per layer the only global traffic is the hi/lo pieces of X_{l+1}
-// (direct row segments straight from registers, the mirrored piece through an in-place
-// ldmatrix.trans / stmatrix transpose in a 2 KB per-warp staging piece).
-template <int MODE>
-__device__ __forceinline__ void resident_workers(const PairParams& p, uint32_t tmem, int warp, int lane,
-                                                 uint32_t rank, int pair_id, int n_pairs, int total,
-                                                 int nk, uint64_t* slot_full, uint64_t* slot_empty,
-                                                 uint8_t* staging, double* red) {
-    using Tr = ModeTraits<MODE>;
-    const int q = warp & 3, c = (warp - 4) >> 2, wk = warp - 4;
-    const int r = q * 32 + lane;
-    const int nb = p.nb, n = p.n, np = p.np;
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + 32 * c;  // + slot * 128
-    const uint32_t tX = tl + 3 * 128;
-    const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
-    const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
-    const uint32_t stg = smem_u32(staging) + wk * 2 * kPieceBytes;  // hi piece, lo piece
-    int m, l_first, pi;
-    pair_decode(p, pair_id, m, l_first, pi);
-    const uint32_t pr = __ldg(p.pairs + pi);
-    const int R = rank ? (pr >> 10) & 1023 : pr & 1023;
-    const int C = (pr >> 20) & 1023;
-    const bool dummy = rank && ((pr >> 30) & 1);
-    const bool diag = R == C;
-    const bool skip = dummy || (diag && c < q);  // lower half of a diagonal block: mirrored
-    const bool dblk = diag && c == q;            // this warp's 32x32 piece is on the diagonal
-    const int gi = R * kBM + r;
-    const bool c_on = gi < n;
-    float areg[32];
-    // X_0 -> TMEM slot 3, A_1 -> registers (K1 wrote both in the tile-interleaved layout)
-    if (!skip) {
-        const float* Xt = p.X + xa_tile_base(m, R, C, nb);
-        const float* At = p.A + xa_tile_base(m, R, C, nb);
-        uint32_t xv[32];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float4 x = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, 8 * c + j)));
-            const float4 a = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, 8 * c + j)));
-            xv[4 * j + 0] = __float_as_uint(x.x); xv[4 * j + 1] = __float_as_uint(x.y);
-            xv[4 * j + 2] = __float_as_uint(x.z); xv[4 * j + 3] = __float_as_uint(x.w);
-            areg[4 * j + 0] = a.x; areg[4 * j + 1] = a.y; areg[4 * j + 2] = a.z; areg[4 * j + 3] = a.w;
-        }
-        tmem_st_32x32b_x32(tX, xv);
-        tmem_st_wait();
-    } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) areg[e] = 0.0f;
-    }
-    int g = 0;
-    for (int item = pair_id; item < total; item += n_pairs) {
-        const int l = l_first + (item - pair_id) / n_pairs;
-        const bool last = (l == p.n_layers - 1);
-        const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
-        int ysl = 0;
-        {
-            float yacc[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) yacc[e] = 0.0f;
-#pragma unroll 1
-            for (int f = 0; f < chunks; ++f, ++g) {
-                const int sl = g % 3;
-                mbar_wait_sleep(&slot_full[sl], (g / 3) & 1);
-                tc_fence_after();
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tl + sl * 128, v);
-                tmem_ld_wait();
-                const bool lastc = f == chunks - 1;
-                if (!lastc) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);
-                }
-#pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    const float2 acc = add_f32x2(make_float2(yacc[e], yacc[e + 1]),
-                                                 make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
-                    yacc[e] = acc.x;
-                    yacc[e + 1] = acc.y;
-                }
-                if (lastc) {  // Y of the layer into this slot; the epilogue below frees it
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(yacc[e] * inv_s2);
-                    tmem_st_32x32b_x32(tl + sl * 128, v);
-                    tmem_st_wait();
-                    ysl = sl;
-                }
-            }
-        }
-        // ------------------------------------------------------------- epilogue of layer l
-        EpiCoef k = load_coef(p.coef, l, p.n_layers, p.a_pair != 0);
-        k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
-        EpiHealth hl;
-        double tr = 0.0, sq = 0.0;
-        const bool work = !skip && !(p.dbg & 1);
-        const int nxt = (l + 1) & 1;
-        uint16_t* const hbase = p.hi[nxt] + (size_t)m * np * np;
-        uint16_t* const lbase = p.lo[nxt] + (size_t)m * np * np;
-        double* Dm = (last && p.D) ? p.D + (size_t)m * n * n : nullptr;
-#pragma unroll
-        for (int h = 0; h < 2 && work; ++h) {
-            uint32_t yv[16], xv[16];
-            tmem_ld_32x32b_x16(tl + ysl * 128 + 16 * h, yv);
-            tmem_ld_32x32b_x16(tX + 16 * h, xv);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const int cl = 32 * c + 16 * h + e;
-                const float y = __uint_as_float(yv[e]);
-                const float x = __uint_as_float(xv[e]);
-                const bool dg = diag && cl == r;
-                const float xn = (dg && c_on) ? poly_step<true>(y, x, k) : poly_step<false>(y, x, k);
-                const bool own = !dblk || cl >= r;
-                if (own) hl.add(xn);
-                if (!last) {
-                    areg[16 * h + e] = acc_step(areg[16 * h + e], xn, k);
-                    xv[e] = __float_as_uint(xn);
-                } else {
-                    const int gj = C * kBN + cl;
-                    if (own && gi < n && gj < n) {
-                        const double dv = (double)areg[16 * h + e] + (double)xn;
-                        if (Dm) {
-                            Dm[(size_t)gi * n + gj] = dv;
-                            if (!dg) Dm[(size_t)gj * n + gi] = dv;
-                        }
-                        if (dg) {
-                            tr += dv;
-                            sq += dv * dv;
-                        } else {
-                            sq += 2.0 * dv * dv;
-                        }
-                    }
-                }
-            }
-            if (!last) {
-                tmem_st_32x32b_x16(tX + 16 * h, xv);
-                uint32_t hp[8], lp[8];
-#pragma unroll
-                for (int e = 0; e < 16; e += 2)
-                    split2<MODE>(__uint_as_float(xv[e]), __uint_as_float(xv[e + 1]), hp[e >> 1], lp[e >> 1], k.fixed);
-                // row segment into the staging pieces (hi at +0, lo at +2 KB; row = lane)
-                sts_v4(stg + sw64(lane, 2 * h + 0), hp[0], hp[1], hp[2], hp[3]);
-                sts_v4(stg + sw64(lane, 2 * h + 1), hp[4], hp[5], hp[6], hp[7]);
-                if (Tr::kHasLo) {
-                    sts_v4(stg + kPieceBytes + sw64(lane, 2 * h + 0), lp[0], lp[1], lp[2], lp[3]);
-                    sts_v4(stg + kPieceBytes + sw64(lane, 2 * h + 1), lp[4], lp[5], lp[6], lp[7]);
-                }
-                tmem_st_wait();
-            }
-        }
-        // Y slot read by this warp: release it (every warp arrives, working or not)
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * ysl);
-        if (!last && work) {
-            __syncwarp();
-#pragma unroll
-            for (int hl2 = 0; hl2 < (Tr::kHasLo ? 2 : 1); ++hl2) {
-                const uint32_t pc = stg + hl2 * kPieceBytes;
-                uint16_t* base = hl2 ? lbase : hbase;
-                if (!dblk) {
-                    // direct: row gi, columns C*128 + 32c .. +31 (64 contiguous bytes)
-                    uint16_t* gd = base + (size_t)gi * np + C * kBN + 32 * c;
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
-                        const uint4 t = lds_v4(pc + sw64(lane, ch));
-                        stg_v4(gd + 8 * ch, t.x, t.y, t.z, t.w);
-                    }
-                    __syncwarp();
-                    transpose_piece_inplace(pc, lane);
-                    __syncwarp();
-                    // mirrored: rows C*128 + 32c + lane, columns R*128 + 32q .. +31
-                    uint16_t* gm = base + (size_t)(C * kBN + 32 * c + lane) * np + R * kBM + 32 * q;
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
-                        const uint4 t = lds_v4(pc + sw64(lane, ch));
-                        stg_v4(gm + 8 * ch, t.x, t.y, t.z, t.w);
-                    }
-                } else {
-                    // diagonal piece: owned (col >= row) values mirrored into the lower triangle
-                    uint16_t own16[32];
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
-                        const uint4 t = lds_v4(pc + sw64(lane, ch));
-                        const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) own16[8 * ch + e] = (uint16_t)(w4[e >> 1] >> (16 * (e & 1)));
-                    }
-                    __syncwarp();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (e > lane) sts_u16(pc + sw64(e, lane >> 3) + (lane & 7) * 2, own16[e]);
-                    __syncwarp();
-                    uint16_t* gd = base + (size_t)gi * np + C * kBN + 32 * c;
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) {
-                        const uint4 t = lds_v4(pc + sw64(lane, ch));
-                        stg_v4(gd + 8 * ch, t.x, t.y, t.z, t.w);
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        if (!dummy) {
-            const bool any_nf = __any_sync(0xffffffffu, hl.nonfinite());
-            const bool any_hr = !last && __any_sync(0xffffffffu, hl.template half_range<MODE>());
-            if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], l + 1);
-            if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], l + 1);
-        }
-        if (last) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                tr += __shfl_xor_sync(0xffffffffu, tr, o);
-                sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            }
-            if (lane == 0) {
-                red[2 * wk + 0] = tr;
-                red[2 * wk + 1] = sq;
-            }
-            named_bar_sync(3, kResWorkers * 32);
-            if (wk == 0 && lane == 0) {
-                double T0 = 0.0, T1 = 0.0;
-                for (int w2 = 0; w2 < kResWorkers; ++w2) {  // fixed order
-                    T0 += red[2 * w2 + 0];
-                    T1 += red[2 * w2 + 1];
-                }
-                p.partials[(size_t)m * 2 * p.PT + 2 * pi + rank] = make_double2(T0, T1);
-            }
-        } else if (!dummy && l + 1 < p.l1) {
-            // publish the block: every worker's hi/lo stores -> (bar) -> release the counters
-            named_bar_sync(4, kResWorkers * 32);
-            if (wk == 0 && lane == 0) {
-                __threadfence();
-                uint32_t* cm = p.counters + (size_t)m * nb;
-                red_release_gpu_add(cm + R, 1u);
-                if (C != R) red_release_gpu_add(cm + C, 1u);
-            }
-        }
-    }
-}
 
 // Streaming 16-worker epilogue (kernel variant V = 2): warps 4-19 all work on every item.  Warp w:
 // TMEM lane quarter q = w & 3 (rows 32q..32q+31), column quarter c = (w - 4) >> 2 (32 columns).
@@ -452,7 +238,7 @@ template <int MODE>
 __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairParams& p, uint32_t tmem,
                                                  int warp, int lane, uint32_t rank, int pair_id, int n_pairs,
                                                  int total, int nk, uint64_t* slot_full, uint64_t* slot_empty,
-                                                 uint8_t* staging, double* red) {
+                                                 uint8_t* staging, double* red, const MatrixMap& mm) {
     using Tr = ModeTraits<MODE>;
     const int wk = warp - 4, q = warp & 3, c = wk >> 2;
     const int r = q * 32 + lane;
@@ -465,7 +251,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
     int g = 0;
     for (int item = pair_id; item < total; item += n_pairs) {
         int m, l, pi;
-        pair_decode(p, item, m, l, pi);
+        pair_decode(p, mm, item, m, l, pi);
         const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
         float yacc[32];
 #pragma unroll
@@ -499,10 +285,12 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
         const bool diag = R == C;
         const bool skip = dummy || (p.dbg & 1) || (diag && c < q);
         const bool dblk = diag && c == q;
+        const bool mir = !p.rowblock || diag;  // row-block: no mirror of an off-diagonal block
         const int gi = R * kBM + r;
         const bool c_on = gi < n;
         EpiCoef k = load_coef(p.coef, l, p.n_layers, p.a_pair != 0);
         k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
+        k.sr = k.fixed && l + 1 < p.sr_layers;
         const int nxt = (l + 1) & 1;
         float* Xt = p.X + xa_tile_base(m, R, C, nb);
         float* At = p.A + xa_tile_base(m, R, C, nb);
@@ -524,10 +312,10 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                     for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * sub + e] * inv_s2);
                     if (diag)
                         epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
-                                                    p.dbg & 64);
+                                                    gi, C * kBN, p.dbg & 64);
                     else
                         epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
-                                                     p.dbg & 64);
+                                                     gi, C * kBN, p.dbg & 64);
                     if (sub == 0) {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) xq[j] = xn[j];
@@ -543,7 +331,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                         if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
                         tma_store_commit();
                     }
-                    if (!dblk) {  // mirrored pieces: transpose in place once the direct stores read them
+                    if (!dblk && mir) {  // mirrored pieces: transpose in place once the direct stores read them
                         if (lane == 0) tma_store_wait_read();
                         __syncwarp();
                         transpose_piece_inplace(stg_a, lane);
@@ -560,7 +348,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                     }
                 }
             } else {
-                double* Dm = p.D ? p.D + (size_t)m * n * n : nullptr;
+                double* Dm = p.D ? p.D + (size_t)m * n * n - (ptrdiff_t)p.drow0 * n : nullptr;
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     const int c0 = 32 * c + 16 * sub;
@@ -570,7 +358,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                     if (diag)
                         epi_sub_last<true>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
                     else
-                        epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                        epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq, mir);
                 }
             }
         }
@@ -581,6 +369,8 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
             if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], l + 1);
         }
         if (last) {
+            // block statistics: one partial per 32x32 piece (index 4c + q), summed in piece order
+            // (the same fixed order as the 8-warp epilogue)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 tr += __shfl_xor_sync(0xffffffffu, tr, o);
@@ -621,10 +411,14 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
     if (lane == 0) tma_store_wait_all();
 }
 
-// dbg & 8: accumulate the cycles a role spends in a wait into a register counter
+// dbg & 8: accumulate the cycles a role spends in a wait into a register counter (measurement
+// builds only, -DFFG_ROLE_PROF=1: the counters cost registers in roles at the edge of their budget)
+#ifndef FFG_ROLE_PROF
+#define FFG_ROLE_PROF 0
+#endif
 #define FFG_TIMED(acc, stmt)                                     \
     do {                                                         \
-        if (p.dbg & 8) {                                         \
+        if (FFG_ROLE_PROF && (p.dbg & 8)) {                                         \
             const long long t_ = clock64();                      \
             stmt;                                                \
             acc += (unsigned long long)(clock64() - t_);         \
@@ -633,30 +427,23 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
         }                                                        \
     } while (0)
 
-// the drain warps run at the edge of their register budget: their wait timing (two registers
-// across the chunk loop) is compiled in only with FFG_ROLE_PROF
-#ifndef FFG_ROLE_PROF
-#define FFG_ROLE_PROF 0
-#endif
-#if FFG_ROLE_PROF
 #define FFG_TIMED_DRAIN(acc, stmt) FFG_TIMED(acc, stmt)
-#else
-#define FFG_TIMED_DRAIN(acc, stmt) stmt
-#endif
 
-// V: 0 streaming (drain + epilogue warps), 1 resident (RES), 2 streaming with 16 workers (S16)
+// V: 0 streaming (drain + epilogue warps), 2 streaming with 16 workers (S16)
 template <int MODE, int V = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     mlsp2_pair_kernel(const __grid_constant__ PairMaps tm, const __grid_constant__ PairParams p) {
-    constexpr bool RES = V == 1;
+    static_assert(V == 0 || V == 2, "K2 variants: 0 streaming, 2 sixteen workers");
     constexpr bool S16 = V == 2;
-    constexpr int kSlots = RES ? 3 : 4;  // TMEM chunk ring (resident: slot 3 holds the X block)
+    constexpr int kSlots = 4;  // TMEM chunk ring
     using Tr = ModeTraits<MODE>;
     constexpr bool kNarrow = pair_narrow<MODE, V>();
     using Cfg = PairCfg<MODE, kNarrow>;
     // (FP32-emulated only: a K-block pair there is 1.5K MMA cycles, enough to hide the polls)
-    constexpr bool kBlockDeps = FFG_BLOCK_DEPS && !RES && Tr::kHasLo;
+    constexpr bool kBlockDeps = FFG_BLOCK_DEPS && Tr::kHasLo;
     constexpr bool kDrain = Tr::kProducts == 3;
+    // per-K16 / per-2-K16 drain layers: only the FFG_FIXED_SPLIT=0 scheme or FFG_SEMI_DRAIN builds
+    constexpr bool kExactPath = !FFG_FIXED_SPLIT || FFG_SEMI_DRAIN;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -675,7 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
     const int pair_id = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-    const int total = (p.l1 - p.l0) * p.B * p.PT;
+    uint32_t* valid_bits = reinterpret_cast<uint32_t*>(smem + Cfg::kValidOff);
     const int nk = p.np / kBK;
     const int nb = p.nb;
 
@@ -686,20 +473,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
         for (int i = 0; i < 4; ++i) {
             mbar_init(&slot_full[i], 1);
-            // streaming: drain warps, or epilogue warps (Y slot); resident: the 16 worker warps
-            mbar_init(&slot_empty[i], (RES || S16) ? 2 * kResWorkers : 2 * kEpiWarps);
+            // drain warps, or epilogue warps (Y slot); S16: the 16 worker warps
+            mbar_init(&slot_empty[i], S16 ? 2 * kResWorkers : 2 * kEpiWarps);
         }
         for (int i = 0; i < 4; ++i) mbar_init(&y_full[i], kEpiWarps);
         fence_barrier_init();
+    }
+    // validity bitmap of this launch's matrices (K1's bounds are final: K1 ran before this launch
+    // in stream order)
+    for (int wd = threadIdx.x; wd < (p.B + 31) / 32; wd += blockDim.x) {
+        uint32_t bits = 0u;
+        for (int b = 0; b < 32; ++b) {
+            const int m = 32 * wd + b;
+            if (m < p.B && matrix_in_region(p.region, p.m0 + m)) bits |= 1u << b;
+        }
+        valid_bits[wd] = bits;
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
     tc_fence_before();
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    MatrixMap mm{valid_bits, 0, false};
+    for (int wd = 0; wd < (p.B + 31) / 32; ++wd) mm.nvalid += __popc(valid_bits[wd]);
+    mm.remap = mm.nvalid != p.B;
+    const int total = (p.l1 - p.l0) * mm.nvalid * p.PT;
 
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"((RES || S16) ? kRRegsCtl : kPRegsCtl) : "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(S16 ? kRRegsCtl : kPRegsCtl) : "memory");
         if (warp == 0 && lane == 0) {
             // ================================================= TMA producer (both CTAs)
             for (int i = 0; i < 2; ++i) {
@@ -716,10 +517,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const long long t_start = clock64();
             for (int item = pair_id; item < total; item += n_pairs) {
                 int m, l, pi;
-                pair_decode(p, item, m, l, pi);
+                pair_decode(p, mm, item, m, l, pi);
                 const uint32_t pr = __ldg(p.pairs + pi);
                 const int a0 = pr & 1023, a1 = (pr >> 10) & 1023, sp = (pr >> 20) & 1023;
-                const bool dummy = (pr >> 30) & 1;
                 const int ap = rank ? a1 : a0;
                 // block-granular dependencies: when a panel is not complete yet, each K-block
                 // pair (one 128-column block of panels A_c and S) is waited for just before it is
@@ -740,17 +540,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     while (ld_acquire_gpu(cm + sp) < need && (FFG_DEP_BACKOFF ? (__nanosleep(FFG_DEP_BACKOFF), 1) : 1))
                         watchdog_check(t0, 4, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + sp),
                                        ((unsigned long long)need << 32) | ld_acquire_gpu(cm + sp));
-                    if (p.dbg & 8) w_dep += (unsigned long long)(clock64() - t0);
+                    if (FFG_ROLE_PROF && (p.dbg & 8)) w_dep += (unsigned long long)(clock64() - t0);
                     fence_proxy_async_global();
                 }
                 // warm L2 with the X/A block the epilogue of a LATER item of this CTA will read
                 // (FFG_XA_AHEAD items ahead; L2 is the coherence point, so an early prefetch
                 // cannot serve stale data)
-                if (!RES && !(p.dbg & 1)) {
+                if (!(p.dbg & 1)) {
                     const int ia = item + FFG_XA_AHEAD * n_pairs;
                     if (ia < total) {
                         int m2, l2, pi2;
-                        pair_decode(p, ia, m2, l2, pi2);
+                        pair_decode(p, mm, ia, m2, l2, pi2);
                         const uint32_t pr2 = __ldg(p.pairs + pi2);
                         if (!(rank && ((pr2 >> 30) & 1))) {
                             const int ap2 = rank ? (pr2 >> 10) & 1023 : pr2 & 1023;
@@ -786,7 +586,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                             watchdog_check(t0, 6, ((unsigned long long)item << 32) | (uint32_t)(sp * 1024 + blk), need);
                             vs = ld_acquire_gpu(fs);
                         }
-                        if (p.dbg & 8) w_dep += (unsigned long long)(clock64() - t0);
+                        if (FFG_ROLE_PROF && (p.dbg & 8)) w_dep += (unsigned long long)(clock64() - t0);
                         fence_proxy_async_global();
                     }
                     FFG_TIMED(w_empty, mbar_wait(&empty[s], ((it / S) & 1) ^ 1));
@@ -807,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     }
                 }
             }
-            if (p.dbg & 8) {
+            if (FFG_ROLE_PROF && (p.dbg & 8)) {
                 unsigned long long* o = p.prof + (size_t)blockIdx.x * 16;
                 o[0] = (unsigned long long)(clock64() - t_start);
                 o[1] = w_dep;
@@ -825,9 +625,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             unsigned long long w_full = 0, w_slot = 0;
             for (int item = pair_id; item < total; item += n_pairs) {
                 int m, l, pi;
-                pair_decode(p, item, m, l, pi);
+                pair_decode(p, mm, item, m, l, pi);
                 const int kst = layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep);
                 const bool exact = kst != 0 && kst < kBK / kUK;
+                // cross-term order (pair-table bit 31): hi*lo then lo*hi, or swapped for an item
+                // whose blocks are the transposes of blocks computed elsewhere in the other
+                // orientation -- element (i, j) then gets exactly the value (j, i) gets there
+                // (the products of each sum are the same; only their accumulation order matters)
+                const bool swapx = (__ldg(p.pairs + pi) >> 31) & 1u;
+                // the item's MMA sequence with the cross-term order fixed at compile time (no extra
+                // registers in this 48-register role)
+                auto run_item = [&](auto swap_tag) {
+                constexpr bool kSwap = decltype(swap_tag)::value;
+                constexpr uint32_t x1a = kSwap ? offAlo : 0u, x1b = kSwap ? offBhi : offBlo;
+                constexpr uint32_t x2a = kSwap ? 0u : offAlo, x2b = kSwap ? offBlo : offBhi;
                 uint32_t t_slot = 0;
                 auto open_slot = [&]() {
                     const int sl = g % kSlots;
@@ -845,7 +656,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 // FFG_FIXED_SPLIT: hi*hi over the whole K in one accumulator (exact: every product
                 // and partial sum lies on the 2^6 grid of the fixed-point hi, |sum| < 2^30), the cross
                 // terms in a second; the drain adds the two once
-                const bool kFixed = kDrain && kst == 0;
+                const bool kFixed = kDrain && kst == 0 && !(p.dbg & 2);
+                // instrumented product count: product passes of this item
+                if (p.products && lane == 0)
+                    atomicAdd(&p.products[m], (uint32_t)(kFixed ? (FFG_FIXED_LOLO ? 4 : 3) : Tr::kProducts));
                 uint32_t t_hh = 0, t_x = 0;
                 if (kFixed) {
                     const int s0 = g % kSlots, s1 = (g + 1) % kSlots;
@@ -866,8 +680,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
                             for (int kk = 0; kk < kBK / kUK; ++kk) {
                                 const uint32_t koff = kk * kUK * 2;
-                                umma_f16_pair(t_x, D(sb, koff), D(sb, offBlo + koff), idesc, (kb | kk) != 0);
-                                umma_f16_pair(t_x, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
+                                umma_f16_pair(t_x, D(sb, x1a + koff), D(sb, x1b + koff), idesc, (kb | kk) != 0);
+                                umma_f16_pair(t_x, D(sb, x2a + koff), D(sb, x2b + koff), idesc, 1u);
                                 if (FFG_FIXED_LOLO)  // lo*lo: the fixed-point lo is absolute (~2^-12), not negligible
                                     umma_f16_pair(t_x, D(sb, offAlo + koff), D(sb, offBlo + koff), idesc, 1u);
                                 umma_f16_pair(t_hh, D(sb, koff), D(sb, offBhi + koff), idesc, (kb | kk) != 0);
@@ -882,7 +696,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                                 umma_f16_pair(t_slot, D(sb, koff), D(sb, offBhi + koff), idesc, (kb | kk) != 0);
                             __syncwarp();
                         }
-                    } else if (exact) {
+                    } else if (kExactPath && exact) {
                         auto issue = [&](auto kc) {
                             constexpr int KST = decltype(kc)::value;
 #pragma unroll
@@ -892,8 +706,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
                                     for (int kk = k0; kk < k0 + KST; ++kk) {
                                         const uint32_t koff = kk * kUK * 2;
-                                        umma_f16_pair(t_slot, D(sb, koff), D(sb, offBlo + koff), idesc, kk != k0);
-                                        umma_f16_pair(t_slot, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
+                                        umma_f16_pair(t_slot, D(sb, x1a + koff), D(sb, x1b + koff), idesc, kk != k0);
+                                        umma_f16_pair(t_slot, D(sb, x2a + koff), D(sb, x2b + koff), idesc, 1u);
                                     }
 #pragma unroll
                                     for (int kk = k0; kk < k0 + KST; ++kk) {
@@ -917,8 +731,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
                             for (int kk = 0; kk < kBK / kUK; ++kk) {
                                 const uint32_t koff = kk * kUK * 2;
-                                umma_f16_pair(t_slot, D(sb, koff), D(sb, offBlo + koff), idesc, !(first && kk == 0));
-                                umma_f16_pair(t_slot, D(sb, offAlo + koff), D(sb, offBhi + koff), idesc, 1u);
+                                umma_f16_pair(t_slot, D(sb, x1a + koff), D(sb, x1b + koff), idesc, !(first && kk == 0));
+                                umma_f16_pair(t_slot, D(sb, x2a + koff), D(sb, x2b + koff), idesc, 1u);
                             }
 #pragma unroll
                             for (int kk = 0; kk < kBK / kUK; ++kk) {
@@ -943,23 +757,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     if (kDrain) open_slot();
                     close_slot();
                 }
-            }
-            if ((p.dbg & 8) && lane == 0) {
+                            };
+                if (swapx)
+                    run_item(std::true_type{});
+                else
+                    run_item(std::false_type{});
+}
+            if ((FFG_ROLE_PROF && (p.dbg & 8)) && lane == 0) {
                 unsigned long long* o = p.prof + (size_t)blockIdx.x * 16;
                 o[3] = w_full;
                 o[4] = w_slot;
             }
         }
         __syncwarp();
-    } else if constexpr (RES) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRRegsWork) : "memory");
-        resident_workers<MODE>(p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk,
-                               slot_full, slot_empty, smem + Cfg::kStagingOff,
-                               reinterpret_cast<double*>(bars + 2 * S + 14));
     } else if constexpr (S16) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRRegsWork) : "memory");
         stream16_workers<MODE>(tm, p, tmem, warp, lane, rank, pair_id, n_pairs, total, nk, slot_full,
-                               slot_empty, smem + Cfg::kStagingOff, red);
+                               slot_empty, smem + Cfg::kStagingOff, red, mm);
     } else if (warp < 4 + kEpiWarps) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsDrain) : "memory");
         // ===================================================== chunk drain -> Y (both CTAs)
@@ -974,7 +788,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             unsigned long long w_sf = 0;
             for (int item = pair_id; item < total; item += n_pairs, ++u) {
                 int m, l, pi;
-                pair_decode(p, item, m, l, pi);
+                pair_decode(p, mm, item, m, l, pi);
                 const int chunks = (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
                 float yacc[kEpiCols];
     #pragma unroll
@@ -1036,7 +850,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     if (lane == 0) mbar_arrive(&y_full[sl]);
                 }
             }
-            if ((p.dbg & 8) && warp == 4 && lane == 0) p.prof[(size_t)blockIdx.x * 16 + 5] = w_sf;
+            if ((FFG_ROLE_PROF && (p.dbg & 8)) && warp == 4 && lane == 0) p.prof[(size_t)blockIdx.x * 16 + 5] = w_sf;
         }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPRegsEpi) : "memory");
@@ -1054,16 +868,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         uint32_t yph = 0;  // per-slot phase bits of y_full (a slot holds Y until freed here)
         unsigned long long w_y = 0, w_pub = 0, w_st = 0, w_cmp = 0, w_pc = 0, w_tail = 0, w_item = 0;
         for (int item = pair_id; item < total; item += n_pairs) {
-            const long long t_item = (p.dbg & 8) ? clock64() : 0;
+            const long long t_item = (FFG_ROLE_PROF && (p.dbg & 8)) ? clock64() : 0;
             int m, l, pi;
-            pair_decode(p, item, m, l, pi);
+            pair_decode(p, mm, item, m, l, pi);
             const uint32_t pr = __ldg(p.pairs + pi);
             const int R = rank ? (pr >> 10) & 1023 : pr & 1023;  // block rows (A panel)
             const int C = (pr >> 20) & 1023;                     // block cols (B panel)
             const bool dummy = rank && ((pr >> 30) & 1);
             const bool last = (l == p.n_layers - 1);
             EpiCoef k = load_coef(p.coef, l, p.n_layers, p.a_pair != 0);
-        k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
+            k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
+        k.sr = k.fixed && l + 1 < p.sr_layers;
             const int nxt = (l + 1) & 1;   // hi/lo parity written by this layer
             g += (p.dbg & 2) ? 1 : layer_chunks(MODE, nk, layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep));
             const int ysl = (g - 1) & 3;   // slot holding this item's Y
@@ -1075,6 +890,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             float* At = p.A + xa_tile_base(m, R, C, nb);
             EpiHealth hl;
             double tr = 0.0, sq = 0.0;
+            double t0 = 0.0, s0 = 0.0, t1 = 0.0, s1 = 0.0;  // last layer: statistics per 32x32 piece
             // X of this warp's first sub-block is requested before the wait for Y; every
             // sub-block then requests the next one's X before computing (software pipeline)
             const bool ok0 = !(dummy || (p.dbg & 1) || (diag && s < q));
@@ -1125,7 +941,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     __syncwarp();
                 }
                 const bool dblk = diag && qc == q;  // 32x32 piece on the matrix diagonal
-                const long long t_c0 = (p.dbg & 8) ? clock64() : 0;
+                const bool mir = !p.rowblock || diag;  // row-block: no mirror of an off-diagonal block
+                const long long t_c0 = (FFG_ROLE_PROF && (p.dbg & 8)) ? clock64() : 0;
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     const int c0 = 32 * qc + 16 * sub;
@@ -1143,24 +960,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         if (more && !(p.dbg & 128)) epi_loadx16(Xt, r, sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
                         if (diag)
                             epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
-                                                        p.dbg & 64);
+                                                        gi, C * kBN, p.dbg & 64);
                         else
                             epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
-                                                         p.dbg & 64);
+                                                         gi, C * kBN, p.dbg & 64);
                         if (more) {
 #pragma unroll
                             for (int j = 0; j < 4; ++j) xq[j] = xn[j];
                         }
                     } else {
-                        double* Dm = p.D ? p.D + (size_t)m * n * n : nullptr;
+                        double* Dm = p.D ? p.D + (size_t)m * n * n - (ptrdiff_t)p.drow0 * n : nullptr;
                         if (diag)
                             epi_sub_last<true>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
                         else
-                            epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                            epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq, mir);
                     }
                 }
-                const long long t_c1 = (p.dbg & 8) ? clock64() : 0;
-                if (p.dbg & 8) w_cmp += (unsigned long long)(t_c1 - t_c0);
+                const long long t_c1 = (FFG_ROLE_PROF && (p.dbg & 8)) ? clock64() : 0;
+                if (FFG_ROLE_PROF && (p.dbg & 8)) w_cmp += (unsigned long long)(t_c1 - t_c0);
+                if (last) {  // this piece's statistics over the warp (fixed butterfly)
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        tr += __shfl_xor_sync(0xffffffffu, tr, o);
+                        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                    }
+                    if (qi == 0) {
+                        t0 = tr;
+                        s0 = sq;
+                    } else {
+                        t1 = tr;
+                        s1 = sq;
+                    }
+                    tr = sq = 0.0;
+                }
                 if (kNarrow && !last && !(p.dbg & 32)) {
                     // direct pieces out, then the mirrors transposed in place once the direct stores
                     // have read the staging
@@ -1171,7 +1003,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, C * kBN + 32 * qc, m * np + R * kBM + 32 * q);
                         tma_store_commit();
                     }
-                    if (!dblk) {
+                    if (!dblk && mir) {
                         if (lane == 0) tma_store_wait_read();
                         __syncwarp();
                         transpose_piece_inplace(stg_a, lane);
@@ -1184,7 +1016,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         }
                     }
                 } else if (!last) {
-                    if (!dblk) {  // mirrored pieces: warp transpose of the direct pieces
+                    if (!dblk && mir) {  // mirrored pieces: warp transpose of the direct pieces
                         __syncwarp();
                         transpose_piece(stg_a, stg_a + 2 * kPieceBytes, lane);
                         if (Tr::kHasLo) transpose_piece(stg_a + kPieceBytes, stg_a + 3 * kPieceBytes, lane);
@@ -1196,7 +1028,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         const int pcol = C * kBN + 32 * qc;
                         tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
                         if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
-                        if (!dblk) {
+                        if (!dblk && mir) {
                             const int mrow = m * np + C * kBN + 32 * qc;
                             const int mcol = R * kBM + 32 * q;
                             tma_store_2d(&tm.p_hi[nxt], stg + 2 * kPieceBytes, mcol, mrow);
@@ -1205,9 +1037,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     }
                 }
                 if (lane == 0) tma_store_commit();  // one bulk group per quarter, possibly empty
-                if (p.dbg & 8) w_pc += (unsigned long long)(clock64() - t_c1);
+                if (FFG_ROLE_PROF && (p.dbg & 8)) w_pc += (unsigned long long)(clock64() - t_c1);
             }
-            const long long t_tail = (p.dbg & 8) ? clock64() : 0;
+            const long long t_tail = (FFG_ROLE_PROF && (p.dbg & 8)) ? clock64() : 0;
             // this warp's Y reads are done: release the pair's TMEM slot
             tc_fence_before();
             __syncwarp();
@@ -1219,20 +1051,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], l + 1);
             }
             if (last) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    tr += __shfl_xor_sync(0xffffffffu, tr, o);
-                    sq += __shfl_xor_sync(0xffffffffu, sq, o);
-                }
+                // block statistics: the 16 piece partials (index 4 * quarter + lane quarter) summed in
+                // piece order -- the same fixed order as the 16-worker epilogue
                 named_bar_sync(3, kEpiWarps2 * 32);  // previous block's partial consumed
                 if (lane == 0) {
-                    red[2 * ew + 0] = tr;
-                    red[2 * ew + 1] = sq;
+                    red[2 * (4 * s + q) + 0] = t0;
+                    red[2 * (4 * s + q) + 1] = s0;
+                    red[2 * (4 * (s + 2) + q) + 0] = t1;
+                    red[2 * (4 * (s + 2) + q) + 1] = s1;
                 }
                 named_bar_sync(3, kEpiWarps2 * 32);
                 if (ew == 0 && lane == 0) {
                     double T0 = 0.0, T1 = 0.0;
-                    for (int w = 0; w < kEpiWarps2; ++w) {  // fixed order
+                    for (int w = 0; w < 16; ++w) {  // fixed order
                         T0 += red[2 * w + 0];
                         T1 += red[2 * w + 1];
                     }
@@ -1264,16 +1095,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         if (C != R) red_relaxed_gpu_add(cm + C, 1u);
                     }
                 }
-                if (p.dbg & 8) w_pub += (unsigned long long)(clock64() - tp);
+                if (FFG_ROLE_PROF && (p.dbg & 8)) w_pub += (unsigned long long)(clock64() - tp);
             }
-            if (p.dbg & 8) {
+            if (FFG_ROLE_PROF && (p.dbg & 8)) {
                 const long long te = clock64();
                 w_tail += (unsigned long long)(te - t_tail);
                 w_item += (unsigned long long)(te - t_item);
             }
         }
         if (lane == 0) tma_store_wait_all();
-        if ((p.dbg & 8) && warp == 12 && lane == 0) {
+        if ((FFG_ROLE_PROF && (p.dbg & 8)) && warp == 12 && lane == 0) {
             unsigned long long* o = p.prof + (size_t)blockIdx.x * 16;
             o[6] = w_y;
             o[7] = w_pub;

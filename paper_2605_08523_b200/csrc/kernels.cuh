@@ -3,7 +3,7 @@
 //   K1  rescale_tiles        H (fp64) -> X0 = alpha H + gamma I (fp32 master), A1 = d0 X0,
 //                            binary16 hi/lo split of X0 * 2^14 (or bf16), Gershgorin bounds.
 //                            One HBM pass; HBM-bound.
-//                            (rescale_gershgorin: the row-per-lane form, spectral bounds API)
+//                            (gershgorin_kernel: bounds only, the spectral_bounds API)
 //   K2  mlsp2_pair_kernel    all recursion layers on tcgen05 CTA pairs (k2_pair.cuh, epilogue in
 //                            epilogue.cuh): (scalar_models.cpp:243-252 lifted to matrices;
 //                            SPEC.md:359-377)
@@ -60,17 +60,54 @@ struct ModeTraits<kModeBF16> {
 #ifndef FFG_FIXED_SPLIT
 #define FFG_FIXED_SPLIT 1  // FP32E exact layers: fixed-point hi instead of per-K16 drains (k2_pair.cuh)
 #endif
+#ifndef FFG_SR_LO
+#define FFG_SR_LO 1  // fixed-point split: stochastic (hash) rounding of the lo part
+#endif
+
+// Stochastic rounding of the fixed-point split's lo part.  The residual x 2^14 - hi is exact in
+// fp32; rounding it to nearest binary16 gives IDENTICAL errors to identical matrix entries (a
+// tight-binding X_0 has one hopping value on every bond), and the recursion turns that correlated
+// error into a systematic shift of the electron count (~1e-6 relative, measured; the first layers'
+// errors are amplified ~beta0/4).  Rounding up with probability (distance to the lower binary16
+// neighbour) / ulp instead -- the random draw a hash of the element's unordered index pair and the
+// layer, so it is symmetric, deterministic and independent of batch position -- makes the error
+// zero-mean and uncorrelated; the trace error drops ~10x.  Only the first
+// `sr_layers` layers' operands (default 3: the layers whose errors the recursion amplifies most)
+// are rounded this way.  Normal binary16 range: add 13 random bits below the binary16 precision of
+// the fp32 pattern and truncate; residuals in the binary16 subnormal range (< 2^-38 in X units)
+// then round to nearest in the conversion.
+#ifndef FFG_SR_LAYERS
+#define FFG_SR_LAYERS 3
+#endif
+__device__ __forceinline__ uint32_t sr_mix(uint32_t key, uint32_t layer) {
+    uint32_t x = key + layer * 0x9E3779B9u;
+    x *= 0x85EBCA77u;
+    x ^= x >> 13;
+    x *= 0xC2B2AE3Du;
+    x ^= x >> 16;
+    return x;
+}
+// key of the unordered pair {i, j} (indices < 65536)
+__device__ __forceinline__ uint32_t sr_hash(uint32_t i, uint32_t j, uint32_t layer) {
+    return sr_mix((min(i, j) << 16) | max(i, j), layer);
+}
+__device__ __forceinline__ float sr_f16_grid(float r, uint32_t h) {
+    return __uint_as_float((__float_as_uint(r) + (h & 0x1FFFu)) & ~0x1FFFu);
+}
+
 template <int MODE>
-__device__ __forceinline__ void split16(float x, uint16_t& hi, uint16_t& lo, bool fixed = false) {
+__device__ __forceinline__ void split16(float x, uint16_t& hi, uint16_t& lo, bool fixed = false, bool sr = false,
+                                        uint32_t h = 0) {
     if constexpr (MODE == kModeBF16) {
         hi = __bfloat16_as_ushort(__float2bfloat16_rn(x));
         lo = 0;
     } else {
         const float xs = x * kHalfScale;
-        const __half h = __float2half_rn((MODE == kModeF32E && fixed) ? rintf(xs * 0.125f) * 8.0f : xs);
-        hi = __half_as_ushort(h);
+        const __half hh = __float2half_rn((MODE == kModeF32E && fixed) ? rintf(xs * 0.125f) * 8.0f : xs);
+        hi = __half_as_ushort(hh);
         if constexpr (MODE == kModeF32E) {
-            lo = __half_as_ushort(__float2half_rn(xs - __half2float(h)));
+            const float r = xs - __half2float(hh);
+            lo = __half_as_ushort(__float2half_rn((FFG_SR_LO && fixed && sr) ? sr_f16_grid(r, h) : r));
         } else {
             lo = 0;
         }
@@ -104,105 +141,46 @@ struct RescaleParams {
     uint16_t* lo;               // [B][np][np] parity 0 (F32E only)
     unsigned long long* bounds; // [B][2] ordered keys of (eps_min, eps_max) before widening
     int* flags;                 // [B][2] first bad X_k index: [0] non-finite, [1] half range
-    int n, np, mode, write_operands;
+    int n, np, mode;
     const uint8_t* xa_used;     // [nb][nb] blocks whose X/A K2 reads (null: all blocks)
     int fixed;                  // FP32E: fixed-point hi split of X0 (layer 0 is an exact layer)
+    int sr;                     // ... with the stochastically rounded lo (sr_layers > 0)
 };
 
-// One warp per row; 8 rows per CTA; grid (np/8, B).
-__global__ void __launch_bounds__(256) rescale_gershgorin_kernel(const __grid_constant__ RescaleParams p) {
+// Gershgorin bounds only (the spectral_bounds entry): one warp per row, 8 rows per
+// CTA, grid (ceil(n/8), B); per-row radius in a fixed-order warp tree, exact min/max through
+// order-preserving integer atomics (deterministic).
+__global__ void __launch_bounds__(256) gershgorin_kernel(const double* __restrict__ H, int n,
+                                                         unsigned long long* bounds) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.y;
     const int i = blockIdx.x * 8 + warp;
-    const int n = p.n, np = p.np;
     __shared__ double s_lo[8], s_hi[8];
     double rlo = DBL_MAX, rhi = -DBL_MAX;
-    bool bad_nf = false, bad_hr = false;
-    if (i < np) {
-        const double alpha = p.alpha[m], gamma = p.gamma[m];
-        const size_t orow = ((size_t)m * np + i) * np;
-        const double* hrow = p.H + ((size_t)m * n + (i < n ? i : 0)) * n;
+    if (i < n) {
+        const double* hrow = H + ((size_t)m * n + i) * n;
         double radius = 0.0, hii = 0.0;
-        const bool vec = ((n & 3) == 0);
-        // columns in groups of 4 per lane: j = 4*lane + 128*t
-        for (int j0 = 4 * lane; j0 < np; j0 += 128) {
-            double h[4];
-            if (i < n && vec && j0 + 3 < n) {
-                const double2 v0 = *reinterpret_cast<const double2*>(hrow + j0);
-                const double2 v1 = *reinterpret_cast<const double2*>(hrow + j0 + 2);
-                h[0] = v0.x; h[1] = v0.y; h[2] = v1.x; h[3] = v1.y;
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) h[e] = (i < n && j0 + e < n) ? hrow[j0 + e] : 0.0;
-            }
-            float x[4];
+        // the column order of K1's per-lane sums (128-column tiles, 4 consecutive columns per lane),
+        // so both kernels produce bit-identical bounds
+        for (int c0 = 4 * lane; c0 < n; c0 += 128)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int j = j0 + e;
-                if (j == i) {
-                    hii = h[e];
-                } else {
-                    radius += fabs(h[e]);
-                }
-                double v = alpha * h[e];
-                if (j == i && i < n) v += gamma;
-                x[e] = (float)v;
-                bad_nf |= !isfinite(x[e]);
+                const int j = c0 + e;
+                const double h = j < n ? hrow[j] : 0.0;
+                if (j == i) hii = h; else radius += fabs(h);
             }
-            if (p.write_operands) {
-                // X / A: tile-interleaved layout (see xa_tile_base); hi / lo: row-major
-                const size_t xo = ((((size_t)m * (np / 128) + i / 128) * (np / 128) + j0 / 128) * 16384) +
-                                  ((size_t)((j0 & 127) >> 2) * 128 + (i & 127)) * 4;
-                *reinterpret_cast<float4*>(p.X + xo) = make_float4(x[0], x[1], x[2], x[3]);
-                const float d0 = (float)p.d0;
-                float a[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) a[e] = (float)(p.d0 * (double)x[e]);
-                (void)d0;
-                *reinterpret_cast<float4*>(p.A + xo) = make_float4(a[0], a[1], a[2], a[3]);
-                uint16_t hb[4], lb[4];
-                if (p.mode == kModeBF16) {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) split16<kModeBF16>(x[e], hb[e], lb[e]);
-                } else if (p.mode == kModeF16) {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        split16<kModeF16>(x[e], hb[e], lb[e]);
-                        bad_hr |= half_range_bad<kModeF16>(x[e]);
-                    }
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        split16<kModeF32E>(x[e], hb[e], lb[e], p.fixed != 0);
-                        bad_hr |= half_range_bad<kModeF32E>(x[e]);
-                    }
-                }
-                uint2 hv, lv;
-                hv.x = hb[0] | ((uint32_t)hb[1] << 16); hv.y = hb[2] | ((uint32_t)hb[3] << 16);
-                lv.x = lb[0] | ((uint32_t)lb[1] << 16); lv.y = lb[2] | ((uint32_t)lb[3] << 16);
-                *reinterpret_cast<uint2*>(p.hi + orow + j0) = hv;
-                if (p.mode == kModeF32E) *reinterpret_cast<uint2*>(p.lo + orow + j0) = lv;
-            }
-        }
-        // fixed-order warp tree (deterministic for a given n)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             radius += __shfl_xor_sync(0xffffffffu, radius, o);
             hii += __shfl_xor_sync(0xffffffffu, hii, o);  // exactly one lane holds H_ii
         }
-        if (i < n) {
-            rlo = hii - radius;
-            rhi = hii + radius;
-        }
+        rlo = hii - radius;
+        rhi = hii + radius;
     }
     if (lane == 0) {
         s_lo[warp] = rlo;
         s_hi[warp] = rhi;
     }
-    const bool any_nf = __any_sync(0xffffffffu, bad_nf);
-    const bool any_hr = __any_sync(0xffffffffu, bad_hr);
-    if (lane == 0 && any_nf) atomicMin(&p.flags[2 * m + 0], 0);
-    if (lane == 0 && any_hr) atomicMin(&p.flags[2 * m + 1], 0);
     __syncthreads();
     if (threadIdx.x == 0) {
         double lo = s_lo[0], hi = s_hi[0];
@@ -211,8 +189,8 @@ __global__ void __launch_bounds__(256) rescale_gershgorin_kernel(const __grid_co
             hi = fmax(hi, s_hi[w]);
         }
         if (lo <= hi) {
-            atomicMin(&p.bounds[2 * m + 0], ordered_key(lo));
-            atomicMax(&p.bounds[2 * m + 1], ordered_key(hi));
+            atomicMin(&bounds[2 * m + 0], ordered_key(lo));
+            atomicMax(&bounds[2 * m + 1], ordered_key(hi));
         }
     }
 }
@@ -235,8 +213,6 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
     const int row0 = blockIdx.x * kK1Rows;          // first row of this CTA
     const int I = row0 / 128, q = (row0 & 127) / kK1Rows;
     const double alpha = p.alpha[m], gamma = p.gamma[m];
-    const float d0f = (float)p.d0;
-    (void)d0f;
     double radius[4] = {0.0, 0.0, 0.0, 0.0}, hii[4] = {0.0, 0.0, 0.0, 0.0};
     bool bad_nf = false, bad_hr = false;
     // the four rows of tile J (this lane's 4 columns); tile J+1 is requested before tile J is
@@ -286,7 +262,7 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
                 x[e] = (float)v;
                 bad_nf |= !isfinite(x[e]);
             }
-            if (p.write_operands) {
+            {
                 float a[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) a[e] = (float)(p.d0 * (double)x[e]);
@@ -305,7 +281,8 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
                 } else {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        split16<kModeF32E>(x[e], hb[e], lb[e], p.fixed != 0);
+                        split16<kModeF32E>(x[e], hb[e], lb[e], p.fixed != 0, p.sr != 0,
+                                           p.sr ? sr_hash((uint32_t)i, (uint32_t)(c0 + e), 0u) : 0u);
                         bad_hr |= half_range_bad<kModeF32E>(x[e]);
                     }
                 }
@@ -317,7 +294,7 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
                 if (p.mode == kModeF32E) *reinterpret_cast<uint2*>(p.lo + orow + c0) = lv;
             }
         }
-        if (p.write_operands && (!p.xa_used || p.xa_used[I * nb + J])) {
+        if (!p.xa_used || p.xa_used[I * nb + J]) {
             __syncthreads();
             // block (I, J), rows 32q .. 32q+31: [c4][row][4]; thread t -> c4 = t / 8, rows 4(t%8)..+3
             const size_t tb = xa_tile_base(m, I, J, nb);
@@ -380,13 +357,41 @@ __device__ __forceinline__ uint32_t sw64(uint32_t r, uint32_t c) {
 constexpr int kEpiWarps2 = 8;                                       // epilogue warps
 constexpr int kPieceBytes = 32 * 64;                                // 32x32 binary16 piece
 
+// Region of validity of each matrix (Eq. 41 in the model's un-flipped frame,
+// SURVEY.md 0.4): x = mu0 + (beta/beta0)(eps - mu) must lie in [0, 1] at both Gershgorin bounds,
+// widened by 1e-12 W.  K2 skips matrices that fail it (rescale_to_model fails before
+// apply_model) and K3 reports the status; both evaluate this one function.
+struct RegionCheck {
+    const unsigned long long* bounds;  // [B][2] ordered keys of (eps_min, eps_max) from K1
+    const double* scale;               // [B] beta/beta0, or null: no check (apply_model, mixed_square)
+    const double* mu;                  // [B]
+    double mu0;
+};
+__device__ __forceinline__ void widened_bounds(const RegionCheck& rc, int m, double& lo, double& hi) {
+    lo = key_to_double(rc.bounds[2 * m + 0]);
+    hi = key_to_double(rc.bounds[2 * m + 1]);
+    const double w = 1e-12 * (hi - lo);
+    lo -= w;
+    hi += w;
+}
+__device__ __forceinline__ bool matrix_in_region(const RegionCheck& rc, int m, double* xmin = nullptr,
+                                                 double* xmax = nullptr) {
+    if (!rc.scale) return true;
+    double lo, hi;
+    widened_bounds(rc, m, lo, hi);
+    const double x0 = rc.mu0 + rc.scale[m] * (lo - rc.mu[m]);
+    const double x1 = rc.mu0 + rc.scale[m] * (hi - rc.mu[m]);
+    if (xmin) *xmin = x0;
+    if (xmax) *xmax = x1;
+    return x0 >= 0.0 && x1 <= 1.0;  // (false for NaN)
+}
+
 struct FinalizeParams {
     const double2* partials;          // [B][T]
-    const unsigned long long* bounds; // [B][2]
     const int* flags;                 // [B][2]
-    const double* scale;              // [B] beta/beta0 (validity check), may be null
-    const double* mu;                 // [B]
-    double mu0;
+    RegionCheck region;               // bounds + validity inputs (scale null: no check)
+    double* D;                        // [B][d_elems] or null: an out-of-region matrix's D is set to NaN
+    int64_t d_elems;                  // elements of D per matrix (n * n, or a row-block rank's rows * n)
     int T, B;
     double* stats;                    // [B][2] (Tr D, Tr D^2)
     double* bounds_out;               // [B][4] (eps_min, eps_max, x_min, x_max) widened
@@ -396,6 +401,12 @@ struct FinalizeParams {
 // status codes mirror ffg_status (include/fermiforge/ffg.h)
 __global__ void __launch_bounds__(256) finalize_stats_kernel(const __grid_constant__ FinalizeParams p) {
     const int m = blockIdx.x;
+    if (p.D && !matrix_in_region(p.region, m)) {
+        // K2 skipped this matrix (no recursion outside the region): its D is NaN,
+        // never a stale or plausible-looking matrix in the caller's buffer
+        double* Dm = p.D + (size_t)m * p.d_elems;
+        for (int64_t i = threadIdx.x; i < p.d_elems; i += blockDim.x) Dm[i] = __longlong_as_double(0x7ff8000000000000ll);
+    }
     __shared__ double s0[256], s1[256];
     double a = 0.0, b = 0.0;
     for (int t = threadIdx.x; t < p.T; t += 256) {
@@ -416,18 +427,11 @@ __global__ void __launch_bounds__(256) finalize_stats_kernel(const __grid_consta
     if (threadIdx.x == 0) {
         p.stats[2 * m + 0] = s0[0];
         p.stats[2 * m + 1] = s1[0];
-        double lo = key_to_double(p.bounds[2 * m + 0]);
-        double hi = key_to_double(p.bounds[2 * m + 1]);
-        const double w = 1e-12 * (hi - lo);
-        lo -= w;
-        hi += w;
+        double lo, hi;
+        widened_bounds(p.region, m, lo, hi);
         int st = 0;
         double xmin = 0.0, xmax = 0.0;
-        if (p.scale) {
-            xmin = p.mu0 + p.scale[m] * (lo - p.mu[m]);
-            xmax = p.mu0 + p.scale[m] * (hi - p.mu[m]);
-            if (!(xmin >= 0.0) || !(xmax <= 1.0)) st = 2;  // FFG_ERR_OUT_OF_REGION
-        }
+        if (!matrix_in_region(p.region, m, &xmin, &xmax)) st = 2;  // FFG_ERR_OUT_OF_REGION
         // the earlier event wins (a binary16 split overflow at X_k precedes a non-finite X_{k+1});
         // a non-finite X_k also overflows its split, so ties report divergence
         const int nf = p.flags[2 * m + 0], hr = p.flags[2 * m + 1];

@@ -34,6 +34,7 @@ LIB_PATH = os.environ.get("FFG_LIB_PATH") or os.path.join(_PKG, "lib", "libfermi
 
 _D = ctypes.POINTER(ctypes.c_double)
 _F = ctypes.POINTER(ctypes.c_float)
+MODEL_SCHEMA_VERSION = 1  # ModelFile schema
 
 
 class PrecisionMode(IntEnum):
@@ -213,10 +214,31 @@ class Mlsp2Model:
 
     @staticmethod
     def from_json(path: str) -> "Mlsp2Model":
+        """Load a ModelFile: schema_version is checked on load, coefficients are
+        decimal strings with 17 significant digits (bit-exact binary64 round trip)."""
         with open(path) as f:
             d = json.load(f)
+        ver = d.get("schema_version")
+        if ver != MODEL_SCHEMA_VERSION:
+            raise ValidationError(f"{path}: ModelFile schema_version {ver!r} is not supported "
+                                  f"(expected {MODEL_SCHEMA_VERSION})")
+        if str(d.get("architecture", "")).lower() != "mlsp2":
+            raise ValidationError(f"{path}: architecture {d.get('architecture')!r} is not MLSP2")
         abcd = np.array([[float(v) for v in row] for row in d["layers"]], dtype=np.float64)
         return Mlsp2Model(abcd, float(d["beta0"]), float(d["mu0"]), d.get("name", ""), d)
+
+    def to_json(self, path: str, **extra) -> None:
+        """Write a ModelFile: schema_version, created timestamp, 17-significant-digit decimals."""
+        import datetime
+        d = {k: v for k, v in self.meta.items() if k not in ("layers", "beta0", "mu0")}
+        d.update(extra)
+        d.update({"schema_version": MODEL_SCHEMA_VERSION, "name": self.name or d.get("name", ""),
+                  "architecture": "mlsp2", "beta0": "%.17g" % self.beta0, "mu0": "%.17g" % self.mu0,
+                  "layers": [["%.17g" % v for v in row] for row in self.abcd]})
+        d.setdefault("created", datetime.datetime.now(datetime.timezone.utc).strftime("%Y-%m-%dT%H:%M:%SZ"))
+        with open(path, "w") as f:
+            json.dump(d, f, indent=1)
+            f.write("\n")
 
 
 def load_model(name: str = "M1500") -> Mlsp2Model:
@@ -399,20 +421,31 @@ def compute_density_matrices_device(H_dev, mu, kT, model: Mlsp2Model,
     """
     import torch
 
-    if H_dev.dtype != torch.float64 or not H_dev.is_cuda or H_dev.dim() != 3:
+    if H_dev.dtype != torch.float64 or not H_dev.is_cuda or H_dev.dim() != 3 or H_dev.shape[1] != H_dev.shape[2]:
         raise ValidationError("H_dev must be a CUDA float64 tensor [B, n, n]")
-    H_dev = H_dev.contiguous()
     B, n, _ = H_dev.shape
     dev = H_dev.device
-    if stats_dev is None:
-        stats_dev = torch.empty((B, 2), dtype=torch.float64, device=dev)
-    if status_dev is None:
-        status_dev = torch.empty((B,), dtype=torch.int32, device=dev)
-    if bounds_dev is None:
-        bounds_dev = torch.empty((B, 4), dtype=torch.float64, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+
+    def _out(t, shape, dtype, name):
+        # caller-supplied outputs receive raw device writes: check them exactly
+        if t is None:
+            return torch.empty(shape, dtype=dtype, device=dev)
+        if t.dtype != dtype or tuple(t.shape) != shape or t.device != dev or not t.is_contiguous():
+            raise ValidationError(f"{name} must be a contiguous {dtype} tensor {list(shape)} on {dev} "
+                                  f"(got {t.dtype} {list(t.shape)} on {t.device})")
+        return t
+
+    if D_dev is not None:
+        _out(D_dev, (B, n, n), torch.float64, "D_dev")
+    stats_dev = _out(stats_dev, (B, 2), torch.float64, "stats_dev")
+    status_dev = _out(status_dev, (B,), torch.int32, "status_dev")
+    bounds_dev = _out(bounds_dev, (B, 4), torch.float64, "bounds_dev")
+    if not H_dev.is_contiguous():
+        H_dev = H_dev.contiguous()
+        H_dev.record_stream(st)  # the temporary must outlive the kernels queued on `st`
     mu = np.ascontiguousarray(np.broadcast_to(np.asarray(mu, dtype=np.float64), (B,)))
     kT = np.ascontiguousarray(np.broadcast_to(np.asarray(kT, dtype=np.float64), (B,)))
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
     m = model._c()
     _check(lib().ffg_density_matrices_dev(B, H_dev.data_ptr(), n, _dp(mu), _dp(kT), ctypes.byref(m),
                                           int(mode), D_dev.data_ptr() if D_dev is not None else None,

@@ -54,6 +54,9 @@ class EntropyModel:
     def from_json(path: str) -> "EntropyModel":
         with open(path) as f:
             d = json.load(f)
+        if d.get("schema_version") != E.MODEL_SCHEMA_VERSION:
+            raise E.ValidationError(f"{path}: ModelFile schema_version {d.get('schema_version')!r} is not "
+                                    f"supported (expected {E.MODEL_SCHEMA_VERSION})")
         abcd = np.array([[float(v) for v in row] for row in d["layers"]], dtype=np.float64)
         inner = E.Mlsp2Model(abcd, float(d["beta0"]), float(d["mu0"]), d.get("name", ""), d)
         return EntropyModel(inner, float(d["alpha"]), d.get("name", ""), d)

@@ -68,7 +68,7 @@ def test_cli_apply_and_solve_mu(tmp_path):
                        capture_output=True, text=True, cwd=ROOT, timeout=300)
     assert r.returncode == 0, r.stderr
     prov = json.loads(r.stdout.splitlines()[-1])
-    assert prov["model"]["beta0"] == 1500.0 and prov["half_products"] == 90
+    assert prov["model"]["beta0"] == 1500.0 and prov["half_products"] == 100
     D, _, _ = E.compute_density_matrix(read_matrix_market(str(hp)), 0.0, 0.01, E.load_model("M1500"))
     assert np.array_equal(read_matrix_market(str(dp)), D)
     r = subprocess.run([sys.executable, "-m", "paper_2605_08523_b200", "apply", "--model", "M1500",

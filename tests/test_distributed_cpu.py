@@ -77,3 +77,23 @@ def test_result_gather_single_process():
     rec = g.gather(torch.ones((3, 2), dtype=torch.float64), torch.zeros(3, dtype=torch.int32))
     stats, status = ResultGather.unpack(rec, 3)
     assert stats.shape == (3, 2) and status.tolist() == [0, 0, 0]
+
+
+def test_bench_gpus_2_self_launches_two_ranks():
+    """`python bench.py --gpus 2` (no torchrun in the environment) re-launches itself as two
+    ranks under torch.distributed.run; with --fake-compute they run over gloo on CPU, gather
+    every matrix's record and rank 0 prints exactly one JSON line for n_gpus=2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--fake-compute",
+                        "--n", "64", "--batch", "3", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, env=env, timeout=240, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["fake"] and d["gathered"] == 6 and d["gather_ok"]
+    assert d["config"]["global_batch"] == 6 and d["value"] > 0

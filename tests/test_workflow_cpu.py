@@ -61,3 +61,27 @@ def test_library_pairs_entropy_models_by_trained_at():
         em = lib.entropy_for(m)
         assert (em.beta0, em.mu0) == (m.beta0, m.mu0)
         assert 0.5 <= em.alpha <= 0.98
+
+
+def test_model_file_schema_version_checked_and_round_trips(tmp_path):
+    """schema_version checked on load; 17-significant-digit decimals round-trip
+    the coefficients bit-exactly; a created timestamp is written."""
+    import json
+    from paper_2605_08523_b200 import engine as E
+    m = E.load_model("M40")
+    assert m.meta["schema_version"] == E.MODEL_SCHEMA_VERSION and "created" in m.meta
+    p = tmp_path / "m.json"
+    m.to_json(str(p))
+    m2 = E.Mlsp2Model.from_json(str(p))
+    assert np.array_equal(m2.abcd, m.abcd) and m2.beta0 == m.beta0 and m2.mu0 == m.mu0
+    d = json.loads(p.read_text())
+    for bad in (None, 2):
+        d2 = dict(d)
+        if bad is None:
+            d2.pop("schema_version")
+        else:
+            d2["schema_version"] = bad
+        q = tmp_path / f"bad{bad}.json"
+        q.write_text(json.dumps(d2))
+        with pytest.raises(E.ValidationError, match="schema_version"):
+            E.Mlsp2Model.from_json(str(q))
