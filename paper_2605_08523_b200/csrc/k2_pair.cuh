@@ -492,6 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
     tc_fence_before();
     cluster_sync_all();
+    __syncthreads();  // (the cluster barrier already orders the slot write; this makes it visible to racecheck)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     MatrixMap mm{valid_bits, 0, false};

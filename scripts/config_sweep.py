@@ -5,9 +5,13 @@ Accuracy references (measurement only; the CPU oracle stays test infrastructure)
   * fp64 recursion: the same MLSP2 polynomial evaluated with torch float64 GEMMs on the GPU
     (X0 = (1 - mu0) I - (beta/beta0)(H - mu I); A += d X; X = a X^2 + b X + c I; D = A + X),
   * exact Fermi matrix V diag(f(lambda)) V^T from torch.linalg.eigh (float64), reported, not gated.
+Every row carries the nvidia-smi clocks / throttle reasons sampled while it was timed, the
+fraction of the measured bf16 peak (burst: each row times its kernels alone), and -- for the
+single-matrix configs -- the paper's comparator on the same box: cuSOLVER diagonalisation
+(torch.linalg.eigh -> cusolverDn{D,S}syevd) plus the D = V f(lambda) V^T assembly.
 Writes one JSON document (stdout, or --out).
 
-    python scripts/config_sweep.py [--out profiles/r1_configs.json] [--quick]
+    python scripts/config_sweep.py [--out profiles/r2_configs.json] [--quick]
 """
 from __future__ import annotations
 
@@ -23,6 +27,7 @@ import torch  # noqa: E402
 
 from paper_2605_08523_b200 import engine as E  # noqa: E402
 from paper_2605_08523_b200.hamiltonians import tight_binding, batch_params  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 DEV = torch.device("cuda", 0)
 
@@ -66,31 +71,58 @@ def timed(H_dev, mu, kT, model, mode, reps):
     E.compute_density_matrices_device(H_dev, mu, kT, model, mode, D_dev=D)
     torch.cuda.synchronize()
     ts = []
+    with ClockSampler(0) as clk:
+        t_end = time.perf_counter() + 0.3  # at least ~0.3 s under load so the clock sampler sees it
+        while len(ts) < reps or time.perf_counter() < t_end:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            _, status, _ = E.compute_density_matrices_device(H_dev, mu, kT, model, mode, D_dev=D)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+    st = status.cpu().numpy()
+    assert (st == 0).all(), st
+    return float(np.median(ts)), D, clk.summary()
+
+
+def cusolver_time(H: torch.Tensor, mu: float, kT: float, dtype, reps: int = 3) -> float:
+    """Paper's comparator: cusolverDn{D,S}syevd (torch.linalg.eigh) + D = V f V^T, median seconds."""
+    Hd = H.to(dtype)
+    fermi_exact(Hd, mu, kT)
+    torch.cuda.synchronize()
+    ts = []
     for _ in range(reps):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
-        _, status, _ = E.compute_density_matrices_device(H_dev, mu, kT, model, mode, D_dev=D)
+        fermi_exact(Hd, mu, kT)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) / 1e3)
-    st = status.cpu().numpy()
-    assert (st == 0).all(), st
-    return float(np.median(ts)), D
+    return float(np.median(ts))
 
 
-def run_case(name, n, B, mode, model, pk, reps, ref_idx=(0,), exact=True, mu=None, kT=None):
+def run_case(name, n, B, mode, model, pk, reps, ref_idx=(0,), exact=True, mu=None, kT=None, cusolver=False):
     if mu is None:
         mu, kT = np.zeros(B), np.full(B, 0.01)
     seeds = [1234] if B == 1 else [10000 + k for k in range(B)]
     H = np.stack([tight_binding(n, seed=s) for s in seeds])
     H_dev = torch.from_numpy(H).to(DEV)
-    t, D = timed(H_dev, mu, kT, model, mode, reps)
+    t, D, clocks = timed(H_dev, mu, kT, model, mode, reps)
     F = B * E.algorithmic_flops(n, model.layer_count, mode)
     out = {"config": name, "n": n, "batch": B, "mode": mode.name, "seconds": t,
            "matrices_per_s": B / t, "algorithmic_tflops": F / t / 1e12,
+           "frac_of_burst_bf16": F / t / 1e12 / pk["bf16_tflops"],
            "frac_of_sustained_bf16": F / t / 1e12 / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
-           "fp32_equiv_gemm_tflops": B * model.layer_count * 2.0 * n ** 3 / t / 1e12}
+           "fp32_equiv_gemm_tflops": B * model.layer_count * 2.0 * n ** 3 / t / 1e12, "clocks": clocks}
+    if cusolver:
+        td = cusolver_time(H_dev[0], float(mu[0]), float(kT[0]), torch.float64)
+        ts_ = cusolver_time(H_dev[0], float(mu[0]), float(kT[0]), torch.float32)
+        out["cusolver"] = {"dsyevd_plus_D_s": td, "ssyevd_plus_D_s": ts_,
+                           "speedup_vs_dsyevd": td / (t / B), "speedup_vs_ssyevd": ts_ / (t / B),
+                           "note": "torch.linalg.eigh (cusolverDn{D,S}syevd) + V f(lambda) V^T on the same B200; "
+                                   "the paper's comparator (PAPER.md:682-688: 16x / 9x vs D, 5x / 2x vs S on RTX 6000 Ada)"}
     errs, errs_exact = [], []
     for k in ref_idx:
         R = recursion_f64(H_dev[k], float(mu[k]), float(kT[k]), model)
@@ -115,15 +147,15 @@ def main():
     args = ap.parse_args()
     model = E.load_model("M1500")
     pk = peaks()
-    F32E, BF16 = E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16
+    F32E, BF16, FP16 = E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16, E.PrecisionMode.FP16
     rows = []
     rows.append(run_case("configs[0] N=256 single", 256, 1, F32E, model, pk, 20))
     rows.append(run_case("configs[0] N=256 single", 256, 1, BF16, model, pk, 20))
-    rows.append(run_case("configs[1] N=1024 single", 1024, 1, F32E, model, pk, 10))
+    rows.append(run_case("configs[1] N=1024 single", 1024, 1, F32E, model, pk, 10, cusolver=True))
     rows.append(run_case("configs[1] N=1024 batch 16 (bench)", 1024, 16, F32E, model, pk, 10, ref_idx=(0, 7)))
     for n in (4096, 8192):
-        for mode in (F32E, BF16):
-            rows.append(run_case("configs[2] N=%d single" % n, n, 1, mode, model, pk, 3))
+        for mode in (F32E, BF16, FP16):
+            rows.append(run_case("configs[2] N=%d single" % n, n, 1, mode, model, pk, 3, cusolver=mode == F32E))
     if not args.quick:
         mu, kT = batch_params(512)
         for mode in (F32E, BF16):

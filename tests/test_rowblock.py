@@ -125,3 +125,33 @@ def test_rowblock_out_of_region_and_order_checks():
     assert torch.isnan(D).all()
     with pytest.raises(E.DimensionError, match="divide evenly"):
         RB.RowBlockRank(H, 0.0, 0.01, m, rank=0, world=3)
+
+
+@pytest.mark.gpu
+def test_rowblock_nccl_driver_single_rank():
+    """The torch.distributed driver (per-layer in-place NCCL all-gather of the operand rows, rank-order
+    statistics) with one rank on the one GPU of this box: D equals the single-GPU D bit for bit."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import os, sys, torch, numpy as np, torch.distributed as dist
+sys.path.insert(0, %r)
+from paper_2605_08523_b200 import engine as E, rowblock as RB
+from paper_2605_08523_b200.hamiltonians import tight_binding
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=%r)
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+m = E.load_model("M1500")
+H = torch.from_numpy(tight_binding(1024, seed=5)).cuda()
+D1 = torch.empty((1, 1024, 1024), dtype=torch.float64, device="cuda")
+s1, st1, _ = E.compute_density_matrices_device(H.unsqueeze(0), [0.0], [0.01], m, D_dev=D1)
+D, row0, stats, status = RB.rowblock_density_matrix(H, 0.0, 0.01, m)
+torch.cuda.synchronize()
+assert status == 0 and row0 == 0 and torch.equal(D, D1[0])
+assert abs(stats.trace - s1[0, 0].item()) <= 1e-12 * stats.trace
+dist.destroy_process_group()
+print("NCCL_ROWBLOCK_OK")
+""" % (root, str(_free_port()))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "NCCL_ROWBLOCK_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
