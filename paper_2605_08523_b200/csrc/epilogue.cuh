@@ -92,7 +92,8 @@ __device__ __forceinline__ float acc_step(float a, float x, const EpiCoef& k) {
 }
 
 // packed binary16 split of two values: hi = rn(x * 2^14), lo = rn(x * 2^14 - hi)
-// (bf16 mode: hi = rn_bf16(x), lo = 0).  fixed (FP32E, the layers before `exact_layers`): hi is
+// (bf16 mode: hi = rn_bf16(x), lo = rn_bf16(x - hi)).  Every mode stores lo: the next layer's
+// epilogue rebuilds X from hi + lo (load_xop); only FP32-emulated multiplies with it.  fixed (FP32E, the layers before `exact_layers`): hi is
 // rounded to a multiple of 8 in the 2^14-scaled domain (x on a 2^-11 grid, or 2^-10 where binary16
 // rounds it again for |x| >= 1), so the next layer's hi*hi products and all their partial sums lie on
 // the 2^6 grid and an fp32 accumulator adds them exactly (|sums| < 2^30 for a spectrum in [0, 1]);
@@ -103,25 +104,23 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
     if constexpr (MODE == kModeBF16) {
         const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
         hi = *reinterpret_cast<const uint32_t*>(&h);
-        lo = 0u;
+        const float2 f = __bfloat1622float2(h);
+        const __nv_bfloat162 r = __floats2bfloat162_rn(x0 - f.x, x1 - f.y);
+        lo = *reinterpret_cast<const uint32_t*>(&r);
     } else {
         const float s0 = x0 * kHalfScale, s1 = x1 * kHalfScale;
         const __half2 h = (MODE == kModeF32E && fixed)
                               ? __floats2half2_rn(rintf(s0 * 0.125f) * 8.0f, rintf(s1 * 0.125f) * 8.0f)
                               : __floats2half2_rn(s0, s1);
         hi = *reinterpret_cast<const uint32_t*>(&h);
-        if constexpr (MODE == kModeF32E) {
-            const float2 f = __half22float2(h);
-            float r0 = s0 - f.x, r1 = s1 - f.y;  // exact
-            if (FFG_SR_LO && fixed && sr) {
-                r0 = sr_f16_grid(r0, h0);
-                r1 = sr_f16_grid(r1, h1);
-            }
-            const __half2 r = __floats2half2_rn(r0, r1);
-            lo = *reinterpret_cast<const uint32_t*>(&r);
-        } else {
-            lo = 0u;
+        const float2 f = __half22float2(h);
+        float r0 = s0 - f.x, r1 = s1 - f.y;  // exact
+        if (MODE == kModeF32E && FFG_SR_LO && fixed && sr) {
+            r0 = sr_f16_grid(r0, h0);
+            r1 = sr_f16_grid(r1, h1);
         }
+        const __half2 r = __floats2half2_rn(r0, r1);
+        lo = *reinterpret_cast<const uint32_t*>(&r);
     }
 }
 
@@ -196,10 +195,36 @@ __device__ __forceinline__ void red_add_v4(float* gp, float a, float b, float c,
 }
 __device__ __forceinline__ float acc_term(float x, const EpiCoef& k) { return fmaf(k.d_hi, x, k.d_lo * x); }
 
-// X of 16 columns (c0 .. c0+15) of row r
-__device__ __forceinline__ void epi_loadx16(const float* Xt, int r, int c0, float4 (&xq)[4]) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) xq[j] = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
+// X_l of 16 consecutive columns of one row, as the packed binary16 (bf16) hi / lo operands the
+// layer multiplies (there is no fp32 master copy of X): one 32-byte load each (256-bit LDG: a warp
+// reads 32 whole sectors).  Rebuilt as (hi + lo) / scale -- exact in fp32 -- so b X and the
+// paired A term see X to the split's ~22 bits (16 in bf16 mode), measured inside the gates
+// (DESIGN.md 3).
+struct XOp {
+    uint32_t h[8], l[8];
+};
+__device__ __forceinline__ void ld_cg_v8(const void* p, uint32_t (&v)[8]) {
+    asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(p));
+}
+// hi / lo: the operand arrays of the layer's input parity at (row, first column) of the 16 values
+__device__ __forceinline__ void load_xop(const uint16_t* hi, const uint16_t* lo, XOp& x) {
+    ld_cg_v8(hi, x.h);
+    ld_cg_v8(lo, x.l);
+}
+template <int MODE>
+__device__ __forceinline__ float2 xop_pair(const XOp& x, int k) {  // elements 2k, 2k+1
+    if constexpr (MODE == kModeBF16) {
+        const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.h[k]));
+        const float2 l = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.l[k]));
+        return make_float2(h.x + l.x, h.y + l.y);
+    } else {
+        const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&x.h[k]));
+        const float2 l = __half22float2(*reinterpret_cast<const __half2*>(&x.l[k]));
+        constexpr float inv = 1.0f / kHalfScale;
+        return make_float2((h.x + l.x) * inv, (h.y + l.y) * inv);
+    }
 }
 
 // One 16-column sub-block (columns c0..c0+15 of the 128x128 block) of this thread's row r,
@@ -212,7 +237,7 @@ __device__ __forceinline__ void epi_loadx16(const float* Xt, int r, int c0, floa
 // gi / gj0: global row of this thread and first global column of the block (stochastic-rounding
 // hashes of the fixed-point split).
 template <int MODE, bool DIAG>
-__device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const float4 (&xq)[4], float* Xt, float* At,
+__device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const XOp& xq, float* At,
                                                 int r, int c0, int lane, int sub, bool c_on, const EpiCoef& k,
                                                 uint32_t stg_d, bool dblk, EpiHealth& hl, int gi, int gj0,
                                                 bool nomem = false) {
@@ -220,7 +245,8 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
     uint32_t hp[8], lp[8];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        float xs[4] = {xq[j].x, xq[j].y, xq[j].z, xq[j].w};
+        const float2 x01 = xop_pair<MODE>(xq, 2 * j), x23 = xop_pair<MODE>(xq, 2 * j + 1);
+        float xs[4] = {x01.x, x01.y, x23.x, x23.y};
         float ts[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -237,10 +263,8 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
             ts[e] = acc_term(xn, k) + fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]);
             xs[e] = xn;
         }
-        if (!nomem) {  // (measurement only: dbg & 64)
-            __stcg(reinterpret_cast<float4*>(Xt + xa_off(r, c0 / 4 + j)), make_float4(xs[0], xs[1], xs[2], xs[3]));
-            if (k.red) red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
-        }
+        if (!nomem && k.red)  // (nomem: measurement only, dbg & 64)
+            red_add_v4(At + xa_off(r, c0 / 4 + j), ts[0], ts[1], ts[2], ts[3]);
         uint32_t hh[4] = {0u, 0u, 0u, 0u};
         if (MODE == kModeF32E && FFG_SR_LO && k.sr) {
             // sr_hash(gi, gj, layer) incrementally: the key of {i, j} is (min << 16) | max; a block
@@ -259,10 +283,8 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
     if (!dblk) {
         sts_v4(stg_d + sw64(lane, 2 * sub + 0), hp[0], hp[1], hp[2], hp[3]);
         sts_v4(stg_d + sw64(lane, 2 * sub + 1), hp[4], hp[5], hp[6], hp[7]);
-        if (Tr::kHasLo) {
-            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 0), lp[0], lp[1], lp[2], lp[3]);
-            sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 1), lp[4], lp[5], lp[6], lp[7]);
-        }
+        sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 0), lp[0], lp[1], lp[2], lp[3]);
+        sts_v4(stg_d + kPieceBytes + sw64(lane, 2 * sub + 1), lp[4], lp[5], lp[6], lp[7]);
     } else {
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -274,10 +296,8 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
             const uint32_t doff = sw64(lane, col >> 3) + (col & 7) * 2;
             sts_u16(stg_d + off, hb);
             sts_u16(stg_d + doff, hb);
-            if (Tr::kHasLo) {
-                sts_u16(stg_d + kPieceBytes + off, lb);
-                sts_u16(stg_d + kPieceBytes + doff, lb);
-            }
+            sts_u16(stg_d + kPieceBytes + off, lb);
+            sts_u16(stg_d + kPieceBytes + doff, lb);
         }
     }
 }
@@ -286,16 +306,16 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const f
 // elements (Tr D, sum D^2 with off-diagonal elements counted twice); sixteen columns.  mir = false
 // (row-block table, off the diagonal blocks): only the direct entry, counted once -- the mirrored
 // entry belongs to another rank's rows, which computes it itself.
-template <bool DIAG>
-__device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const float* Xt, const float* At,
+template <int MODE, bool DIAG>
+__device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const XOp& xop, const float* At,
                                              int r, int c0, int gi, int gj0, int n, bool c_on,
                                              const EpiCoef& k, double* Dm, EpiHealth& hl, double& tr,
                                              double& sq, bool mir = true) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const float4 xq = __ldcg(reinterpret_cast<const float4*>(Xt + xa_off(r, c0 / 4 + j)));
+        const float2 x01 = xop_pair<MODE>(xop, 2 * j), x23 = xop_pair<MODE>(xop, 2 * j + 1);
         const float4 aq = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
-        const float xs[4] = {xq.x, xq.y, xq.z, xq.w};
+        const float xs[4] = {x01.x, x01.y, x23.x, x23.y};
         const float as[4] = {aq.x, aq.y, aq.z, aq.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {

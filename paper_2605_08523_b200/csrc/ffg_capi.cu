@@ -166,7 +166,6 @@ struct Workspace {
     int cap_B = 0;
     size_t cap_T = 0;      // B * T
     size_t cap_h = 0;      // staging elements (B * n * n)
-    float* X = nullptr;
     float* A = nullptr;
     uint16_t* op[4] = {nullptr, nullptr, nullptr, nullptr};  // hi0, lo0, hi1, lo1
     double* Hs = nullptr;
@@ -231,7 +230,6 @@ Workspace* get_ws(int dev, cudaStream_t st) {
 }
 
 void free_ws(Workspace* w) {
-    cudaFree(w->X);
     cudaFree(w->A);
     for (auto& p : w->op) cudaFree(p);
     cudaFree(w->Hs);
@@ -290,7 +288,6 @@ int ensure(Workspace& w, int B, int64_t np, int64_t T, bool operands) {
     const size_t elems = (size_t)B * np * np;
     if (operands && elems > w.cap_elems) {
         int rc;
-        if ((rc = grow(&w.X, dummy, elems))) return rc;
         if ((rc = grow(&w.A, dummy, elems))) return rc;
         for (auto& p : w.op)
             if ((rc = grow(&p, dummy, elems))) return rc;
@@ -851,7 +848,6 @@ int enqueue_k1(Workspace& w, const Job& j, cudaStream_t st, EnqueueCtx& cx) {
     rp.alpha = w.params;
     rp.gamma = w.params + B;
     rp.d0 = md.abcd[3];
-    rp.X = w.X;
     rp.A = w.A;
     rp.hi = w.op[0];
     rp.lo = w.op[1];
@@ -876,7 +872,10 @@ int enqueue_k2(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx
     const bool rowblock = j.rb_world > 0;
     int rc;
     PairParams pp{};
-    pp.X = w.X;
+    pp.ophi[0] = w.op[0];
+    pp.oplo[0] = w.op[1];
+    pp.ophi[1] = w.op[2];
+    pp.oplo[1] = w.op[3];
     pp.A = w.A;
     pp.D = (l1 == md.n_layers) ? j.D_dev : nullptr;
     pp.partials = w.partials;

@@ -156,8 +156,9 @@ struct PairMaps {
 };
 
 struct PairParams {
-    float* X;                 // [B][nb][nb] tile-interleaved blocks (all orientations written by K1)
-    float* A;
+    const uint16_t* ophi[2];  // binary16 (bf16) operand arrays [B][np][np] per parity: the epilogue
+    const uint16_t* oplo[2];  // rebuilds X_l from them (no fp32 master copy of X)
+    float* A;                 // [B][nb][nb] tile-interleaved blocks (the blocks K2 touches)
     double* D;                // last layer: [B][n][n] fp64 (full storage) or null
     double2* partials;        // last layer: [B][2*PT] per block (sum diag, sum sq)
     int* flags;               // [B][2]
@@ -292,34 +293,34 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
         k.fixed = FFG_FIXED_SPLIT && MODE == kModeF32E && l + 1 < p.exact_layers;  // next layer exact
         k.sr = k.fixed && l + 1 < p.sr_layers;
         const int nxt = (l + 1) & 1;
-        float* Xt = p.X + xa_tile_base(m, R, C, nb);
         float* At = p.A + xa_tile_base(m, R, C, nb);
+        // X_l of this thread's row in the block, from the layer's input operands (parity l & 1)
+        const size_t xrow = ((size_t)m * np + gi) * np + (size_t)C * kBN;
+        const uint16_t* xh = p.ophi[l & 1] + xrow;
+        const uint16_t* xl = p.oplo[l & 1] + xrow;
         EpiHealth hl;
         double tr = 0.0, sq = 0.0;
         if (!skip) {
             if (!last) {
                 if (lane == 0) tma_store_wait_read();  // the staging pieces are free again
                 __syncwarp();
-                float4 xq[4];
-                if (!(p.dbg & 128)) epi_loadx16(Xt, r, 32 * c, xq);
+                XOp xq;
+                if (!(p.dbg & 128)) load_xop(xh + 32 * c, xl + 32 * c, xq);
 #pragma unroll
                 for (int sub = 0; sub < 2; ++sub) {
                     const int c0 = 32 * c + 16 * sub;
-                    float4 xn[4];
-                    if (sub == 0 && !(p.dbg & 128)) epi_loadx16(Xt, r, c0 + 16, xn);
+                    XOp xn;
+                    if (sub == 0 && !(p.dbg & 128)) load_xop(xh + c0 + 16, xl + c0 + 16, xn);
                     uint32_t v[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * sub + e] * inv_s2);
                     if (diag)
-                        epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
+                        epi_sub_mid_red<MODE, true>(v, xq, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
                                                     gi, C * kBN, p.dbg & 64);
                     else
-                        epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
+                        epi_sub_mid_red<MODE, false>(v, xq, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
                                                      gi, C * kBN, p.dbg & 64);
-                    if (sub == 0) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) xq[j] = xn[j];
-                    }
+                    if (sub == 0) xq = xn;
                 }
                 if (!(p.dbg & 32)) {
                     fence_proxy_async_smem();
@@ -328,21 +329,21 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                         const int prow = m * np + R * kBM + 32 * q;  // direct piece origin
                         const int pcol = C * kBN + 32 * c;
                         tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
-                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
+                        tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
                         tma_store_commit();
                     }
                     if (!dblk && mir) {  // mirrored pieces: transpose in place once the direct stores read them
                         if (lane == 0) tma_store_wait_read();
                         __syncwarp();
                         transpose_piece_inplace(stg_a, lane);
-                        if (Tr::kHasLo) transpose_piece_inplace(stg_a + kPieceBytes, lane);
+                        transpose_piece_inplace(stg_a + kPieceBytes, lane);
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
                             const int mrow = m * np + C * kBN + 32 * c;
                             const int mcol = R * kBM + 32 * q;
                             tma_store_2d(&tm.p_hi[nxt], stg, mcol, mrow);
-                            if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, mcol, mrow);
+                            tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, mcol, mrow);
                             tma_store_commit();
                         }
                     }
@@ -355,10 +356,12 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                     uint32_t v[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * sub + e] * inv_s2);
+                    XOp xo;
+                    load_xop(xh + c0, xl + c0, xo);
                     if (diag)
-                        epi_sub_last<true>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                        epi_sub_last<MODE, true>(v, xo, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
                     else
-                        epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq, mir);
+                        epi_sub_last<MODE, false>(v, xo, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq, mir);
                 }
             }
         }
@@ -556,7 +559,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         if (!(rank && ((pr2 >> 30) & 1))) {
                             const int ap2 = rank ? (pr2 >> 10) & 1023 : pr2 & 1023;
                             const size_t tb = xa_tile_base(m2, ap2, (pr2 >> 20) & 1023, nb);
-                            tma_prefetch_l2_bulk(p.X + tb, kBM * kBN * 4);
                             tma_prefetch_l2_bulk(p.A + tb, kBM * kBN * 4);
                         }
                     }
@@ -887,8 +889,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const int gi = R * kBM + r;
             const bool c_on = gi < n;      // identity term only on real rows
             const uint32_t tacc = tlane + ysl * 128;
-            float* Xt = p.X + xa_tile_base(m, R, C, nb);
             float* At = p.A + xa_tile_base(m, R, C, nb);
+            // X_l of this thread's row in the block, from the layer's input operands (parity l & 1)
+            const size_t xrow = ((size_t)m * np + gi) * np + (size_t)C * kBN;
+            const uint16_t* xh = p.ophi[l & 1] + xrow;
+            const uint16_t* xl = p.oplo[l & 1] + xrow;
             EpiHealth hl;
             double tr = 0.0, sq = 0.0;
             double t0 = 0.0, s0 = 0.0, t1 = 0.0, s1 = 0.0;  // last layer: statistics per 32x32 piece
@@ -896,7 +901,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             // sub-block then requests the next one's X before computing (software pipeline)
             const bool ok0 = !(dummy || (p.dbg & 1) || (diag && s < q));
             const bool ok1 = !(dummy || (p.dbg & 1) || (diag && s + 2 < q));
-            float4 xq[4];
+            XOp xq;
             if (!last && (ok0 || ok1)) {
                 // the block's X of layer l is complete once panel R is (the producer's
                 // dependency wait; the early read must not rely on the wait for Y)
@@ -914,7 +919,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     }
                     __syncwarp();
                 }
-                if (!(p.dbg & 128)) epi_loadx16(Xt, r, 32 * (ok0 ? s : s + 2), xq);
+                if (!(p.dbg & 128)) {
+                    const int cq = 32 * (ok0 ? s : s + 2);
+                    load_xop(xh + cq, xl + cq, xq);
+                }
             }
             if constexpr (!kDrain) {
                 // single-product modes: the slot holds the whole-K accumulator, read directly
@@ -956,25 +964,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                             v[e] = __float_as_uint(__uint_as_float(v[e]) * (1.0f / (Tr::kScale * Tr::kScale)));
                     }
                     if (!last) {
-                        float4 xn[4];
+                        XOp xn;
                         const bool more = sub == 0 || (qi == 0 && ok1);
-                        if (more && !(p.dbg & 128)) epi_loadx16(Xt, r, sub == 0 ? c0 + 16 : 32 * (s + 2), xn);
+                        if (more && !(p.dbg & 128)) {
+                            const int cn = sub == 0 ? c0 + 16 : 32 * (s + 2);
+                            load_xop(xh + cn, xl + cn, xn);
+                        }
                         if (diag)
-                            epi_sub_mid_red<MODE, true>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
+                            epi_sub_mid_red<MODE, true>(v, xq, At, r, c0, lane, sub, c_on, k, stg_a, dblk, hl,
                                                         gi, C * kBN, p.dbg & 64);
                         else
-                            epi_sub_mid_red<MODE, false>(v, xq, Xt, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
+                            epi_sub_mid_red<MODE, false>(v, xq, At, r, c0, lane, sub, c_on, k, stg_a, false, hl,
                                                          gi, C * kBN, p.dbg & 64);
-                        if (more) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) xq[j] = xn[j];
-                        }
+                        if (more) xq = xn;
                     } else {
                         double* Dm = p.D ? p.D + (size_t)m * n * n - (ptrdiff_t)p.drow0 * n : nullptr;
+                        XOp xo;
+                        load_xop(xh + c0, xl + c0, xo);
                         if (diag)
-                            epi_sub_last<true>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
+                            epi_sub_last<MODE, true>(v, xo, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq);
                         else
-                            epi_sub_last<false>(v, Xt, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq, mir);
+                            epi_sub_last<MODE, false>(v, xo, At, r, c0, gi, C * kBN, n, c_on, k, Dm, hl, tr, sq, mir);
                     }
                 }
                 const long long t_c1 = (FFG_ROLE_PROF && (p.dbg & 8)) ? clock64() : 0;
@@ -1001,26 +1011,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     __syncwarp();
                     if (lane == 0) {
                         tma_store_2d(&tm.p_hi[nxt], stg, C * kBN + 32 * qc, m * np + R * kBM + 32 * q);
-                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, C * kBN + 32 * qc, m * np + R * kBM + 32 * q);
+                        tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, C * kBN + 32 * qc, m * np + R * kBM + 32 * q);
                         tma_store_commit();
                     }
                     if (!dblk && mir) {
                         if (lane == 0) tma_store_wait_read();
                         __syncwarp();
                         transpose_piece_inplace(stg_a, lane);
-                        if (Tr::kHasLo) transpose_piece_inplace(stg_a + kPieceBytes, lane);
+                        transpose_piece_inplace(stg_a + kPieceBytes, lane);
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
                             tma_store_2d(&tm.p_hi[nxt], stg, R * kBM + 32 * q, m * np + C * kBN + 32 * qc);
-                            if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, R * kBM + 32 * q, m * np + C * kBN + 32 * qc);
+                            tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, R * kBM + 32 * q, m * np + C * kBN + 32 * qc);
                         }
                     }
                 } else if (!last) {
                     if (!dblk && mir) {  // mirrored pieces: warp transpose of the direct pieces
                         __syncwarp();
                         transpose_piece(stg_a, stg_a + 2 * kPieceBytes, lane);
-                        if (Tr::kHasLo) transpose_piece(stg_a + kPieceBytes, stg_a + 3 * kPieceBytes, lane);
+                        transpose_piece(stg_a + kPieceBytes, stg_a + 3 * kPieceBytes, lane);
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -1028,12 +1038,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         const int prow = m * np + R * kBM + 32 * q;   // direct piece origin
                         const int pcol = C * kBN + 32 * qc;
                         tma_store_2d(&tm.p_hi[nxt], stg, pcol, prow);
-                        if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
+                        tma_store_2d(&tm.p_lo[nxt], stg + kPieceBytes, pcol, prow);
                         if (!dblk && mir) {
                             const int mrow = m * np + C * kBN + 32 * qc;
                             const int mcol = R * kBM + 32 * q;
                             tma_store_2d(&tm.p_hi[nxt], stg + 2 * kPieceBytes, mcol, mrow);
-                            if (Tr::kHasLo) tma_store_2d(&tm.p_lo[nxt], stg + 3 * kPieceBytes, mcol, mrow);
+                            tma_store_2d(&tm.p_lo[nxt], stg + 3 * kPieceBytes, mcol, mrow);
                         }
                     }
                 }

@@ -1,7 +1,7 @@
 // MLSP2 density-matrix kernels for sm_100a: shared definitions, K1 and K3.
 //
-//   K1  rescale_tiles        H (fp64) -> X0 = alpha H + gamma I (fp32 master), A1 = d0 X0,
-//                            binary16 hi/lo split of X0 * 2^14 (or bf16), Gershgorin bounds.
+//   K1  rescale_tiles        H (fp64) -> X0 = alpha H + gamma I (fp32), A1 = d0 X0,
+//                            binary16 hi/lo split of X0 * 2^14 (or bf16 hi/lo), Gershgorin bounds.
 //                            One HBM pass; HBM-bound.
 //                            (gershgorin_kernel: bounds only, the spectral_bounds API)
 //   K2  mlsp2_pair_kernel    all recursion layers on tcgen05 CTA pairs (k2_pair.cuh, epilogue in
@@ -11,9 +11,10 @@
 //                            status per matrix.
 //
 // Data layout in HBM (per batch of B matrices, padded size np = ceil(n/128)*128):
-//   X, A  fp32, tile-interleaved 128x128 blocks (xa_tile_base / xa_off), upper blocks live
-//   hi/lo binary16 (or bf16 hi) [2 parities][B][np][np], full symmetric storage:
-//      layer l reads parity l&1 through TMA, writes parity (l+1)&1.
+//   A     fp32, tile-interleaved 128x128 blocks (xa_tile_base / xa_off), the blocks K2 touches
+//   hi/lo binary16 (or bf16) [2 parities][B][np][np], full symmetric storage: layer l reads parity
+//      l&1 (TMA operands, and the epilogue's X_l = (hi + lo) / scale), writes parity (l+1)&1.
+//      There is no fp32 copy of X.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -98,19 +99,17 @@ __device__ __forceinline__ float sr_f16_grid(float r, uint32_t h) {
 template <int MODE>
 __device__ __forceinline__ void split16(float x, uint16_t& hi, uint16_t& lo, bool fixed = false, bool sr = false,
                                         uint32_t h = 0) {
+    // every mode writes lo: K2's epilogue rebuilds X_0 from hi + lo (there is no fp32 copy of X)
     if constexpr (MODE == kModeBF16) {
-        hi = __bfloat16_as_ushort(__float2bfloat16_rn(x));
-        lo = 0;
+        const __nv_bfloat16 hb = __float2bfloat16_rn(x);
+        hi = __bfloat16_as_ushort(hb);
+        lo = __bfloat16_as_ushort(__float2bfloat16_rn(x - __bfloat162float(hb)));
     } else {
         const float xs = x * kHalfScale;
         const __half hh = __float2half_rn((MODE == kModeF32E && fixed) ? rintf(xs * 0.125f) * 8.0f : xs);
         hi = __half_as_ushort(hh);
-        if constexpr (MODE == kModeF32E) {
-            const float r = xs - __half2float(hh);
-            lo = __half_as_ushort(__float2half_rn((FFG_SR_LO && fixed && sr) ? sr_f16_grid(r, h) : r));
-        } else {
-            lo = 0;
-        }
+        const float r = xs - __half2float(hh);
+        lo = __half_as_ushort(__float2half_rn((MODE == kModeF32E && FFG_SR_LO && fixed && sr) ? sr_f16_grid(r, h) : r));
     }
 }
 template <int MODE>
@@ -135,10 +134,9 @@ struct RescaleParams {
     const double* alpha;        // [B] X0 = alpha_m H + gamma_m I
     const double* gamma;        // [B]
     double d0;                  // first accumulator weight: A1 = d0 X0
-    float* X;                   // [B][np][np] tile-interleaved (xa_tile_base)
-    float* A;                   // [B][np][np] tile-interleaved
+    float* A;                   // [B][np][np] tile-interleaved (xa_tile_base)
     uint16_t* hi;               // [B][np][np] parity 0, row-major
-    uint16_t* lo;               // [B][np][np] parity 0 (F32E only)
+    uint16_t* lo;               // [B][np][np] parity 0
     unsigned long long* bounds; // [B][2] ordered keys of (eps_min, eps_max) before widening
     int* flags;                 // [B][2] first bad X_k index: [0] non-finite, [1] half range
     int n, np, mode;
@@ -197,14 +195,13 @@ __global__ void __launch_bounds__(256) gershgorin_kernel(const double* __restric
 
 // K1 (tiled): one CTA = 32 consecutive rows of one matrix (a quarter of block row I), all
 // columns, 128-column tiles.  Each warp streams 4 rows per tile (coalesced double2 loads, 1 KB
-// per row), writes the binary16 split row-major (256 B per row), and stages X0 / A1 in shared
+// per row), writes the binary16 split row-major (256 B per row), and stages A1 = d0 X0 in shared
 // memory so that the block-interleaved [c4][row][4] layout is written with 512-byte contiguous
 // runs (the row-per-lane K1 above stored 2 KB apart per lane).  Blocks K2 never reads
-// (xa_used) skip the X/A stores.  Gershgorin radii: fixed-order per-row warp trees.
+// (xa_used) skip the A stores.  Gershgorin radii: fixed-order per-row warp trees.
 constexpr int kK1Rows = 32;
 constexpr int kK1Pad = 132;  // padded fp32 row stride of the staging tiles (conflict-free float4)
 __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constant__ RescaleParams p) {
-    __shared__ __align__(16) float sX[kK1Rows * kK1Pad];
     __shared__ __align__(16) float sA[kK1Rows * kK1Pad];
     __shared__ double s_lo[8], s_hi[8];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -266,7 +263,6 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
                 float a[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) a[e] = (float)(p.d0 * (double)x[e]);
-                *reinterpret_cast<float4*>(&sX[rl * kK1Pad + 4 * lane]) = make_float4(x[0], x[1], x[2], x[3]);
                 *reinterpret_cast<float4*>(&sA[rl * kK1Pad + 4 * lane]) = make_float4(a[0], a[1], a[2], a[3]);
                 uint16_t hb[4], lb[4];
                 if (p.mode == kModeBF16) {
@@ -291,7 +287,7 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
                 hv.x = hb[0] | ((uint32_t)hb[1] << 16); hv.y = hb[2] | ((uint32_t)hb[3] << 16);
                 lv.x = lb[0] | ((uint32_t)lb[1] << 16); lv.y = lb[2] | ((uint32_t)lb[3] << 16);
                 *reinterpret_cast<uint2*>(p.hi + orow + c0) = hv;
-                if (p.mode == kModeF32E) *reinterpret_cast<uint2*>(p.lo + orow + c0) = lv;
+                *reinterpret_cast<uint2*>(p.lo + orow + c0) = lv;
             }
         }
         if (!p.xa_used || p.xa_used[I * nb + J]) {
@@ -302,11 +298,8 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int rl = r4 + k;
-                const float4 xv = *reinterpret_cast<const float4*>(&sX[rl * kK1Pad + 4 * c4]);
                 const float4 av = *reinterpret_cast<const float4*>(&sA[rl * kK1Pad + 4 * c4]);
-                const size_t o = tb + xa_off(q * kK1Rows + rl, c4);
-                *reinterpret_cast<float4*>(p.X + o) = xv;
-                *reinterpret_cast<float4*>(p.A + o) = av;
+                *reinterpret_cast<float4*>(p.A + tb + xa_off(q * kK1Rows + rl, c4)) = av;
             }
         }
         __syncthreads();
