@@ -20,6 +20,7 @@
 
 #include "fermiforge/ffg.h"
 #include "k2_pair.cuh"
+#include "k2_wide.cuh"
 
 using namespace ffg;
 
@@ -392,6 +393,31 @@ std::vector<uint32_t> pair_table(int nb) {
     return out;
 }
 
+// Wide kernel (k2_wide.cuh) item table: every super-block (S, T), S <= T, of the upper triangle of
+// 256 x 256 super-blocks, row-major (super-rows complete early); entry S | T << 10.
+std::vector<uint32_t> wide_table(int nb) {
+    std::vector<uint32_t> out;
+    const int nsb = nb / 2;
+    for (int S = 0; S < nsb; ++S)
+        for (int T = S; T < nsb; ++T) out.push_back((uint32_t)S | ((uint32_t)T << 10));
+    return out;
+}
+
+// The wide kernel runs a batch when its blocks pair up into 256 x 256 super-blocks (nb even) and the
+// FP32-emulated scheme is the default one (fixed-point exact layers, no per-2-K16 drain layers);
+// the row-block mode keeps the pair kernel.  Default from np >= 1024: below that a matrix has at
+// most 3 super-block items per layer and the pair kernel's finer items keep more CTA pairs busy on
+// the layer chain (measured: 128 x N=512 FP32E 3.8 ms wide vs 3.1 pair; one N=256 0.65 vs 0.39 ms;
+// 16 x N=1024 equal, BF16 -6%; N=2048-8192 BF16 -18..-27%, N=8192 FP32E -12%).  The choice depends
+// only on n and the mode -- never on the batch size -- so a matrix gets the same bits in every batch
+// and through every entry point.  FFG_WIDE=0/1 overrides (read on every call).
+bool use_wide(int mode, int nb, bool rowblock) {
+    const char* e = getenv("FFG_WIDE");
+    const bool ok = nb % 2 == 0 && !rowblock && (mode != kModeF32E || FFG_FIXED_SPLIT);
+    if (e) return ok && atoi(e) != 0;
+    return ok && nb >= 8;
+}
+
 // --------------------------------------------------------------------- small kernels
 __global__ void reset_kernel(unsigned long long* bounds, int* flags, int B,
                              uint32_t* counters = nullptr, int n_counters = 0, uint32_t* products = nullptr) {
@@ -468,7 +494,8 @@ int normal_kstep() {
     static int v = [] {
         const char* e = getenv("FFG_NORMAL_KSTEP");
         const int k = e ? atoi(e) : 8;  // measured: 8 as fast as 16, inside the gates with margin
-        return (k == 4 || k == 16) ? k : 8;
+        // any multiple of 4 (whole K-blocks per chunk; >= 4 nk: one chunk) is accepted for measurement
+        return (k >= 4 && k % 4 == 0) ? k : 8;
     }();
     return v;
 }
@@ -503,7 +530,8 @@ struct DevState {
     bool init = false;
     cudaStream_t lib = nullptr, k2 = nullptr;
     int sms = 148;
-    int cap[3][3] = {{-1, -1, -1}, {-1, -1, -1}, {-1, -1, -1}};  // [mode][V] co-resident CTA pairs
+    int cap[3][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}, {-1, -1, -1, -1}};  // [mode][V] co-resident CTA pairs
+                                                                       // (V = 3: the wide kernel)
     bool watch = false;
 };
 std::mutex g_dev_mu;
@@ -633,6 +661,73 @@ int launch_pair(const PairMaps& maps, const PairParams& pp, int64_t items, cudaS
     return FFG_OK;
 }
 
+// Matrices per L2-resident group of the wide kernel.  Its per-matrix working set is the upper block
+// triangle of two hi/lo parities and of A (~6.75 np^2 bytes, half the pair kernel's), and its items
+// are four blocks each, so a layer needs more matrices to give every CTA pair work beyond the
+// dependency chain: 3 items per resident pair if they fit 1.3x the L2 budget (FFG_GROUP_MB, default
+// 100 MiB), else the budget (measured 16 x N=1024: G = 16 -12% vs 8).  Equal groups as above.
+int wide_group_size(int B, int64_t np, int PT, int resident_pairs) {
+    const char* e = getenv("FFG_GROUP");
+    if (e) return std::max(1, std::min(B, atoi(e)));
+    const char* mb = getenv("FFG_GROUP_MB");
+    const double budget = (mb ? atof(mb) : 100.0) * 1048576.0;
+    const double per = 6.75 * (double)np * np;
+    const int fit = std::max(1, (int)(budget / per));
+    const int fill = (3 * resident_pairs + PT - 1) / PT;
+    const int g = std::max(1, std::min(B, std::max(fit, std::min(fill, (int)(1.3 * fit)))));
+    const int ng = (B + g - 1) / g;
+    return (B + ng - 1) / ng;
+}
+
+// Co-resident CTA pairs of the wide kernel (k2_wide.cuh) on the current device.
+template <int MODE>
+int wide_capacity(int* out) {
+    DevState* d;
+    int rc;
+    if ((rc = dev_state(&d))) return rc;
+    int& max_pairs = d->cap[MODE][3];
+    if (max_pairs < 0) {
+        CK(cudaFuncSetAttribute(mlsp2_wide_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                WideCfg<MODE>::kSmem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * (d->sms / 2));
+        cfg.blockDim = dim3(kWideThreads);
+        cfg.dynamicSmemBytes = WideCfg<MODE>::kSmem;
+        int nc = 0;
+        CK(cudaOccupancyMaxActiveClusters(&nc, mlsp2_wide_kernel<MODE>, &cfg));
+        if (nc < 1) return set_err(FFG_ERR_CUDA, "wide kernel: no co-resident CTA pair fits");
+        max_pairs = nc;
+    }
+    *out = max_pairs;
+    return FFG_OK;
+}
+template <int MODE>
+int launch_wide(const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
+    DevState* d;
+    int cap, rc;
+    if ((rc = wide_capacity<MODE>(&cap))) return rc;
+    if ((rc = dev_state(&d))) return rc;
+    if ((rc = install_watchdog(*d))) return rc;
+    const int pairs = (int)std::min<int64_t>(cap, items);
+    mlsp2_wide_kernel<MODE><<<2 * pairs, kWideThreads, WideCfg<MODE>::kSmem, st>>>(maps, pp);
+    CK(cudaGetLastError());
+    return FFG_OK;
+}
+int wide_capacity_mode(int mode, int* cap) {
+    switch (mode) {
+        case kModeF32E: return wide_capacity<kModeF32E>(cap);
+        case kModeF16: return wide_capacity<kModeF16>(cap);
+        default: return wide_capacity<kModeBF16>(cap);
+    }
+}
+int launch_wide_mode(int mode, const PairMaps& maps, const PairParams& pp, int64_t items, cudaStream_t st) {
+    switch (mode) {
+        case kModeF32E: return launch_wide<kModeF32E>(maps, pp, items, st);
+        case kModeF16: return launch_wide<kModeF16>(maps, pp, items, st);
+        default: return launch_wide<kModeBF16>(maps, pp, items, st);
+    }
+}
+
 // V: 0 streaming, 2 streaming with 16 workers
 template <int V>
 int pair_capacity_mode(int mode, int* cap) {
@@ -722,7 +817,8 @@ std::vector<uint32_t> rowblock_table(int nb, int r0, int r1) {
     return out;
 }
 
-int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L, int rb_rank = 0, int rb_world = 0) {
+int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L, int rb_rank = 0, int rb_world = 0,
+                bool wide = false) {
     size_t dummy = 0;
     int rc;
     const size_t ncnt = (size_t)B * nb * (1 + nb);  // panel counters, then block flags
@@ -730,10 +826,12 @@ int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L, int rb_rank = 0,
         if ((rc = grow(&w.counters, dummy, ncnt))) return rc;
         w.cap_cnt = ncnt;
     }
-    const int64_t pkey = (int64_t)nb | ((int64_t)rb_rank << 24) | ((int64_t)rb_world << 44);
+    const int64_t pkey = (int64_t)nb | ((int64_t)rb_rank << 24) | ((int64_t)rb_world << 44) | ((int64_t)wide << 62);
     if (w.pairs_nb != pkey) {
         std::vector<uint32_t> t;
-        if (rb_world > 0) {
+        if (wide) {
+            t = wide_table(nb);
+        } else if (rb_world > 0) {
             int r0, r1;
             rowblock_rows(nb, rb_rank, rb_world, &r0, &r1);
             t = rowblock_table(nb, r0, r1);
@@ -746,10 +844,15 @@ int ensure_pair(Workspace& w, int B, int64_t np, int nb, int L, int rb_rank = 0,
         }
         CK(cudaMemcpy(w.pairs, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
         std::vector<uint8_t> used((size_t)nb * nb, 0);
-        for (uint32_t e : t) {
-            const int a0 = e & 1023, a1 = (e >> 10) & 1023, sp = (e >> 20) & 1023;
-            used[(size_t)a0 * nb + sp] = 1;
-            if (!((e >> 30) & 1)) used[(size_t)a1 * nb + sp] = 1;
+        if (wide) {  // the upper block triangle (k2_wide.cuh storage)
+            for (int P = 0; P < nb; ++P)
+                for (int Q = P; Q < nb; ++Q) used[(size_t)P * nb + Q] = 1;
+        } else {
+            for (uint32_t e : t) {
+                const int a0 = e & 1023, a1 = (e >> 10) & 1023, sp = (e >> 20) & 1023;
+                used[(size_t)a0 * nb + sp] = 1;
+                if (!((e >> 30) & 1)) used[(size_t)a1 * nb + sp] = 1;
+            }
         }
         if (used.size() > w.cap_used) {
             if ((rc = grow(&w.xa_used, dummy, used.size()))) return rc;
@@ -791,6 +894,7 @@ struct EnqueueCtx {
     int nb = 0;
     int64_t Tpart = 0;
     int exact_layers = 0;
+    bool wide = false;   // k2_wide.cuh kernel (use_wide)
     RegionCheck region{};
 };
 
@@ -802,7 +906,8 @@ int enqueue_k1(Workspace& w, const Job& j, cudaStream_t st, EnqueueCtx& cx) {
     const ffg_model& md = *j.model;
     int rc;
     if ((rc = ensure(w, B, np, 0, true))) return rc;
-    if ((rc = ensure_pair(w, B, np, nb, md.n_layers, j.rb_rank, j.rb_world))) return rc;
+    cx.wide = use_wide(j.mode, nb, j.rb_world > 0);
+    if ((rc = ensure_pair(w, B, np, nb, md.n_layers, j.rb_rank, j.rb_world, cx.wide))) return rc;
     const int64_t Tpart = 2 * (int64_t)w.PT;  // statistics partials per matrix
     if ((size_t)B * Tpart > w.cap_T) {
         size_t dummy = 0;
@@ -931,6 +1036,14 @@ int enqueue_k2(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx
         lp.m0 = m0;
         lp.B = Bl;
         int cap = 0;
+        if (cx.wide) {
+            if ((rc = wide_capacity_mode(j.mode, &cap))) return rc;
+            lp.G = wide_group_size(Bl, cx.np, w.PT, cap);
+            lp.blockdeps = 0;
+            const int64_t items = (int64_t)(l1 - l0) * Bl * w.PT;
+            if ((rc = launch_wide_mode(j.mode, w.pmaps, lp, items, k2s))) return rc;
+            continue;
+        }
         if ((rc = pair_capacity_mode<0>(j.mode, &cap))) return rc;
         lp.G = group_size(Bl, cx.np, w.PT, cap, j.mode);
         const bool s16 = use_s16(j.mode, cx.np, (int64_t)lp.G * w.PT, cap);

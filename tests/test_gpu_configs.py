@@ -107,9 +107,12 @@ def test_config4_all_512_members_vs_fp64_recursion(torch, model, mode):
     assert torch.equal(D1[0], D[137]) and s1[0].tolist() == stats[137].tolist()
 
 
-def test_config5_n16384_single_gpu_vs_fp64_recursion(torch, model):
-    """configs[4] on one GPU: N=16384 (seed 1234, mu=0, kT=0.01), FP32-emulated, whole D."""
+@pytest.mark.parametrize("wide", ["1", "0"])
+def test_config5_n16384_single_gpu_vs_fp64_recursion(torch, model, wide, monkeypatch):
+    """configs[4] on one GPU: N=16384 (seed 1234, mu=0, kT=0.01), FP32-emulated, whole D, with the
+    wide kernel (the default at this size) and with the pair kernel (the row-block shards' kernel)."""
     n = 16384
+    monkeypatch.setenv("FFG_WIDE", wide)
     H = torch.from_numpy(tight_binding(n, seed=1234)).cuda().unsqueeze(0)
     D, stats, status = run_device(torch, H, [0.0], [0.01], model, E.PrecisionMode.MIXED_EMULATED)
     assert status.tolist() == [0]
@@ -117,17 +120,18 @@ def test_config5_n16384_single_gpu_vs_fp64_recursion(torch, model):
     R = DR.density_matrices_f64(H, 0.0, 0.01, model.abcd, model.beta0, model.mu0)
     del H
     mx, fro, tr = DR.errors(D, R)
-    gate(E.PrecisionMode.MIXED_EMULATED, mx, fro, tr, "N=16384")
+    gate(E.PrecisionMode.MIXED_EMULATED, mx, fro, tr, f"N=16384 wide={wide}")
 
 
-def test_config5_rowblock_8_ranks_bit_identical(torch, model):
+def test_config5_rowblock_8_ranks_bit_identical(torch, model, monkeypatch):
     """configs[4] as specified: N=16384 row-block sharded over 8 ranks (each its 2048 rows x all
     columns, operand rows exchanged every layer).  Emulated on one device (8 workspaces, exchange by
-    device copies): the assembled D is bit-identical to the single-GPU D, so the fp64 gate of
-    test_config5_n16384_single_gpu_vs_fp64_recursion carries over."""
+    device copies): the assembled D is bit-identical to the single-GPU D of the same (pair) kernel,
+    so the fp64 gate of test_config5_n16384_single_gpu_vs_fp64_recursion[wide=0] carries over."""
     from paper_2605_08523_b200 import rowblock as RB
     n = 16384
     H = torch.from_numpy(tight_binding(n, seed=1234)).cuda()
+    monkeypatch.setenv("FFG_WIDE", "0")
     D1, _, status = run_device(torch, H.unsqueeze(0), [0.0], [0.01], model, E.PrecisionMode.MIXED_EMULATED)
     assert status.tolist() == [0]
     D, stats, st = RB.rowblock_virtual(H, 0.0, 0.01, model, 8)

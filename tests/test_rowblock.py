@@ -89,16 +89,19 @@ def test_exchange_rows_world2_gloo():
 @pytest.mark.parametrize("n,world,mode", [(2048, 2, "MIXED_EMULATED"), (2048, 4, "MIXED_EMULATED"),
                                           (1000, 2, "MIXED_EMULATED"), (1024, 1, "MIXED_EMULATED"),
                                           (1024, 2, "BF16"), (1024, 4, "FP16")])
-def test_rowblock_virtual_bit_identical_to_single_gpu(n, world, mode):
+def test_rowblock_virtual_bit_identical_to_single_gpu(n, world, mode, monkeypatch):
     """Each rank computes its block rows against all columns (the blocks below the diagonal with
     the swapped cross-term order), exchanging the operand rows every layer: the assembled D equals
-    the single-GPU D bit for bit; the rank-order statistics agree to fp64 summation order."""
+    the single-GPU D of the same (pair) kernel bit for bit; the rank-order statistics agree to fp64
+    summation order.  (Row-block shards run the pair kernel; the single-GPU default for nb even and
+    N >= 1024 is the wide kernel, gated separately in tests/test_gpu_wide.py.)"""
     if not E.device_available():
         pytest.fail("no sm_100 device")
     m = E.load_model("M1500")
     md = E.PrecisionMode[mode]
     H = torch.from_numpy(tight_binding(n, seed=2024)).cuda()
     D1 = torch.empty((1, n, n), dtype=torch.float64, device="cuda")
+    monkeypatch.setenv("FFG_WIDE", "0")
     s1, st1, _ = E.compute_density_matrices_device(H.unsqueeze(0), [0.02], [0.011], m, md, D_dev=D1)
     D, stats, status = RB.rowblock_virtual(H, 0.02, 0.011, m, world, md)
     torch.cuda.synchronize()
@@ -153,5 +156,6 @@ assert abs(stats.trace - s1[0, 0].item()) <= 1e-12 * stats.trace
 dist.destroy_process_group()
 print("NCCL_ROWBLOCK_OK")
 """ % (root, str(_free_port()))
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    env = dict(os.environ, FFG_WIDE="0")  # the single-GPU reference on the row-block shards' kernel
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0 and "NCCL_ROWBLOCK_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
