@@ -100,7 +100,12 @@ def cpu_eigh_sample(n: int, reps: int = 3):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region.
+
+    The query loop (-lms 50) starts before the warm-up and its lines are time-stamped as they arrive
+    (a reader thread), so that sampling is already running when the timed region begins; summary()
+    keeps the samples that arrived between mark("start") and mark("end") (+ one period), or the
+    nearest one when the region is shorter than the sampling period ("window": "nearest")."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -108,39 +113,59 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.p = None
+        self.rows = []
+        self.t = {}
+
+    def _reader(self):
+        for line in self.p.stdout:
+            self.rows.append((time.monotonic(), line))
 
     def __enter__(self):
+        import threading
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._reader, daemon=True).start()
+            t0 = time.monotonic()
+            while not self.rows and time.monotonic() - t0 < 3.0:
+                time.sleep(0.01)
         except Exception:
             self.p = None
         return self
 
+    def mark(self, which: str):
+        self.t[which] = time.monotonic()
+
     def __exit__(self, *exc):
-        self.out = ""
         if self.p is not None:
             self.p.terminate()
             try:
-                self.out, _ = self.p.communicate(timeout=5)
+                self.p.wait(timeout=5)
             except Exception:
                 self.p.kill()
         return False
 
     def summary(self):
-        rows = []
-        for line in (self.out or "").strip().splitlines():
+        parsed = []
+        for ts, line in list(self.rows):
             f = [x.strip() for x in line.split(",")]
             if len(f) >= 9 and f[1].isdigit():
-                rows.append(f)
-        if not rows:
+                parsed.append((ts, f))
+        if not parsed:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        t0, t1 = self.t.get("start", 0.0), self.t.get("end", float("inf")) + 0.06
+        rows = [f for ts, f in parsed if t0 <= ts <= t1]
+        window = "timed region"
+        if not rows:
+            mid = 0.5 * (t0 + min(t1, parsed[-1][0]))
+            rows = [min(parsed, key=lambda x: abs(x[0] - mid))[1]]
+            window = "nearest"
         sm = [int(r[1]) for r in rows]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
         return {"sm_mhz": float(statistics.median(sm)), "sm_max_mhz": int(rows[0][2]),
-                "reasons": reasons, "samples": len(rows),
+                "reasons": reasons, "samples": len(rows), "window": window,
                 "power_w_max": max(float(r[3]) for r in rows if r[3].replace('.', '', 1).isdigit())}
 
 
@@ -311,21 +336,23 @@ def main():
             dist.barrier(device_ids=[local])
 
     # ---------------------------------------------------------------- device-resident timing
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    st = status_dev.cpu().numpy()
-    if (st != 0).any():
-        raise SystemExit(f"rank {rank}: matrices failed with status {st.tolist()}")
-    barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        st = status_dev.cpu().numpy()
+        if (st != 0).any():
+            raise SystemExit(f"rank {rank}: matrices failed with status {st.tolist()}")
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk.mark("start")
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        clk.mark("end")
     barrier()
     t_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -350,11 +377,13 @@ def main():
     peak_tf = pk["bf16_tflops"]
     # DRAM bytes per K2 launch from the committed `ncu --set full` capture of this exact config
     # (an ncu capture cannot run inside the timed bench); null for any other config
+    kernel = E.k2_kernel_name(n, mode)
     traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as f:
             tr = json.load(f)
-        if tr.get("n") == n and tr.get("batch") == B and tr.get("mode") == args.mode:
+        if (tr.get("n") == n and tr.get("batch") == B and tr.get("mode") == args.mode
+                and tr.get("kernel") == kernel):
             traffic = tr.get("dram_bytes_per_launch")
             traffic_src = tr.get("source")
     except Exception:
@@ -416,7 +445,7 @@ def main():
                                 f"{B * n * n * 16 / 2**20:.0f} MiB per GPU"},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_tf, "traffic": traffic, "traffic_source": traffic_src,
-                         "kernel": "mlsp2_pair_kernel (K2, all layers in one launch)",
+                         "kernel": f"{kernel} (K2, all layers in one launch)",
                          "peak_kind": f"{pk_kind} bf16 burst (kernel timed alone at max clock)",
                          "frac_of_sustained_peak": achieved_tf / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
                          "algorithmic_flops_per_launch": flops_per_launch,

@@ -244,6 +244,11 @@ int ffg_solve_chemical_potential(const double* H, int64_t n, double kT, double n
 /* Number of kernels ffg_density_matrices_dev launches for one call (for accounting). */
 int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, int32_t mode);
 
+/* Which recursion kernel (K2) computes matrices of order n in `mode` (the choice depends only on
+ * n and the mode; FFG_WIDE=0/1 overrides): 0 = mlsp2_pair_kernel (256 x 128 pair items),
+ * 1 = mlsp2_wide_kernel (256 x 256 super-block items), negative = unsupported mode / size. */
+int32_t ffg_k2_kernel(int64_t n, int32_t mode);
+
 /* Measurement hooks (bench.py): when enabled, every recursion-kernel (K2) launch is
  * bracketed by CUDA events on its stream; ffg_profile_read() synchronises them and
  * returns the summed device time and launch count since the last read. */

@@ -405,17 +405,18 @@ std::vector<uint32_t> wide_table(int nb) {
 
 // The wide kernel runs a batch when its blocks pair up into 256 x 256 super-blocks (nb even) and the
 // FP32-emulated scheme is the default one (fixed-point exact layers, no per-2-K16 drain layers);
-// the row-block mode keeps the pair kernel.  Default from np >= 1024: below that a matrix has at
-// most 3 super-block items per layer and the pair kernel's finer items keep more CTA pairs busy on
-// the layer chain (measured: 128 x N=512 FP32E 3.8 ms wide vs 3.1 pair; one N=256 0.65 vs 0.39 ms;
-// 16 x N=1024 equal, BF16 -6%; N=2048-8192 BF16 -18..-27%, N=8192 FP32E -12%).  The choice depends
-// only on n and the mode -- never on the batch size -- so a matrix gets the same bits in every batch
-// and through every entry point.  FFG_WIDE=0/1 overrides (read on every call).
+// the row-block mode keeps the pair kernel.  Default from np >= 2048: below that a matrix has at
+// most 10 super-block items per layer and the pair kernel's finer items keep more CTA pairs busy on
+// the layer chain (measured, profiles/r2_configs.json: one N=1024 FP32E 1.11 ms wide vs 0.70 pair,
+// 16 x N=1024 2.29 vs 2.23, 128 x N=512 3.8 vs 3.1; N=4096 BF16 2.46 vs 3.05, N=8192 FP32E 37.9 vs
+// 46.1, N=16384 FP32E 305 vs 407).  The choice depends only on n and the mode -- never on the batch
+// size -- so a matrix gets the same bits in every batch and through every entry point.
+// FFG_WIDE=0/1 overrides (read on every call).
 bool use_wide(int mode, int nb, bool rowblock) {
     const char* e = getenv("FFG_WIDE");
     const bool ok = nb % 2 == 0 && !rowblock && (mode != kModeF32E || FFG_FIXED_SPLIT);
     if (e) return ok && atoi(e) != 0;
-    return ok && nb >= 8;
+    return ok && nb >= 16;
 }
 
 // --------------------------------------------------------------------- small kernels
@@ -1794,6 +1795,13 @@ int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, cons
     j.status_dev = status_dev;
     j.bounds_dev = bounds_dev;
     return enqueue(w, j, st);
+}
+
+int32_t ffg_k2_kernel(int64_t n, int32_t mode) {
+    int m;
+    if (n < 1 || mode_to_internal(mode, &m)) return -1;
+    const int64_t np = (n + kBM - 1) / kBM * kBM;
+    return use_wide(m, (int)(np / kBM), false) ? 1 : 0;
 }
 
 int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, int32_t mode) {

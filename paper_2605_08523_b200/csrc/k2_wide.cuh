@@ -77,41 +77,106 @@ __device__ __forceinline__ void st_v4_f64(double* gp, double a, double b, double
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(gp), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FMUL2 / FADD2): each lane of a pair is rounded exactly like the
+// scalar instruction, so the epilogue's results do not change -- only its issue cost halves.
+__device__ __forceinline__ uint64_t f2u(float2 a) {
+    uint64_t r;
+    memcpy(&r, &a, 8);
+    return r;
+}
+__device__ __forceinline__ float2 u2f(uint64_t r) {
+    float2 a;
+    memcpy(&a, &r, 8);
+    return a;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+
 // 16 consecutive columns (cl .. cl+15 of block (P, Q)) of this thread's row r, mid-recursion layer:
-// X' = a Y + b X (+ c), A += d'X' (+ dc X) by L2 reduction, packed binary16 (bf16) split into hp / lp.
+// X' = a Y + b X (+ c), A += d'X' (+ dc X) by L2 reduction, packed binary16 (bf16) split into hp / lp
+// -- epilogue.cuh's poly_step / acc_term / split2 arithmetic, two elements per instruction.
 // DIAG: only columns >= r are owned (health); the identity term at column r.
 template <int MODE, bool DIAG>
 __device__ __forceinline__ void wide_mid(const uint32_t (&v)[16], const XOp& xq, float* At, int r, int cl,
                                          bool c_on, const EpiCoef& k, EpiHealth& hl, int gi, int gj0,
-                                         uint32_t (&hp)[8], uint32_t (&lp)[8]) {
+                                         uint32_t (&hp)[8], uint32_t (&lp)[8], bool nomem = false) {
+    static_assert(FFG_EPI_EFT == 0, "the packed wide epilogue implements the fused-FMA form");
+    float2 z2 = make_float2(0.0f, 0.0f);
+    float mx = hl.mx;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const float2 x01 = xop_pair<MODE>(xq, 2 * j), x23 = xop_pair<MODE>(xq, 2 * j + 1);
-        float xs[4] = {x01.x, x01.y, x23.x, x23.y};
-        float ts[4];
+        float2 x[2], xn[2], ts[2];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float y = __uint_as_float(v[4 * j + e]);
-            float xn;
+        for (int h = 0; h < 2; ++h) {
+            const int e = 4 * j + 2 * h;  // elements e, e+1
+            x[h] = xop_pair<MODE>(xq, e >> 1);
+            const float2 y = make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+            // poly_step: t = a_lo y + b_lo x (+ c); x' = a_hi y + (b_hi x + t)
+            float2 t = fma2(bc2(k.a_lo), y, mul2(bc2(k.b_lo), x[h]));
             if constexpr (DIAG) {
-                const int col = cl + 4 * j + e;
-                xn = (col == r && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
-                if (col >= r) hl.add(xn);
-            } else {
-                xn = poly_step<false>(y, xs[e], k);
-                hl.add(xn);
+                if (c_on && (r >> 1) == ((cl + e) >> 1)) {  // the identity term at column r
+                    if (cl + e == r) t.x += k.c_hi + k.c_lo;
+                    else t.y += k.c_hi + k.c_lo;
+                }
             }
-            ts[e] = acc_term(xn, k) + fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]);
-            xs[e] = xn;
+            xn[h] = fma2(bc2(k.a_hi), y, fma2(bc2(k.b_hi), x[h], t));
+            // acc_term(x') + dc x
+            const float2 at = fma2(bc2(k.d_hi), xn[h], mul2(bc2(k.d_lo), xn[h]));
+            const float2 dt = fma2(bc2(k.dc_hi), x[h], mul2(bc2(k.dc_lo), x[h]));
+            ts[h] = make_float2(at.x + dt.x, at.y + dt.y);
+            // health of the owned elements
+            if constexpr (DIAG) {
+                const int col = cl + e;
+                if (col >= r) hl.add(xn[h].x);
+                if (col + 1 >= r) hl.add(xn[h].y);
+            } else {
+                z2 = fma2(xn[h], bc2(0.0f), z2);
+                mx = fmaxf(mx, fmaxf(fabsf(xn[h].x), fabsf(xn[h].y)));
+            }
         }
-        if (k.red) red_add_v4(At + xa_off(r, cl / 4 + j), ts[0], ts[1], ts[2], ts[3]);
-        uint32_t hh[4] = {0u, 0u, 0u, 0u};
-        if (MODE == kModeF32E && FFG_SR_LO && k.sr) {
+        if (k.red && !nomem) red_add_v4(At + xa_off(r, cl / 4 + j), ts[0].x, ts[0].y, ts[1].x, ts[1].y);
+        if constexpr (MODE == kModeF32E) {
+            if (FFG_SR_LO && k.sr) {
+                uint32_t hh[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) hh[e] = sr_hash((uint32_t)gi, (uint32_t)(gj0 + cl + 4 * j + e), k.layer);
+                for (int e = 0; e < 4; ++e) hh[e] = sr_hash((uint32_t)gi, (uint32_t)(gj0 + cl + 4 * j + e), k.layer);
+                split2<MODE>(xn[0].x, xn[0].y, hp[2 * j], lp[2 * j], k.fixed, true, hh[0], hh[1]);
+                split2<MODE>(xn[1].x, xn[1].y, hp[2 * j + 1], lp[2 * j + 1], k.fixed, true, hh[2], hh[3]);
+                continue;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                // split2: hi = rn_f16(x 2^14) (fixed: a multiple of 8), lo = rn_f16(x 2^14 - hi)
+                float2 sx = mul2(xn[h], bc2(kHalfScale));
+                float2 hv = sx;
+                if (k.fixed) {
+                    const float2 q8 = mul2(sx, bc2(0.125f));
+                    hv = mul2(make_float2(rintf(q8.x), rintf(q8.y)), bc2(8.0f));
+                }
+                const __half2 hh2 = __floats2half2_rn(hv.x, hv.y);
+                const float2 f = __half22float2(hh2);
+                const float2 rr = fma2(f, bc2(-1.0f), sx);  // exact
+                const __half2 ll2 = __floats2half2_rn(rr.x, rr.y);
+                hp[2 * j + h] = *reinterpret_cast<const uint32_t*>(&hh2);
+                lp[2 * j + h] = *reinterpret_cast<const uint32_t*>(&ll2);
+            }
+        } else {
+            split2<MODE>(xn[0].x, xn[0].y, hp[2 * j], lp[2 * j], false);
+            split2<MODE>(xn[1].x, xn[1].y, hp[2 * j + 1], lp[2 * j + 1], false);
         }
-        split2<MODE>(xs[0], xs[1], hp[2 * j], lp[2 * j], k.fixed, k.sr, hh[0], hh[1]);
-        split2<MODE>(xs[2], xs[3], hp[2 * j + 1], lp[2 * j + 1], k.fixed, k.sr, hh[2], hh[3]);
+    }
+    if constexpr (!DIAG) {
+        hl.z = hl.z + (z2.x + z2.y);  // NaN iff any x' is non-finite
+        hl.mx = mx;
     }
 }
 
@@ -175,7 +240,7 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
     constexpr float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
     const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
     int g = 0;
-    unsigned long long w_chunk = 0, w_epi = 0, w_pub = 0, w_dep = 0, w_drain = 0;
+    unsigned long long w_chunk = 0, w_epi = 0, w_pub = 0, w_dep = 0, w_drain = 0, w_setup = 0;
     for (int item = pair_id; item < total; item += n_pairs) {
         int m, l, pi;
         pair_decode(p, mm, item, m, l, pi);
@@ -204,10 +269,10 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
             __syncwarp();
         }
         // X operands of the next live sub-block in flight (issued before the wait for Y)
-        XOp xa;
+        XOp xa = {};
         int sa = 0;
         while (sa < 4 && !wide_sub_live(redundant, diag, cg, q, sa)) ++sa;
-        if (!kDrain && sa < 4) load_xop(xh + 16 * sa, xl + 16 * sa, xa);
+        if (!kDrain && sa < 4 && !(p.dbg & 128)) load_xop(xh + 16 * sa, xl + 16 * sa, xa);
         int ysl;
         if constexpr (kDrain) {
             const int kst = layer_kstep(l, p.exact_layers, p.semi_layers, p.normal_kstep);
@@ -250,7 +315,7 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
                 for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(yacc[16 * ch + e] * inv_s2);
                 tmem_st_32x32b_x16(tl + ysl * 256 + ch * 16, v);
             }
-            if (sa < 4) load_xop(xh + 16 * sa, xl + 16 * sa, xa);
+            if (sa < 4 && !(p.dbg & 128)) load_xop(xh + 16 * sa, xl + 16 * sa, xa);
             tmem_st_wait();
         } else {
             ysl = g & 1;
@@ -273,8 +338,10 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
         EpiHealth hl;
         double tr = 0.0, sq = 0.0;
         // Y of the next sub-block is requested from TMEM before this one is processed
-        uint32_t vn[16];
-        if (sa < 4) tmem_ld_32x32b_x16(tl + ysl * 256 + 16 * sa, vn);
+        if (FFG_ROLE_PROF) w_setup += (unsigned long long)(clock64() - t_e0);
+        uint32_t vn[16] = {};
+        const bool ldy = !(p.dbg & 512);  // (measurement only: dbg & 512 skips the Y reads)
+        if (sa < 4 && ldy) tmem_ld_32x32b_x16(tl + ysl * 256 + 16 * sa, vn);
 #pragma unroll 1
         for (int sub = sa; sub < 4; ++sub) {  // (sa: first live sub-block; all later ones are live)
             const int cl = 64 * (cg & 1) + 16 * sub;  // first column in block Q
@@ -282,18 +349,18 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
             uint32_t v[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = vn[e];
-            if (sub + 1 < 4) tmem_ld_32x32b_x16(tl + ysl * 256 + 16 * (sub + 1), vn);
+            if (sub + 1 < 4 && ldy) tmem_ld_32x32b_x16(tl + ysl * 256 + 16 * (sub + 1), vn);
             if constexpr (!kDrain && Tr::kScale != 1.0f) {
 #pragma unroll
                 for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * inv_s2);
             }
             const XOp xq = xa;
-            if (sub + 1 < 4) load_xop(xh + 16 * (sub + 1), xl + 16 * (sub + 1), xa);
+            if (sub + 1 < 4 && !(p.dbg & 128)) load_xop(xh + 16 * (sub + 1), xl + 16 * (sub + 1), xa);
             if (!last) {
                 uint32_t hp[8], lp[8];
                 const size_t orow = ((size_t)m * np + gi) * np + (size_t)Q * kBN + cl;
                 if (diag) {
-                    wide_mid<MODE, true>(v, xq, At, r, cl, c_on, k, hl, gi, Q * kBN, hp, lp);
+                    wide_mid<MODE, true>(v, xq, At, r, cl, c_on, k, hl, gi, Q * kBN, hp, lp, p.dbg & 64);
                     const size_t mrow0 = ((size_t)m * np + Q * kBN + cl) * np + (size_t)P * kBM + r;
                     uint16_t* mh = oh + mrow0;
                     uint16_t* ml = ol + mrow0;
@@ -312,9 +379,11 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
                         }
                     }
                 } else {
-                    wide_mid<MODE, false>(v, xq, At, r, cl, c_on, k, hl, gi, Q * kBN, hp, lp);
-                    st_v8(oh + orow, hp);
-                    st_v8(ol + orow, lp);
+                    wide_mid<MODE, false>(v, xq, At, r, cl, c_on, k, hl, gi, Q * kBN, hp, lp, p.dbg & 64);
+                    if (!(p.dbg & 32)) {  // (measurement only: dbg & 32 skips the hi/lo stores)
+                        st_v8(oh + orow, hp);
+                        st_v8(ol + orow, lp);
+                    }
                 }
             } else if (diag) {
                 wide_last<MODE, true>(v, xq, At, r, cl, gi, Q * kBN, n, c_on, k, Dm, hl, tr, sq);
@@ -371,12 +440,15 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
         if (FFG_ROLE_PROF) w_pub += (unsigned long long)(clock64() - t_e1);
     }
     if (FFG_ROLE_PROF && (p.dbg & 8) && lane == 0 && (wk == 0 || wk == 5)) {
-        unsigned long long* o = p.prof + (size_t)blockIdx.x * 16 + (wk == 0 ? 6 : 11);
+        unsigned long long* o = p.prof + (size_t)blockIdx.x * 16 + (wk == 0 ? 6 : 12);
         o[0] = w_chunk;
         o[1] = w_drain - w_chunk;
         o[2] = w_dep;
         o[3] = w_epi;
-        o[4] = w_pub;
+        if (wk == 0) {
+            o[4] = w_pub;
+            o[5] = w_setup;
+        }
     }
 }
 

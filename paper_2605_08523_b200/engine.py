@@ -122,7 +122,7 @@ SYMBOLS = ("ffg_abi_version", "ffg_last_error", "ffg_device_available", "ffg_in_
            "ffg_kernel_launches", "ffg_profile_layers", "ffg_profile_read",
            "ffg_profile_read_ex", "ffg_pair_table", "ffg_release_workspaces",
            "ffg_entropy_trace", "ffg_expectation", "ffg_solve_chemical_potential",
-           "ffg_density_matrices_async", "ffg_wait")
+           "ffg_density_matrices_async", "ffg_wait", "ffg_k2_kernel")
 
 
 @lru_cache(maxsize=None)
@@ -151,6 +151,8 @@ def lib() -> ctypes.CDLL:
                                            ctypes.POINTER(_Model), ctypes.c_int32, ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_void_p]
+    L.ffg_k2_kernel.restype = ctypes.c_int32
+    L.ffg_k2_kernel.argtypes = [ctypes.c_int64, ctypes.c_int32]
     L.ffg_kernel_launches.restype = ctypes.c_int64
     L.ffg_kernel_launches.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(_Model),
                                       ctypes.c_int32]
@@ -457,6 +459,14 @@ def compute_density_matrices_device(H_dev, mu, kT, model: Mlsp2Model,
 def kernel_launches(batch: int, n: int, model: Mlsp2Model, mode=PrecisionMode.MIXED_EMULATED) -> int:
     m = model._c()
     return int(lib().ffg_kernel_launches(batch, n, ctypes.byref(m), int(mode)))
+
+
+def k2_kernel_name(n: int, mode: PrecisionMode = PrecisionMode.MIXED_EMULATED) -> str:
+    """The recursion kernel that computes order-n matrices in `mode` (depends only on n and mode)."""
+    k = int(lib().ffg_k2_kernel(int(n), int(mode)))
+    if k < 0:
+        raise ValidationError(f"no recursion kernel for n={n}, mode={mode}")
+    return ("mlsp2_pair_kernel", "mlsp2_wide_kernel")[k]
 
 
 def profile_layers(enable: bool) -> None:

@@ -72,6 +72,7 @@ def timed(H_dev, mu, kT, model, mode, reps):
     torch.cuda.synchronize()
     ts = []
     with ClockSampler(0) as clk:
+        clk.mark("start")
         t_end = time.perf_counter() + 0.3  # at least ~0.3 s under load so the clock sampler sees it
         while len(ts) < reps or time.perf_counter() < t_end:
             a = torch.cuda.Event(enable_timing=True)
@@ -81,6 +82,7 @@ def timed(H_dev, mu, kT, model, mode, reps):
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) / 1e3)
+        clk.mark("end")
     st = status.cpu().numpy()
     assert (st == 0).all(), st
     return float(np.median(ts)), D, clk.summary()
@@ -115,7 +117,8 @@ def run_case(name, n, B, mode, model, pk, reps, ref_idx=(0,), exact=True, mu=Non
            "matrices_per_s": B / t, "algorithmic_tflops": F / t / 1e12,
            "frac_of_burst_bf16": F / t / 1e12 / pk["bf16_tflops"],
            "frac_of_sustained_bf16": F / t / 1e12 / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
-           "fp32_equiv_gemm_tflops": B * model.layer_count * 2.0 * n ** 3 / t / 1e12, "clocks": clocks}
+           "fp32_equiv_gemm_tflops": B * model.layer_count * 2.0 * n ** 3 / t / 1e12, "clocks": clocks,
+           "k2_kernel": E.k2_kernel_name(n, mode)}
     if cusolver:
         td = cusolver_time(H_dev[0], float(mu[0]), float(kT[0]), torch.float64)
         ts_ = cusolver_time(H_dev[0], float(mu[0]), float(kT[0]), torch.float32)

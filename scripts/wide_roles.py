@@ -16,8 +16,8 @@ from paper_2605_08523_b200.hamiltonians import tight_binding, batch_params
 
 m = E.load_model("M1500")
 names = ["total", "prod_dep", "prod_empty", "mma_full", "mma_slot", "mma_slot2",
-         "w0_chunk", "w0_drainwork", "w0_dep", "w0_epi", "w0_pub",
-         "w5_chunk", "w5_drainwork", "w5_dep", "w5_epi", "w5_pub"]
+         "w0_chunk", "w0_drainwork", "w0_dep", "w0_epi", "w0_pub", "w0_setup",
+         "w5_chunk", "w5_drainwork", "w5_dep", "w5_epi"]
 modes = [E.PrecisionMode[x] for x in os.environ.get("MODES", "MIXED_EMULATED").split(",")]
 for spec in (sys.argv[1:] or ["1024x16", "512x64", "4096x1"]):
     n, B = (int(x) for x in spec.split("x"))

@@ -1,7 +1,7 @@
 """The wide K2 kernel (csrc/k2_wide.cuh: 256 x 256 super-block items, hi/lo blocks stored once and
 read MN-major for the mirrored orientation) against the fp64 recursion (-m gpu).
 
-The default for nb even and N >= 1024 (ffg_capi.cu use_wide); FFG_WIDE=1 forces it below that,
+The default for nb even and N >= 2048 (ffg_capi.cu use_wide); FFG_WIDE=1 forces it below that,
 FFG_WIDE=0 selects the pair kernel.  Gates are SURVEY.md 8(c), unchanged:
 
   MIXED_EMULATED: max|dD| <= 5e-6, ||dD||_F/||D||_F <= 1e-5, |dTr|/Tr <= 1e-6
@@ -58,8 +58,8 @@ def gate(mode, D, R, what):
 @pytest.mark.parametrize("n,B", [(1024, 6), (1000, 3), (1280, 2), (2048, 2)])
 @pytest.mark.parametrize("mode", list(GATE))
 def test_wide_vs_fp64_recursion(torch, model, n, B, mode, monkeypatch):
-    """Default selection at N >= 1024 (nb even; 1000 pads to 1024, 1280 has an odd number of
-    super-rows): every member within the gates, D exactly symmetric, statistics consistent with D."""
+    """Forced at N >= 1000 (nb even; 1000 pads to 1024, 1280 has an odd number of super-rows; the
+    default from N=2048): every member within the gates, D exactly symmetric, statistics consistent."""
     monkeypatch.setenv("FFG_WIDE", "1")
     mu, kT = batch_params(B)
     H = torch.from_numpy(np.stack([tight_binding(n, seed=300 + k) for k in range(B)])).cuda()
@@ -88,16 +88,18 @@ def test_wide_forced_small(torch, model, n, monkeypatch):
 
 
 def test_wide_and_pair_kernels_agree(torch, model, monkeypatch):
-    """Both kernels evaluate the same recursion: at N=1024 their D differ only by rounding (both are
+    """Both kernels evaluate the same recursion: at N=2048 their D differ only by rounding (both are
     within the gates of the fp64 recursion) and the wide kernel is the default there."""
-    mu, kT = batch_params(4)
-    H = torch.from_numpy(np.stack([tight_binding(1024, seed=70 + k) for k in range(4)])).cuda()
+    assert E.k2_kernel_name(2048) == "mlsp2_wide_kernel" and E.k2_kernel_name(1024) == "mlsp2_pair_kernel"
+    assert E.k2_kernel_name(2176) == "mlsp2_pair_kernel"  # nb = 17: no super-block tiling
+    mu, kT = batch_params(2)
+    H = torch.from_numpy(np.stack([tight_binding(2048, seed=70 + k) for k in range(2)])).cuda()
     Dd, _, _ = run(torch, H, mu, kT, model, E.PrecisionMode.MIXED_EMULATED)
     monkeypatch.setenv("FFG_WIDE", "1")
     Dw, _, _ = run(torch, H, mu, kT, model, E.PrecisionMode.MIXED_EMULATED)
     monkeypatch.setenv("FFG_WIDE", "0")
     Dp, _, _ = run(torch, H, mu, kT, model, E.PrecisionMode.MIXED_EMULATED)
-    assert torch.equal(Dd, Dw)              # the default at N=1024 is the wide kernel
+    assert torch.equal(Dd, Dw)              # the default at N=2048 is the wide kernel
     assert (Dw - Dp).abs().max().item() < 5e-6
     assert not torch.equal(Dw, Dp)          # (different accumulation schedules: not the same bits)
 
@@ -105,6 +107,7 @@ def test_wide_and_pair_kernels_agree(torch, model, monkeypatch):
 def test_wide_schedule_invariance(torch, model, monkeypatch):
     """L2 group sizes reorder independent work only: D and the statistics are bit-identical; a
     member computed alone equals the same member inside the batch."""
+    monkeypatch.setenv("FFG_WIDE", "1")
     mu, kT = batch_params(5)
     H = torch.from_numpy(np.stack([tight_binding(1024, seed=90 + k) for k in range(5)])).cuda()
     D0, s0, _ = run(torch, H, mu, kT, model, E.PrecisionMode.MIXED_EMULATED)
@@ -117,9 +120,10 @@ def test_wide_schedule_invariance(torch, model, monkeypatch):
     assert torch.equal(D3[0], D0[3]) and np.array_equal(s3[0], s0[3])
 
 
-def test_wide_out_of_region_member(torch, model):
+def test_wide_out_of_region_member(torch, model, monkeypatch):
     """An out-of-region member of a wide batch issues no products and gets D = NaN; the other members
     are bit-identical to the batch without it."""
+    monkeypatch.setenv("FFG_WIDE", "1")
     mu, kT = batch_params(4)
     kT = np.array(kT)
     H = torch.from_numpy(np.stack([tight_binding(1024, seed=120 + k) for k in range(4)])).cuda()
@@ -134,9 +138,10 @@ def test_wide_out_of_region_member(torch, model):
     assert torch.equal(D[keep], D2) and np.array_equal(stats[keep], s2)
 
 
-def test_wide_provenance_products(model):
+def test_wide_provenance_products(model, monkeypatch):
     """Instrumented product count through the wide kernel: 4 products in the 10
     fixed-point layers, 3 in the others (FP32-emulated), 1 per layer in BF16."""
+    monkeypatch.setenv("FFG_WIDE", "1")
     H = tight_binding(1024, seed=7)
     _, _, pv = E.compute_density_matrix(H, 0.0, 0.01, model, E.PrecisionMode.MIXED_EMULATED)
     assert pv.half_products == 10 * 4 + (model.layer_count - 10) * 3
