@@ -239,6 +239,7 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + 64 * cg;  // + slot * 256
     constexpr float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
     const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
+    const uint32_t slot_full_a = smem_u32(&slot_full[0]);
     int g = 0;
     unsigned long long w_chunk = 0, w_epi = 0, w_pub = 0, w_dep = 0, w_drain = 0, w_setup = 0;
     for (int item = pair_id; item < total; item += n_pairs) {
@@ -283,7 +284,7 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
 #pragma unroll 1
             for (int f = 0; f < chunks; ++f, ++g) {
                 const int sl = g & 1;
-                FFG_TIMED(w_chunk, mbar_wait(&slot_full[sl], (g >> 1) & 1));
+                FFG_TIMED(w_chunk, mbar_wait_at(slot_full_a + 8 * sl, (g >> 1) & 1));
                 tc_fence_after();
                 uint32_t dep = 0;
 #pragma unroll
@@ -319,7 +320,7 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
             tmem_st_wait();
         } else {
             ysl = g & 1;
-            FFG_TIMED(w_chunk, mbar_wait(&slot_full[ysl], (g >> 1) & 1));
+            FFG_TIMED(w_chunk, mbar_wait_at(slot_full_a + 8 * ysl, (g >> 1) & 1));
             tc_fence_after();
             ++g;
         }
@@ -470,6 +471,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
     uint64_t* slot_empty = bars + 2 * S_ + 2;   // [2]  leader: slot read by both CTAs' workers
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S_ + 4);
     double* red = reinterpret_cast<double*>(bars + 2 * S_ + 6);  // [16][2]
+    // 32-bit shared addresses of the barriers (the wait loops keep these, not generic pointers)
+    const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), slot_empty_a = smem_u32(slot_empty);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -508,6 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
     for (int wd = 0; wd < (p.B + 31) / 32; ++wd) mm.nvalid += __popc(valid_bits[wd]);
     mm.remap = mm.nvalid != p.B;
     const int total = (p.l1 - p.l0) * mm.nvalid * p.PT;
+    const uint32_t full_l0 = mapa_shared(full_a, 0);  // the leader's full barriers (TMA complete_tx)
 
     if (warp < kWideWorker0) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kWRegsCtl) : "memory");
@@ -546,8 +550,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
                 const int PA = 2 * S + (int)rank, PB = 2 * T + (int)rank;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % S_;
-                    FFG_TIMED(w_empty, mbar_wait(&empty[s], ((it / S_) & 1) ^ 1));
-                    const uint32_t fbar = mapa_shared(smem_u32(&full[s]), 0);
+                    FFG_TIMED(w_empty, mbar_wait_at(empty_a + 8 * s, ((it / S_) & 1) ^ 1));
+                    const uint32_t fbar = full_l0 + 8 * s;
                     if (leader) mbar_expect_tx(&full[s], bytes);
                     uint8_t* st = smem + s * Cfg::kStageBytes;
                     const int kc = kb >> 1;
@@ -599,7 +603,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
                 uint32_t t_slot = 0, t_hh = 0, t_x = 0;
                 auto open_slot = [&]() {
                     const int sl = g % kSlots;
-                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[sl], ((g / kSlots) & 1) ^ 1));
+                    FFG_TIMED(w_slot, mbar_wait_at(slot_empty_a + 8 * sl, ((g / kSlots) & 1) ^ 1));
                     tc_fence_after();
                     t_slot = tmem + sl * kWideBN;
                 };
@@ -610,8 +614,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
                 };
                 if (kFixed) {
                     const int s0 = g % kSlots, s1 = (g + 1) % kSlots;
-                    FFG_TIMED(w_slot2, mbar_wait(&slot_empty[s0], ((g / kSlots) & 1) ^ 1));
-                    FFG_TIMED(w_slot2, mbar_wait(&slot_empty[s1], (((g + 1) / kSlots) & 1) ^ 1));
+                    FFG_TIMED(w_slot2, mbar_wait_at(slot_empty_a + 8 * s0, ((g / kSlots) & 1) ^ 1));
+                    FFG_TIMED(w_slot2, mbar_wait_at(slot_empty_a + 8 * s1, (((g + 1) / kSlots) & 1) ^ 1));
                     tc_fence_after();
                     t_hh = tmem + s0 * kWideBN;
                     t_x = tmem + s1 * kWideBN;
@@ -620,7 +624,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
                 const int kbc = kDrain && !kFixed ? kst / (kBK / kUK) : 1;  // K-blocks per chunk
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % S_;
-                    FFG_TIMED(w_full, mbar_wait(&full[s], (it / S_) & 1));
+                    FFG_TIMED(w_full, mbar_wait_at(full_a + 8 * s, (it / S_) & 1));
                     tc_fence_after();
                     const uint32_t st = sbase + s * Cfg::kStageBytes;
                     const bool amn = (kb >> 1) <= 2 * S, bmn = (kb >> 1) <= 2 * T;

@@ -81,6 +81,19 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
     const long long t0 = clock64();
     while (!mbar_try_wait_sleep(a, parity)) watchdog_check(t0, 1, a, parity);
 }
+// wait on an mbarrier given by its (precomputed) shared-memory address: a wait loop that holds a
+// generic pointer can make ptxas rematerialise the dynamic shared-memory base on every iteration
+// (the address goes through an opaque move so that it stays in a register across the loop)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+__device__ __forceinline__ void mbar_wait_at(uint32_t a, uint32_t parity) {
+    if (mbar_try_wait(a, parity)) return;
+    a = opaque_u32(a);
+    const long long t0 = clock64();
+    while (!mbar_try_wait(a, parity)) watchdog_check(t0, 2, a, parity);
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait(a, parity)) return;
