@@ -54,7 +54,7 @@ static_assert(WideCfg<kModeBF16>::kSmem <= 227 * 1024, "wide kernel smem");
 // moves registers from the control warpgroup to the workers (per SMSP: one control warp + four workers)
 constexpr int kWideThreads = 640;
 constexpr int kWideWorker0 = 4;
-constexpr int kWRegsCtl = 56, kWRegsWork = 104;
+constexpr int kWRegsCtl = 64, kWRegsWork = 104;
 static_assert(128 * kWRegsCtl + 512 * kWRegsWork <= kWideThreads * 96, "setmaxnreg budget (wide)");
 
 // K-major SW128 operand descriptor (128 rows x 64 K, 8-row atoms at 1024 B); K16 step = +32 B

@@ -6,9 +6,11 @@ Between layers every rank needs the binary16 operands of X_{l+1} for ALL rows: o
 all-gather of the hi and lo arrays (NCCL over NVLink, one process per GPU).  D stays distributed
 as row slabs; Tr D and Tr D^2 are the rank partials summed in rank order (deterministic).
 
-The arithmetic of every block is that of the single-GPU path (the pair table's cross-order bit),
-so the assembled D equals the single-GPU D bit for bit -- the row-block path changes where the
-work runs, never the result.
+The arithmetic of every block is that of the single-GPU pair kernel (the pair table's cross-order
+bit), so the assembled D equals the single-GPU pair-kernel D (FFG_WIDE=0) bit for bit -- the
+row-block path changes where the work runs, never the result.  (The single-GPU default for N >= 2048
+is the wide kernel, k2_wide.cuh: the same recursion with another accumulation schedule, gated
+against the fp64 recursion on its own.)
 
 Drivers:
   rowblock_density_matrix(...)   one rank per process under torch.distributed (NCCL)

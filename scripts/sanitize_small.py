@@ -1,5 +1,6 @@
 """Workload for compute-sanitizer (memcheck / racecheck / synccheck): K1 -> K2 -> K3 at N=256 in
-FP32-emulated and BF16 mode, a 3-matrix batch (8-warp and 16-worker epilogues), one row-block rank.
+FP32-emulated and BF16 mode, a 3-matrix batch (8-warp and 16-worker epilogues), one row-block rank,
+and the wide kernel (forced, FFG_WIDE=1) on a 2-matrix N=512 batch in both modes.
 
     compute-sanitizer --tool racecheck python scripts/sanitize_small.py
 """
@@ -30,3 +31,10 @@ for s16 in ("0", "1"):
 D, stats, status = RB.rowblock_virtual(torch.from_numpy(H).cuda(), 0.0, 0.01, m, 2)
 torch.cuda.synchronize()
 print("rowblock", status, stats.trace, flush=True)
+os.environ["FFG_WIDE"] = "1"
+Hw = torch.from_numpy(np.stack([tight_binding(512, seed=11 + k) for k in range(2)])).cuda()
+Dw = torch.empty_like(Hw)
+for mode in (E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16):
+    s, status, _ = E.compute_density_matrices_device(Hw, mu[:2], kT[:2], m, mode, D_dev=Dw)
+    torch.cuda.synchronize()
+    print("wide", mode.name, status.tolist(), s[:, 0].tolist(), flush=True)

@@ -13,7 +13,7 @@ n, batch, mode = (int(sys.argv[3]), int(sys.argv[4]), sys.argv[5]) if len(sys.ar
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units, vals = rows[0], rows[1], rows[2]
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "sector": 1, "": 1}
 
 
 def get(name):
