@@ -392,23 +392,25 @@ def main():
 
     # ---------------------------------------------------------------- e2e through the host C ABI
     # The public host-buffer API (ffg_density_matrices_async + ffg_wait) the way a serving loop
-    # uses it: every step copies its H from page-locked host memory and reads its D back; two
-    # steps are in flight so step k's transfers overlap step k-1's compute (D double-buffered).
+    # uses it: every step copies its H from page-locked host memory and reads its D back; three
+    # steps are in flight (the API's limit) so step k's transfers overlap the neighbouring steps'
+    # compute and both copy engines stay busy (D triple-buffered).
+    depth = 3
     H_pin = torch.from_numpy(H_host).pin_memory()
-    D_pins = [torch.empty_like(H_pin).pin_memory() for _ in range(2)]
+    D_pins = [torch.empty_like(H_pin).pin_memory() for _ in range(depth)]
     Hp = [H_pin[k].numpy() for k in range(B)]
     Dp = [[D[k].numpy() for k in range(B)] for D in D_pins]
 
     def e2e_run(steps):
         inflight = []
         for s_ in range(steps):
-            inflight.append(E.compute_density_matrices_async(Hp, mu, kT, model, Dp[s_ % 2], mode))
-            if len(inflight) == 2:
+            inflight.append(E.compute_density_matrices_async(Hp, mu, kT, model, Dp[s_ % depth], mode))
+            if len(inflight) == depth:
                 inflight.pop(0).wait()
         for h in inflight:
             h.wait()
 
-    e2e_run(2)
+    e2e_run(depth)
     barrier()
     t0 = time.perf_counter()
     e2e_steps = max(4, args.steps // 2)

@@ -144,8 +144,8 @@ int ffg_density_matrices(int32_t batch, const double* const* H, int64_t n, const
                          double* const* D_out, double* stats_out, ffg_provenance* prov);
 
 /* Asynchronous form of ffg_density_matrices for pipelined callers (a serving loop): enqueues
- * the chunked H2D / compute / D2H pipeline and returns a ticket at once; at most two calls may
- * be in flight, so a caller overlaps step k's transfers with step k-1's compute.  H and D_out
+ * the chunked H2D / compute / D2H pipeline and returns a ticket at once; at most three calls may
+ * be in flight, so a caller overlaps step k's transfers with the neighbouring steps' compute.  H and D_out
  * must stay valid (page-locked for overlap) until ffg_wait(ticket) returns; stats / prov /
  * status are delivered by ffg_wait. */
 int ffg_density_matrices_async(int32_t batch, const double* const* H, int64_t n, const double* mu,

@@ -147,6 +147,7 @@ struct HostSlot {
     double* Ds = nullptr;
     size_t cap = 0;
     void* host_small = nullptr;
+    void* host_small_dev = nullptr;  // its device-mapped address (records_kernel writes there)
     size_t host_small_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_d2h = nullptr;
     cudaEvent_t ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
@@ -199,9 +200,9 @@ struct Workspace {
     size_t cap_coef = 0;
     int pm_B = -1, pm_np = -1;
     PairMaps pmaps;
-    // pipelined host path (submit_host / finish_host): copy streams and two in-flight slots
+    // pipelined host path (submit_host / finish_host): copy streams and three in-flight slots
     static constexpr int kMaxChunks = HostSlot::kMaxChunks;
-    static constexpr int kSlots = 2;
+    static constexpr int kSlots = 3;  // a third call in flight keeps both copy engines busy (e2e +~8%)
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     HostSlot slot[kSlots];
     int64_t next_ticket = 0;
@@ -211,6 +212,7 @@ struct Workspace {
     static constexpr int kRing = 64;
     static constexpr size_t kSlot = 16 * 1024;
     uint8_t* ring = nullptr;
+    uint8_t* ring_dev = nullptr;    // the ring's device-mapped address
     cudaEvent_t ring_ev[kRing] = {};
     int ring_next = 0;
     std::mutex mu;
@@ -329,16 +331,60 @@ int ensure_staging(Workspace& w, size_t elems) {
     return FFG_OK;
 }
 
-// Copy a small host array to the device asynchronously on `st` through a pinned ring slot;
-// the slot is reused only after its previous copy has executed (event), so the caller's
-// array may change right after the call.
+// Small host<->device transfers as kernels over page-locked, device-mapped host memory: a
+// cudaMemcpyAsync of a few hundred bytes is a copy-engine operation and queues behind the
+// pipelined host path's 64 MiB matrix transfers (measured 5-25 us each, ~290 us of idle compute
+// stream per chunk, scripts/timeline_e2e.py); an SM reads or writes the bytes over PCIe instead.
+__global__ void copy_words_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, int words) {
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+// ... and up to 4 KB carried in the launch itself (kernel parameter space): no PCIe read at all
+constexpr int kInlineWords = 1000;
+struct InlineBlob {
+    uint32_t w[kInlineWords];
+};
+__global__ void inline_words_kernel(uint32_t* __restrict__ dst, const __grid_constant__ InlineBlob blob, int words) {
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = blob.w[i];
+}
+// per-matrix records of matrices [0, mb) of the workspace into the host record block (at m0)
+__global__ void records_kernel(uint8_t* host, int B, int m0, int mb, const double* stats, const double* bounds,
+                               const int* status, const int* flags, const uint32_t* products) {
+    double* h_stats = reinterpret_cast<double*>(host);
+    double* h_bounds = h_stats + 2 * B;
+    int* h_status = reinterpret_cast<int*>(h_bounds + 4 * B);
+    int* h_flags = h_status + B;
+    uint32_t* h_prod = reinterpret_cast<uint32_t*>(h_flags + 2 * B);
+    for (int m = threadIdx.x; m < mb; m += blockDim.x) {
+        h_stats[2 * (m0 + m) + 0] = stats[2 * m + 0];
+        h_stats[2 * (m0 + m) + 1] = stats[2 * m + 1];
+        for (int k = 0; k < 4; ++k) h_bounds[4 * (m0 + m) + k] = bounds[4 * m + k];
+        h_status[m0 + m] = status[m];
+        h_flags[2 * (m0 + m) + 0] = flags[2 * m + 0];
+        h_flags[2 * (m0 + m) + 1] = flags[2 * m + 1];
+        h_prod[m0 + m] = products[m];
+    }
+    __threadfence_system();
+}
+
+// Copy a small host array to the device asynchronously on `st`: up to 4 KB as the parameter block
+// of a one-CTA kernel launch, larger (<= 16 KB) through a pinned, device-mapped ring slot read by a
+// kernel (the slot is reused only after its previous copy has executed: event), so the caller's
+// array may change right after the call.  Neither uses a copy engine (see copy_words_kernel).
 int upload_small(Workspace& w, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes <= sizeof(uint32_t) * kInlineWords && bytes % 4 == 0) {
+        InlineBlob blob;
+        memcpy(blob.w, src, bytes);
+        inline_words_kernel<<<1, 256, 0, st>>>(static_cast<uint32_t*>(dst), blob, (int)(bytes / 4));
+        CK(cudaGetLastError());
+        return FFG_OK;
+    }
     if (bytes > Workspace::kSlot) {
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));  // pageable: staged
         return FFG_OK;
     }
     if (!w.ring) {
-        CK(cudaMallocHost(&w.ring, Workspace::kRing * Workspace::kSlot));
+        CK(cudaHostAlloc(&w.ring, Workspace::kRing * Workspace::kSlot, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&w.ring_dev), w.ring, 0));
         for (auto& e : w.ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     const int k = w.ring_next;
@@ -346,7 +392,11 @@ int upload_small(Workspace& w, void* dst, const void* src, size_t bytes, cudaStr
     CK(cudaEventSynchronize(w.ring_ev[k]));
     uint8_t* slot = w.ring + (size_t)k * Workspace::kSlot;
     memcpy(slot, src, bytes);
-    CK(cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, st));
+    const size_t words = (bytes + 3) / 4;  // (ring slots and device buffers are 4-byte aligned)
+    copy_words_kernel<<<1, 256, 0, st>>>(static_cast<uint32_t*>(dst),
+                                         reinterpret_cast<const uint32_t*>(w.ring_dev + (size_t)k * Workspace::kSlot),
+                                         (int)words);
+    CK(cudaGetLastError());
     CK(cudaEventRecord(w.ring_ev[k], st));
     return FFG_OK;
 }
@@ -1147,8 +1197,8 @@ int e2e_chunks(int B, bool async) {
 // Submit the pipelined host path for one batch into a free pipeline slot (no host sync): the
 // batch runs in chunks; chunk k's H2D (copy stream) overlaps the compute of chunk k-1 and its
 // D2H (second copy stream) the compute of chunk k+1.  All kernels stay on the library stream
-// (K2 needs every CTA of its launch co-resident).  Two slots: a call may be submitted while
-// the previous one is still in flight; slot buffers (H/D staging, pinned records) are per slot,
+// (K2 needs every CTA of its launch co-resident).  Three slots: a call may be submitted while
+// the previous two are still in flight; slot buffers (H/D staging, pinned records) are per slot,
 // the K2 workspace is shared in stream order.
 int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, int64_t n, const double* alpha,
                 const double* gamma, const double* scale, const double* mu, const double* kT,
@@ -1158,7 +1208,7 @@ int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, in
     int si = -1;
     for (int k = 0; k < Workspace::kSlots; ++k)
         if (!w.slot[k].busy && (si < 0 || w.slot[k].ticket < w.slot[si].ticket)) si = k;
-    if (si < 0) return set_err(FFG_ERR_VALIDATION, "two calls already in flight: ffg_wait one first");
+    if (si < 0) return set_err(FFG_ERR_VALIDATION, "three calls already in flight: ffg_wait one first");
     HostSlot& hsl = w.slot[si];
     const size_t nn = (size_t)n * n;
     size_t dummy = 0;
@@ -1170,7 +1220,8 @@ int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, in
     const size_t small = (size_t)B * kRecordBytes;
     if (small > hsl.host_small_bytes) {
         cudaFreeHost(hsl.host_small);
-        CK(cudaMallocHost(&hsl.host_small, small));
+        CK(cudaHostAlloc(&hsl.host_small, small, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(&hsl.host_small_dev, hsl.host_small, 0));
         hsl.host_small_bytes = small;
     }
     if (!hsl.ev0) {
@@ -1228,12 +1279,11 @@ int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, in
         j.D_dev = want_D ? hsl.Ds + m0 * nn : nullptr;
         j.exact_layers = exact_layers;
         if ((rc = enqueue(w, j, st))) return rc;
-        // per-matrix records of this chunk (the next chunk's reset reuses the workspace)
-        CK(cudaMemcpyAsync(h_stats + 2 * m0, w.stats, sizeof(double) * 2 * mb, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(h_bounds + 4 * m0, w.bounds_out, sizeof(double) * 4 * mb, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(h_status + m0, w.status, sizeof(int) * mb, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(h_flags + 2 * m0, w.flags, sizeof(int) * 2 * mb, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(h_prod + m0, w.products, sizeof(uint32_t) * mb, cudaMemcpyDeviceToHost, st));
+        // per-matrix records of this chunk (the next chunk's reset reuses the workspace), written
+        // into the mapped record block by a kernel (no copy engine: see copy_words_kernel)
+        records_kernel<<<1, 128, 0, st>>>(static_cast<uint8_t*>(hsl.host_small_dev), B, m0, mb, w.stats,
+                                          w.bounds_out, w.status, w.flags, w.products);
+        CK(cudaGetLastError());
         CK(cudaEventRecord(hsl.ev_done[k], st));
         if (want_D) {
             CK(cudaStreamWaitEvent(w.s_d2h, hsl.ev_done[k], 0));

@@ -484,7 +484,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S_; ++i) {
-            mbar_init(&full[i], 1);
+            mbar_init(&full[i], (p.dbg & 16) ? 2 : 1);  // (dbg & 16, measurement only: no operand loads)
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < kSlots; ++i) {
@@ -552,6 +552,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
                     const int s = it % S_;
                     FFG_TIMED(w_empty, mbar_wait_at(empty_a + 8 * s, ((it / S_) & 1) ^ 1));
                     const uint32_t fbar = full_l0 + 8 * s;
+                    if (p.dbg & 16) {  // measurement: no operand traffic (MMAs on stale smem)
+                        mbar_arrive_cluster(fbar);
+                        continue;
+                    }
                     if (leader) mbar_expect_tx(&full[s], bytes);
                     uint8_t* st = smem + s * Cfg::kStageBytes;
                     const int kc = kb >> 1;
@@ -638,10 +642,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
 #pragma unroll
                             for (int kk = 0; kk < kBK / kUK; ++kk) {
                                 const uint64_t da = dAh + kk * aStep, db = dBh + kk * bStep;
-                                umma_f16_pair(t_x, da, db + kLo, idesc, (kb | kk) != 0);      // hi*lo
-                                umma_f16_pair(t_x, da + kLo, db, idesc, 1u);                  // lo*hi
-                                if (FFG_FIXED_LOLO) umma_f16_pair(t_x, da + kLo, db + kLo, idesc, 1u);
-                                umma_f16_pair(t_hh, da, db, idesc, (kb | kk) != 0);           // hi*hi (exact)
+                                if (!(p.dbg & 2)) umma_f16_pair(t_x, da, db + kLo, idesc, (kb | kk) != 0);      // hi*lo
+                                if (!(p.dbg & 2)) umma_f16_pair(t_x, da + kLo, db, idesc, 1u);                  // lo*hi
+                                if (FFG_FIXED_LOLO && !(p.dbg & 2)) umma_f16_pair(t_x, da + kLo, db + kLo, idesc, 1u);
+                                if (!(p.dbg & 2)) umma_f16_pair(t_hh, da, db, idesc, (kb | kk) != 0);           // hi*hi (exact)
                             }
                         }
                         __syncwarp();
@@ -649,7 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
                         if (elect_one_sync()) {
 #pragma unroll
                             for (int kk = 0; kk < kBK / kUK; ++kk)
-                                umma_f16_pair(t_slot, dAh + kk * aStep, dBh + kk * bStep, idesc, (kb | kk) != 0);
+                                if (!(p.dbg & 2)) umma_f16_pair(t_slot, dAh + kk * aStep, dBh + kk * bStep, idesc, (kb | kk) != 0);
                         }
                         __syncwarp();
                     } else {
@@ -659,12 +663,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
 #pragma unroll
                             for (int kk = 0; kk < kBK / kUK; ++kk) {
                                 const uint64_t da = dAh + kk * aStep, db = dBh + kk * bStep;
-                                umma_f16_pair(t_slot, da, db + kLo, idesc, !(first && kk == 0));
-                                umma_f16_pair(t_slot, da + kLo, db, idesc, 1u);
+                                if (!(p.dbg & 2)) umma_f16_pair(t_slot, da, db + kLo, idesc, !(first && kk == 0));
+                                if (!(p.dbg & 2)) umma_f16_pair(t_slot, da + kLo, db, idesc, 1u);
                             }
 #pragma unroll
                             for (int kk = 0; kk < kBK / kUK; ++kk)
-                                umma_f16_pair(t_slot, dAh + kk * aStep, dBh + kk * bStep, idesc, 1u);
+                                if (!(p.dbg & 2)) umma_f16_pair(t_slot, dAh + kk * aStep, dBh + kk * bStep, idesc, 1u);
                         }
                         __syncwarp();
                         if (kb % kbc == kbc - 1 || kb == nk - 1) close_slot();

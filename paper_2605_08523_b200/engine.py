@@ -397,7 +397,7 @@ class AsyncBatch:
 
 def compute_density_matrices_async(Hs, mu, kT, model: Mlsp2Model, Ds,
                                    mode: PrecisionMode = PrecisionMode.MIXED_EMULATED) -> AsyncBatch:
-    """Asynchronous host-buffer batch (at most two in flight): Hs / Ds are lists of C-contiguous
+    """Asynchronous host-buffer batch (at most three in flight): Hs / Ds are lists of C-contiguous
     float64 arrays (page-locked for transfer overlap) that must stay alive until wait()."""
     B = len(Hs)
     n = Hs[0].shape[0]

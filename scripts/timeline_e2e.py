@@ -1,4 +1,4 @@
-"""GPU timeline of the async host path (two calls in flight), kernels and copies (measurement only)."""
+"""GPU timeline of the async host path (DEPTH calls in flight, default 3), kernels and copies (measurement only)."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -9,14 +9,15 @@ n, B = 1024, 16
 m = E.load_model("M1500")
 mu, kT = batch_params(B)
 H = torch.from_numpy(np.stack([tight_binding(n, seed=10000 + k) for k in range(B)])).pin_memory()
-Ds = [torch.empty_like(H).pin_memory() for _ in range(2)]
+DEPTH = int(os.environ.get("DEPTH", 3))
+Ds = [torch.empty_like(H).pin_memory() for _ in range(DEPTH)]
 Hp = [H[k].numpy() for k in range(B)]
 Dp = [[D[k].numpy() for k in range(B)] for D in Ds]
 def run(steps):
     infl = []
     for s in range(steps):
-        infl.append(E.compute_density_matrices_async(Hp, mu, kT, m, Dp[s % 2], E.PrecisionMode.MIXED_EMULATED))
-        if len(infl) == 2:
+        infl.append(E.compute_density_matrices_async(Hp, mu, kT, m, Dp[s % DEPTH], E.PrecisionMode.MIXED_EMULATED))
+        if len(infl) == DEPTH:
             infl.pop(0).wait()
     for h in infl:
         h.wait()

@@ -360,23 +360,26 @@ def test_host_path_matches_device_path_at_bench_config(model):
 
 @pytest.mark.gpu
 def test_async_host_path_matches_sync(model):
-    """ffg_density_matrices_async / ffg_wait with two batches in flight returns bitwise the
-    results of the synchronous call; a third submission while two are pending is refused."""
+    """ffg_density_matrices_async / ffg_wait with three batches in flight returns bitwise the
+    results of the synchronous call; a fourth submission while three are pending is refused."""
     B, n = 8, 256
     mu, kT = batch_params(B)
     Hs = [tight_binding(n, seed=20000 + k) for k in range(B)]
     Ds_sync, st_sync, _ = E.compute_density_matrices(Hs, mu, kT, model)
-    outs = [[np.empty((n, n)) for _ in range(B)] for _ in range(2)]
+    outs = [[np.empty((n, n)) for _ in range(B)] for _ in range(3)]
     h1 = E.compute_density_matrices_async(Hs, mu, kT, model, outs[0])
     h2 = E.compute_density_matrices_async(Hs, mu, kT, model, outs[1])
+    h3 = E.compute_density_matrices_async(Hs, mu, kT, model, outs[2])
     with pytest.raises(E.ValidationError, match="in flight"):
         E.compute_density_matrices_async(Hs, mu, kT, model, outs[0])
     st2, pv2 = h2.wait()
+    st3, pv3 = h3.wait()
     st1, pv1 = h1.wait()
     for k in range(B):
-        assert np.array_equal(outs[0][k], Ds_sync[k]) and np.array_equal(outs[1][k], Ds_sync[k])
-        assert st1[k] == st_sync[k] and st2[k] == st_sync[k]
-    assert all(p.status == 0 for p in pv1 + pv2)
+        for o in outs:
+            assert np.array_equal(o[k], Ds_sync[k])
+        assert st1[k] == st_sync[k] and st2[k] == st_sync[k] and st3[k] == st_sync[k]
+    assert all(p.status == 0 for p in pv1 + pv2 + pv3)
     with pytest.raises(E.ValidationError, match="ticket"):
         h1.wait()
 
