@@ -247,6 +247,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + 32 * c;  // + slot * 128
     const float inv_s2 = 1.0f / (Tr::kScale * Tr::kScale);
     const uint32_t slot_empty_l0 = mapa_shared(smem_u32(&slot_empty[0]), 0);  // leader's
+    const uint32_t slot_full_a = smem_u32(&slot_full[0]);
     uint8_t* stg = staging + wk * 2 * kPieceBytes;  // direct hi piece, lo piece (mirrors in place)
     const uint32_t stg_a = smem_u32(stg);
     int g = 0;
@@ -260,7 +261,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
 #pragma unroll 1
         for (int f = 0; f < chunks; ++f, ++g) {
             const int sl = g & 3;
-            mbar_wait(&slot_full[sl], (g >> 2) & 1);
+            mbar_wait_at(slot_full_a + 8 * sl, (g >> 2) & 1);
             tc_fence_after();
             uint32_t v[32];
             tmem_ld_32x32b_x16(tl + sl * 128, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
@@ -460,6 +461,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                                            //      two groups: [g] = group g drained an item
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 12);
     double* red = reinterpret_cast<double*>(bars + 2 * S + 14);  // [16][2]
+    // 32-bit shared addresses of the barriers (wait loops on generic pointers made ptxas
+    // rematerialise the dynamic shared-memory base, with a spill, on every iteration)
+    const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), slot_full_a = smem_u32(slot_full),
+                   slot_empty_a = smem_u32(slot_empty), y_full_a = smem_u32(y_full);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -592,7 +597,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         if (FFG_ROLE_PROF && (p.dbg & 8)) w_dep += (unsigned long long)(clock64() - t0);
                         fence_proxy_async_global();
                     }
-                    FFG_TIMED(w_empty, mbar_wait(&empty[s], ((it / S) & 1) ^ 1));
+                    FFG_TIMED(w_empty, mbar_wait_at(empty_a + 8 * s, ((it / S) & 1) ^ 1));
                     const uint32_t fbar = mapa_shared(smem_u32(&full[s]), 0);
                     if (p.dbg & 16) {  // measurement: no operand traffic (MMAs on stale smem);
                         mbar_arrive_cluster(fbar);  // both CTAs arrive, keeping them in step
@@ -645,7 +650,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 uint32_t t_slot = 0;
                 auto open_slot = [&]() {
                     const int sl = g % kSlots;
-                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[sl], ((g / kSlots) & 1) ^ 1));
+                    FFG_TIMED(w_slot, mbar_wait_at(slot_empty_a + 8 * sl, ((g / kSlots) & 1) ^ 1));
                     tc_fence_after();
                     t_slot = tmem + sl * 128;
                 };
@@ -666,8 +671,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 uint32_t t_hh = 0, t_x = 0;
                 if (kFixed) {
                     const int s0 = g % kSlots, s1 = (g + 1) % kSlots;
-                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[s0], ((g / kSlots) & 1) ^ 1));
-                    FFG_TIMED(w_slot, mbar_wait(&slot_empty[s1], (((g + 1) / kSlots) & 1) ^ 1));
+                    FFG_TIMED(w_slot, mbar_wait_at(slot_empty_a + 8 * s0, ((g / kSlots) & 1) ^ 1));
+                    FFG_TIMED(w_slot, mbar_wait_at(slot_empty_a + 8 * s1, (((g + 1) / kSlots) & 1) ^ 1));
                     tc_fence_after();
                     t_hh = tmem + s0 * 128;
                     t_x = tmem + s1 * 128;
@@ -675,7 +680,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 if (!kDrain) open_slot();
                 for (int kb = 0; kb < ((p.dbg & 2) ? 0 : nk); ++kb, ++it) {
                     const int s = it % S;
-                    FFG_TIMED(w_full, mbar_wait(&full[s], (it / S) & 1));
+                    FFG_TIMED(w_full, mbar_wait_at(full_a + 8 * s, (it / S) & 1));
                     tc_fence_after();
                     const uint64_t sb = desc0 + (uint64_t)((s * Cfg::kStageBytes) >> 4);
                     if (kFixed) {
@@ -800,9 +805,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 for (int f = 0; f < chunks; ++f, ++g) {
                     const int sl = g & 3;
                     #if FFG_DRAIN_SPIN
-                    FFG_TIMED_DRAIN(w_sf, mbar_wait(&slot_full[sl], (g >> 2) & 1));
+                    FFG_TIMED_DRAIN(w_sf, mbar_wait_at(slot_full_a + 8 * sl, (g >> 2) & 1));
     #else
-                    FFG_TIMED_DRAIN(w_sf, mbar_wait_sleep(&slot_full[sl], (g >> 2) & 1));
+                    FFG_TIMED_DRAIN(w_sf, mbar_wait_at_sleep(slot_full_a + 8 * sl, (g >> 2) & 1));
     #endif
                     tc_fence_after();
                     const bool lastc = f == chunks - 1;
@@ -927,12 +932,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             if constexpr (!kDrain) {
                 // single-product modes: the slot holds the whole-K accumulator, read directly
                 // (no drain pass); the 1/scale^2 is applied as it is loaded
-                FFG_TIMED(w_y, mbar_wait_sleep(&slot_full[ysl], ((g - 1) >> 2) & 1));
+                FFG_TIMED(w_y, mbar_wait_at_sleep(slot_full_a + 8 * ysl, ((g - 1) >> 2) & 1));
             } else {
 #if FFG_EPI_SPIN
-                FFG_TIMED(w_y, mbar_wait(&y_full[ysl], (yph >> ysl) & 1));
+                FFG_TIMED(w_y, mbar_wait_at(y_full_a + 8 * ysl, (yph >> ysl) & 1));
 #else
-                FFG_TIMED(w_y, mbar_wait_sleep(&y_full[ysl], (yph >> ysl) & 1));
+                FFG_TIMED(w_y, mbar_wait_at_sleep(y_full_a + 8 * ysl, (yph >> ysl) & 1));
 #endif
                 yph ^= 1u << ysl;
             }

@@ -94,6 +94,12 @@ __device__ __forceinline__ void mbar_wait_at(uint32_t a, uint32_t parity) {
     const long long t0 = clock64();
     while (!mbar_try_wait(a, parity)) watchdog_check(t0, 2, a, parity);
 }
+__device__ __forceinline__ void mbar_wait_at_sleep(uint32_t a, uint32_t parity) {
+    if (mbar_try_wait_sleep(a, parity)) return;
+    a = opaque_u32(a);
+    const long long t0 = clock64();
+    while (!mbar_try_wait_sleep(a, parity)) watchdog_check(t0, 1, a, parity);
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait(a, parity)) return;
