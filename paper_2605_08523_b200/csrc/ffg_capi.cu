@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "fermiforge/ffg.h"
 #include "k2_pair.cuh"
 #include "k2_wide.cuh"
@@ -27,6 +29,15 @@ using namespace ffg;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range over an entry point or a pipeline stage (header-only NVTX3: a no-op unless a tool such
+// as Nsight Systems is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int set_err(int code, const char* fmt, ...) {
     char buf[1024];
@@ -950,6 +961,7 @@ struct EnqueueCtx {
 };
 
 int enqueue_k1(Workspace& w, const Job& j, cudaStream_t st, EnqueueCtx& cx) {
+    NvtxRange nv("ffg K1 enqueue (uploads, reset, rescale)");
     const int B = j.B;
     const int64_t n = j.n;
     const int64_t np = (n + kBM - 1) / kBM * kBM;
@@ -1022,6 +1034,7 @@ int enqueue_k1(Workspace& w, const Job& j, cudaStream_t st, EnqueueCtx& cx) {
 
 // K2 over layers [l0, l1): forked from `st` to the device's K2 stream (DevState) and joined back.
 int enqueue_k2(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx, int l0, int l1) {
+    NvtxRange nv("ffg K2 enqueue (recursion layers)");
     const int B = j.B;
     const int64_t n = j.n;
     const ffg_model& md = *j.model;
@@ -1119,6 +1132,7 @@ int enqueue_k2(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx
 // K3: statistics, validity status, NaN D for out-of-region matrices (d_rows: rows of D per matrix
 // the kernel owns -- n, or a row-block rank's rows).
 int enqueue_k3(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx, int64_t d_rows) {
+    NvtxRange nv("ffg K3 enqueue (statistics, status)");
     FinalizeParams fp{};
     fp.partials = w.partials;
     fp.flags = w.flags;
@@ -1491,6 +1505,7 @@ int ffg_in_region_of_validity(double beta_prime, double mu_prime, double beta0, 
 }
 
 int ffg_spectral_bounds(const double* H, int64_t n, double* eps_min, double* eps_max) {
+    NvtxRange nv("ffg_spectral_bounds");
     int rc, dev;
     if ((rc = validate_n(n))) return rc;
     if (!H || !eps_min || !eps_max) return set_err(FFG_ERR_VALIDATION, "null argument");
@@ -1518,6 +1533,7 @@ int ffg_spectral_bounds(const double* H, int64_t n, double* eps_min, double* eps
 
 int ffg_apply_model(const double* H0, int64_t n, const ffg_model* model, int32_t mode,
                     double* D_out, ffg_provenance* prov) {
+    NvtxRange nv("ffg_apply_model");
     const double alpha = -1.0, gamma = 1.0;  // X0 = I - H0 (scalar_models.cpp:333)
     double* Dp[1] = {D_out};
     return run_host(1, &H0, n, &alpha, &gamma, nullptr, nullptr, nullptr, model, mode, Dp,
@@ -1533,6 +1549,7 @@ int ffg_apply_model(const double* H0, int64_t n, const ffg_model* model, int32_t
 // products hi*hi + hi*lo + lo*hi of Eq. 48, i.e. 1.5 full-GEMM equivalents against SPEC's "2 half
 // multiplications".  |X| beyond the binary16 range -> FFG_ERR_HALF_RANGE (overflow error).
 int ffg_mixed_square(const float* X, int64_t n, float* Y_out) {
+    NvtxRange nv("ffg_mixed_square");
     int rc;
     if ((rc = validate_n(n))) return rc;
     if (!X || !Y_out) return set_err(FFG_ERR_VALIDATION, "null argument");
@@ -1565,6 +1582,7 @@ int ffg_mixed_square(const float* X, int64_t n, float* Y_out) {
 }
 
 int ffg_expectation(const double* D, const double* A, int64_t n, double* out) {
+    NvtxRange nv("ffg_expectation");
     int rc, dev;
     if ((rc = validate_n(n))) return rc;
     if (!D || !A || !out) return set_err(FFG_ERR_VALIDATION, "null argument");
@@ -1600,6 +1618,7 @@ int ffg_expectation(const double* D, const double* A, int64_t n, double* out) {
 
 int ffg_entropy_trace(const double* H, int64_t n, double mu, double kT, const ffg_entropy_model* em,
                       int32_t mode_api, double* entropy_trace, ffg_provenance* prov) {
+    NvtxRange nv("ffg_entropy_trace");
     int rc, dev, mode;
     if (!em) return set_err(FFG_ERR_VALIDATION, "entropy model is null");
     if ((rc = validate_model(&em->inner))) return rc;
@@ -1635,6 +1654,7 @@ int ffg_entropy_trace(const double* H, int64_t n, double mu, double kT, const ff
 int ffg_solve_chemical_potential(const double* H, int64_t n, double kT, double n_occ, double mu_guess,
                                  const ffg_model* md, int32_t mode_api, double tol, int32_t max_iter,
                                  double* D_out, double* stats_out, double* history, ffg_mu_report* report) {
+    NvtxRange nv("ffg_solve_chemical_potential");
     int rc, dev, mode;
     if ((rc = validate_model(md))) return rc;
     if ((rc = mode_to_internal(mode_api, &mode))) return rc;
@@ -1730,6 +1750,7 @@ int ffg_solve_chemical_potential(const double* H, int64_t n, double kT, double n
 }
 
 int ffg_density_statistics(const double* D, int64_t n, double* stats_out) {
+    NvtxRange nv("ffg_density_statistics");
     int rc, dev;
     if ((rc = validate_n(n))) return rc;
     if (!D || !stats_out) return set_err(FFG_ERR_VALIDATION, "null argument");
@@ -1762,6 +1783,7 @@ int ffg_density_statistics(const double* D, int64_t n, double* stats_out) {
 
 int ffg_density_matrix(const double* H, int64_t n, double mu, double kT, const ffg_model* model,
                        int32_t mode, double* D_out, double* stats_out, ffg_provenance* prov) {
+    NvtxRange nv("ffg_density_matrix");
     double* Dp[1] = {D_out};
     return ffg_density_matrices(1, &H, n, &mu, &kT, model, mode, Dp, stats_out, prov);
 }
@@ -1769,6 +1791,7 @@ int ffg_density_matrix(const double* H, int64_t n, double mu, double kT, const f
 int ffg_density_matrices(int32_t batch, const double* const* H, int64_t n, const double* mu,
                          const double* kT, const ffg_model* model, int32_t mode,
                          double* const* D_out, double* stats_out, ffg_provenance* prov) {
+    NvtxRange nv("ffg_density_matrices");
     int rc;
     if (batch < 1) return set_err(FFG_ERR_DIMENSION, "batch must be >= 1");
     if (!H) return set_err(FFG_ERR_VALIDATION, "H is null");
@@ -1783,6 +1806,7 @@ int ffg_density_matrices(int32_t batch, const double* const* H, int64_t n, const
 int ffg_density_matrices_async(int32_t batch, const double* const* H, int64_t n, const double* mu,
                                const double* kT, const ffg_model* model, int32_t mode_api,
                                double* const* D_out, int64_t* ticket) {
+    NvtxRange nv("ffg_density_matrices_async");
     int rc, dev, mode;
     if (!H || !ticket) return set_err(FFG_ERR_VALIDATION, "H / ticket is null");
     if ((rc = validate_host_call(batch, H, n, model, mode_api, &mode, &dev))) return rc;
@@ -1802,6 +1826,7 @@ int ffg_density_matrices_async(int32_t batch, const double* const* H, int64_t n,
 }
 
 int ffg_wait(int64_t ticket, double* stats_out, ffg_provenance* prov) {
+    NvtxRange nv("ffg_wait");
     int rc, dev;
     if ((rc = check_device(&dev))) return rc;
     cudaStream_t st = lib_stream();
@@ -1817,6 +1842,7 @@ int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, cons
                              const double* kT, const ffg_model* model, int32_t mode,
                              double* D_dev, double* stats_dev, int32_t* status_dev,
                              double* bounds_dev, void* stream) {
+    NvtxRange nv("ffg_density_matrices_dev");
     int rc, dev, imode;
     if (batch < 1) return set_err(FFG_ERR_DIMENSION, "batch must be >= 1");
     if (!H_dev) return set_err(FFG_ERR_VALIDATION, "H_dev is null");
@@ -1918,6 +1944,7 @@ int32_t ffg_rowblock_table(int32_t nb, int32_t rank, int32_t world, uint32_t* ou
 
 int ffg_rowblock_begin(const double* H_dev, int64_t n, double mu, double kT, const ffg_model* model,
                        int32_t mode_api, int32_t rank, int32_t world, void* stream, ffg_rowblock** handle) {
+    NvtxRange nv("ffg_rowblock_begin");
     int rc, dev, mode;
     if (!H_dev || !handle) return set_err(FFG_ERR_VALIDATION, "H_dev / handle is null");
     *handle = nullptr;
@@ -1993,6 +2020,7 @@ int ffg_rowblock_operands(ffg_rowblock* h, int32_t parity, void** hi, void** lo)
 }
 
 int ffg_rowblock_layer(ffg_rowblock* h, int32_t layer, double* D_rows, void* stream) {
+    NvtxRange nv("ffg_rowblock_layer");
     if (!h) return set_err(FFG_ERR_VALIDATION, "null handle");
     RowBlockState& S = h->s;
     if (layer != S.next_layer || layer >= S.model.n_layers)
@@ -2016,6 +2044,7 @@ int ffg_rowblock_layer(ffg_rowblock* h, int32_t layer, double* D_rows, void* str
 
 int ffg_rowblock_end(ffg_rowblock* h, double* partial_stats, int32_t* status, ffg_provenance* prov,
                      void* stream) {
+    NvtxRange nv("ffg_rowblock_end");
     if (!h) return set_err(FFG_ERR_VALIDATION, "null handle");
     RowBlockState& S = h->s;
     Workspace& w = *S.w;

@@ -41,6 +41,19 @@ def test_binary_contains_tcgen05_and_tma():
     assert "HMMA" not in re.sub(r"UTCHMMA", "", sass), "legacy mma.sync found"
 
 
+def test_binary_has_both_k2_kernels_and_nvtx_ranges():
+    """Both recursion kernels are in the product library (the wide one with MN-major operand reads:
+    its instruction descriptors are built at run time, so only the kernel symbols are checked), and
+    the entry points carry NVTX ranges (header-only NVTX3: no link dependency)."""
+    syms = subprocess.run(["cuobjdump", "-symbols", E.LIB_PATH], capture_output=True, text=True).stdout
+    assert "mlsp2_pair_kernel" in syms and "mlsp2_wide_kernel" in syms
+    blob = open(E.LIB_PATH, "rb").read()
+    for name in (b"ffg_density_matrices_dev", b"ffg K2 enqueue (recursion layers)", b"ffg_rowblock_layer"):
+        assert name + b"\0" in blob, name
+    deps = subprocess.run(["ldd", E.LIB_PATH], capture_output=True, text=True).stdout
+    assert "nvToolsExt" not in deps
+
+
 def test_validation_mirrors_reference():
     m = E.load_model("M1500")
     H = np.eye(8)
