@@ -1027,7 +1027,7 @@ int enqueue_k1(Workspace& w, const Job& j, cudaStream_t st, EnqueueCtx& cx) {
     rp.fixed = (FFG_FIXED_SPLIT && j.mode == kModeF32E && cx.exact_layers > 0) ? 1 : 0;
     rp.sr = (rp.fixed && sr_layers() > 0) ? 1 : 0;
     rp.xa_used = w.xa_used;   // X/A stores only for the blocks K2 reads
-    rescale_tiles_kernel<<<dim3((unsigned)(np / kK1Rows), (unsigned)B), 256, 0, st>>>(rp);
+    rescale_tiles_kernel<kK1Warps><<<dim3((unsigned)(np / kK1Rows), (unsigned)B), 32 * kK1Warps, 0, st>>>(rp);
     CK(cudaGetLastError());
     return FFG_OK;
 }

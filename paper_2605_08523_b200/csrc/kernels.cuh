@@ -199,16 +199,25 @@ __global__ void __launch_bounds__(256) gershgorin_kernel(const double* __restric
 // memory so that the block-interleaved [c4][row][4] layout is written with 512-byte contiguous
 // runs (the row-per-lane K1 above stored 2 KB apart per lane).  Blocks K2 never reads
 // (xa_used) skip the A stores.  Gershgorin radii: fixed-order per-row warp trees.
-constexpr int kK1Rows = 32;
+// (template: WARPS warps = 4 WARPS rows per CTA.  Measured under ncu, 16 x N=1024: 8 warps / 32 rows
+// 97 us (512 CTAs: 68 SMs with four, 80 with three), 4 warps 79 us, 2 warps / 8 rows 74 us (2048 CTAs,
+// ~14 per SM, one wave))
+#ifndef FFG_K1_WARPS
+#define FFG_K1_WARPS 2
+#endif
+constexpr int kK1Warps = FFG_K1_WARPS;
+constexpr int kK1Rows = 4 * kK1Warps;
 constexpr int kK1Pad = 132;  // padded fp32 row stride of the staging tiles (conflict-free float4)
-__global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constant__ RescaleParams p) {
-    __shared__ __align__(16) float sA[kK1Rows * kK1Pad];
-    __shared__ double s_lo[8], s_hi[8];
+template <int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) rescale_tiles_kernel(const __grid_constant__ RescaleParams p) {
+    constexpr int kRows = 4 * WARPS;
+    __shared__ __align__(16) float sA[kRows * kK1Pad];
+    __shared__ double s_lo[WARPS], s_hi[WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.y;
     const int n = p.n, np = p.np, nb = np / 128;
-    const int row0 = blockIdx.x * kK1Rows;          // first row of this CTA
-    const int I = row0 / 128, q = (row0 & 127) / kK1Rows;
+    const int row0 = blockIdx.x * kRows;            // first row of this CTA
+    const int I = row0 / 128, q = (row0 & 127) / kRows;
     const double alpha = p.alpha[m], gamma = p.gamma[m];
     double radius[4] = {0.0, 0.0, 0.0, 0.0}, hii[4] = {0.0, 0.0, 0.0, 0.0};
     bool bad_nf = false, bad_hr = false;
@@ -246,7 +255,7 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
         if (J + 1 < nb) load_tile(J + 1, hnext);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int rl = warp * 4 + k;              // local row 0..31
+            const int rl = warp * 4 + k;              // local row 0..kRows-1
             const int i = row0 + rl;
             const double* h = hk[k];
             float x[4];
@@ -292,14 +301,15 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
         }
         if (!p.xa_used || p.xa_used[I * nb + J]) {
             __syncthreads();
-            // block (I, J), rows 32q .. 32q+31: [c4][row][4]; thread t -> c4 = t / 8, rows 4(t%8)..+3
+            // block (I, J), rows q kRows .. +kRows-1: [c4][row][4]; thread t -> c4 = t / (kRows/4),
+            // rows 4 (t % (kRows/4)) .. +3
             const size_t tb = xa_tile_base(m, I, J, nb);
-            const int c4 = threadIdx.x >> 3, r4 = (threadIdx.x & 7) * 4;
+            const int c4 = threadIdx.x / (kRows / 4), r4 = (threadIdx.x % (kRows / 4)) * 4;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int rl = r4 + k;
                 const float4 av = *reinterpret_cast<const float4*>(&sA[rl * kK1Pad + 4 * c4]);
-                *reinterpret_cast<float4*>(p.A + tb + xa_off(q * kK1Rows + rl, c4)) = av;
+                *reinterpret_cast<float4*>(p.A + tb + xa_off(q * kRows + rl, c4)) = av;
             }
         }
         __syncthreads();
@@ -330,7 +340,7 @@ __global__ void __launch_bounds__(256) rescale_tiles_kernel(const __grid_constan
     __syncthreads();
     if (threadIdx.x == 0) {
         double lo = s_lo[0], hi = s_hi[0];
-        for (int w = 1; w < 8; ++w) {
+        for (int w = 1; w < WARPS; ++w) {
             lo = fmin(lo, s_lo[w]);
             hi = fmax(hi, s_hi[w]);
         }
