@@ -306,6 +306,9 @@ __device__ __forceinline__ void epi_sub_mid_red(const uint32_t (&v)[16], const X
 // elements (Tr D, sum D^2 with off-diagonal elements counted twice); sixteen columns.  mir = false
 // (row-block table, off the diagonal blocks): only the direct entry, counted once -- the mirrored
 // entry belongs to another rank's rows, which computes it itself.
+// The direct entries of an off-diagonal block go out as one 32-byte store per four columns when the
+// row slab allows it (n % 4 == 0, all four inside the matrix): a warp then writes 32 whole sectors per
+// instruction instead of touching each sector four times with 8-byte stores.
 template <int MODE, bool DIAG>
 __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const XOp& xop, const float* At,
                                              int r, int c0, int gi, int gj0, int n, bool c_on,
@@ -317,6 +320,9 @@ __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const XOp&
         const float4 aq = __ldcg(reinterpret_cast<const float4*>(At + xa_off(r, c0 / 4 + j)));
         const float xs[4] = {x01.x, x01.y, x23.x, x23.y};
         const float as[4] = {aq.x, aq.y, aq.z, aq.w};
+        const int gjq = gj0 + c0 + 4 * j;  // first column of the quad
+        const bool vec = !DIAG && Dm && gi < n && gjq + 3 < n && (n & 3) == 0;
+        double dq[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int cl = c0 + 4 * j + e;
@@ -326,10 +332,11 @@ __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const XOp&
             const float xn = (dg && c_on) ? poly_step<true>(y, xs[e], k) : poly_step<false>(y, xs[e], k);
             const bool own = !DIAG || cl >= r;
             if (own) hl.add(xn);
+            const double dv = (double)as[e] + (double)fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]) + (double)xn;
+            dq[e] = dv;
             if (own && gi < n && gj < n) {
-                const double dv = (double)as[e] + (double)fmaf(k.dc_hi, xs[e], k.dc_lo * xs[e]) + (double)xn;
                 if (Dm) {
-                    Dm[(size_t)gi * n + gj] = dv;
+                    if (!vec) Dm[(size_t)gi * n + gj] = dv;
                     if (!dg && (DIAG || mir)) Dm[(size_t)gj * n + gi] = dv;
                 }
                 if (dg) {
@@ -340,6 +347,10 @@ __device__ __forceinline__ void epi_sub_last(const uint32_t (&v)[16], const XOp&
                 }
             }
         }
+        if (vec)
+            asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(Dm + (size_t)gi * n + gjq), "d"(dq[0]),
+                         "d"(dq[1]), "d"(dq[2]), "d"(dq[3])
+                         : "memory");
     }
 }
 
