@@ -62,7 +62,7 @@ typedef enum ffg_status {
     FFG_ERR_OUT_OF_REGION = 2, /* rescale_to_model: (beta', mu') outside Eq. 41            */
     FFG_ERR_DIVERGED = 3,      /* non-finite entry mid-recursion (layer in provenance)     */
     FFG_ERR_HALF_RANGE = 4,    /* binary16 split overflow (HalfRangeError)                 */
-    FFG_ERR_UNSUPPORTED = 5,   /* DOUBLE / SINGLE modes stay on the CPU reference          */
+    FFG_ERR_UNSUPPORTED = 5,   /* a mode an entry point does not run (e.g. row-block DOUBLE) */
     FFG_ERR_DIMENSION = 6,     /* std::invalid_argument: dimension mismatch                */
     FFG_ERR_CUDA = 7,          /* no sm_100 device, launch or allocation failure           */
     FFG_ERR_NCCL = 8
@@ -70,8 +70,8 @@ typedef enum ffg_status {
 
 /* PrecisionMode plus the two north-star low-precision modes. */
 typedef enum ffg_mode {
-    FFG_MODE_DOUBLE = 0,          /* not on the GPU path -> FFG_ERR_UNSUPPORTED             */
-    FFG_MODE_SINGLE = 1,          /* not on the GPU path -> FFG_ERR_UNSUPPORTED             */
+    FFG_MODE_DOUBLE = 0,          /* fp64 recursion: library DGEMM + our layer kernels       */
+    FFG_MODE_SINGLE = 1,          /* fp32 recursion: library SGEMM (no TF32) + our kernels   */
     FFG_MODE_MIXED_EMULATED = 2,  /* FP32-emulated: binary16 hi/lo split (x 2^14 pre-scale),
                                      hi*hi + hi*lo + lo*hi with FP32 accumulation (Eq. 48) */
     FFG_MODE_BF16 = 3,            /* one bf16 product per square, FP32 accumulation          */
@@ -246,7 +246,8 @@ int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, in
 
 /* Which recursion kernel (K2) computes matrices of order n in `mode` (the choice depends only on
  * n and the mode; FFG_WIDE=0/1 overrides): 0 = mlsp2_pair_kernel (256 x 128 pair items),
- * 1 = mlsp2_wide_kernel (256 x 256 super-block items), negative = unsupported mode / size. */
+ * 1 = mlsp2_wide_kernel (256 x 256 super-block items), 2 = DOUBLE / SINGLE (cuBLAS {D,S}gemm for the
+ * square + direct.cuh layer kernels), negative = unsupported mode / size. */
 int32_t ffg_k2_kernel(int64_t n, int32_t mode);
 
 /* Measurement hooks (bench.py): when enabled, every recursion-kernel (K2) launch is

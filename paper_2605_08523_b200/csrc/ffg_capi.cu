@@ -18,11 +18,14 @@
 #include <string>
 #include <vector>
 
+#include <cublas_v2.h>
+#include <dlfcn.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include "fermiforge/ffg.h"
 #include "k2_pair.cuh"
 #include "k2_wide.cuh"
+#include "direct.cuh"
 
 using namespace ffg;
 
@@ -78,11 +81,8 @@ int mode_to_internal(int32_t mode, int* out) {
         case FFG_MODE_MIXED_EMULATED: *out = kModeF32E; return FFG_OK;
         case FFG_MODE_FP16: *out = kModeF16; return FFG_OK;
         case FFG_MODE_BF16: *out = kModeBF16; return FFG_OK;
-        case FFG_MODE_DOUBLE:
-        case FFG_MODE_SINGLE:
-            return set_err(FFG_ERR_UNSUPPORTED,
-                           "PrecisionMode %d (DOUBLE/SINGLE) is not a tensor-core mode; "
-                           "use MIXED_EMULATED, BF16 or FP16", mode);
+        case FFG_MODE_DOUBLE: *out = kModeF64; return FFG_OK;
+        case FFG_MODE_SINGLE: *out = kModeF32; return FFG_OK;
         default: return set_err(FFG_ERR_VALIDATION, "unknown PrecisionMode %d", mode);
     }
 }
@@ -181,6 +181,10 @@ struct Workspace {
     size_t cap_h = 0;      // staging elements (B * n * n)
     float* A = nullptr;
     uint16_t* op[4] = {nullptr, nullptr, nullptr, nullptr};  // hi0, lo0, hi1, lo1
+    uint8_t* dX = nullptr;   // DOUBLE / SINGLE modes (direct.cuh): X, Y = X X, A in fp64 or fp32
+    uint8_t* dY = nullptr;
+    uint8_t* dA = nullptr;
+    size_t cap_direct = 0;   // bytes of each
     double* Hs = nullptr;
     double* Ds = nullptr;
     double* params = nullptr;       // [4][cap_B]: alpha, gamma, scale, mu
@@ -245,6 +249,9 @@ Workspace* get_ws(int dev, cudaStream_t st) {
 
 void free_ws(Workspace* w) {
     cudaFree(w->A);
+    cudaFree(w->dX);
+    cudaFree(w->dY);
+    cudaFree(w->dA);
     for (auto& p : w->op) cudaFree(p);
     cudaFree(w->Hs);
     cudaFree(w->Ds);
@@ -1149,7 +1156,139 @@ int enqueue_k3(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx
     return FFG_OK;
 }
 
+// ------------------------------------------------------------------ DOUBLE / SINGLE (direct.cuh)
+// cuBLAS is loaded on first use of these modes only (dlopen: the tensor-core path never loads it).
+struct CublasApi {
+    bool tried = false, ok = false;
+    cublasStatus_t (*create)(cublasHandle_t*) = nullptr;
+    cublasStatus_t (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
+    cublasStatus_t (*set_math)(cublasHandle_t, cublasMath_t) = nullptr;
+    cublasStatus_t (*dgemm)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const double*,
+                            const double*, int, long long, const double*, int, long long, const double*, double*,
+                            int, long long, int) = nullptr;
+    cublasStatus_t (*sgemm)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const float*,
+                            const float*, int, long long, const float*, int, long long, const float*, float*,
+                            int, long long, int) = nullptr;
+};
+CublasApi g_cublas;
+std::mutex g_cublas_mu;
+std::map<int, cublasHandle_t> g_cublas_handle;
+
+int cublas_handle(cudaStream_t st, cublasHandle_t* out) {
+    std::lock_guard<std::mutex> lk(g_cublas_mu);
+    if (!g_cublas.tried) {
+        g_cublas.tried = true;
+        // already loaded by the host process (torch) or the CUDA toolkit's copy
+        const char* names[] = {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12", "libcublas.so"};
+        void* h = nullptr;
+        for (const char* nm : names)
+            if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (h) {
+            g_cublas.create = reinterpret_cast<decltype(g_cublas.create)>(dlsym(h, "cublasCreate_v2"));
+            g_cublas.set_stream = reinterpret_cast<decltype(g_cublas.set_stream)>(dlsym(h, "cublasSetStream_v2"));
+            g_cublas.set_math = reinterpret_cast<decltype(g_cublas.set_math)>(dlsym(h, "cublasSetMathMode"));
+            g_cublas.dgemm = reinterpret_cast<decltype(g_cublas.dgemm)>(dlsym(h, "cublasDgemmStridedBatched"));
+            g_cublas.sgemm = reinterpret_cast<decltype(g_cublas.sgemm)>(dlsym(h, "cublasSgemmStridedBatched"));
+            g_cublas.ok = g_cublas.create && g_cublas.set_stream && g_cublas.set_math && g_cublas.dgemm &&
+                          g_cublas.sgemm;
+        }
+    }
+    if (!g_cublas.ok) return set_err(FFG_ERR_UNSUPPORTED, "DOUBLE/SINGLE modes need cuBLAS (libcublas.so.12 not found)");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    auto it = g_cublas_handle.find(dev);
+    if (it == g_cublas_handle.end()) {
+        cublasHandle_t hd;
+        if (g_cublas.create(&hd) != CUBLAS_STATUS_SUCCESS) return set_err(FFG_ERR_CUDA, "cublasCreate failed");
+        g_cublas.set_math(hd, CUBLAS_PEDANTIC_MATH);  // true fp32 / fp64 arithmetic (no TF32)
+        it = g_cublas_handle.emplace(dev, hd).first;
+    }
+    if (g_cublas.set_stream(it->second, st) != CUBLAS_STATUS_SUCCESS)
+        return set_err(FFG_ERR_CUDA, "cublasSetStream failed");
+    *out = it->second;
+    return FFG_OK;
+}
+
+// The recursion in fp64 (DOUBLE) / fp32 (SINGLE) arithmetic: bounds, X0 / A, L x (GEMM + fused layer
+// update), D + row partials, K3.  Y = X X as a column-major GEMM of the row-major X: X is exactly
+// symmetric, and the layer update reads only upper-triangle entries of Y.
+template <typename T>
+int enqueue_direct(Workspace& w, const Job& j, cudaStream_t st) {
+    NvtxRange nv("ffg direct enqueue (DOUBLE/SINGLE)");
+    const int B = j.B;
+    const int n = (int)j.n;
+    const ffg_model& md = *j.model;
+    const size_t nn = (size_t)n * n;
+    int rc;
+    if ((rc = ensure(w, B, 0, n, false))) return rc;
+    const size_t bytes = (size_t)B * nn * sizeof(T);
+    if (bytes > w.cap_direct) {
+        size_t dummy = 0;
+        if ((rc = grow(&w.dX, dummy, bytes))) return rc;
+        if ((rc = grow(&w.dY, dummy, bytes))) return rc;
+        if ((rc = grow(&w.dA, dummy, bytes))) return rc;
+        w.cap_direct = bytes;
+    }
+    cublasHandle_t hd;
+    if ((rc = cublas_handle(st, &hd))) return rc;
+    std::vector<double> ph((size_t)4 * B);
+    for (int m = 0; m < B; ++m) {
+        ph[0 * B + m] = j.alpha[m];
+        ph[1 * B + m] = j.gamma[m];
+        ph[2 * B + m] = j.scale ? j.scale[m] : 0.0;
+        ph[3 * B + m] = j.mu ? j.mu[m] : 0.0;
+    }
+    if ((rc = upload_small(w, w.params, ph.data(), sizeof(double) * 4 * B, st))) return rc;
+    reset_kernel<<<(B + 127) / 128, 128, 0, st>>>(w.bounds, w.flags, B, nullptr, 0, w.products);
+    CK(cudaGetLastError());
+    gershgorin_kernel<<<dim3((unsigned)((n + 7) / 8), (unsigned)B), 256, 0, st>>>(j.H_dev, n, w.bounds);
+    CK(cudaGetLastError());
+    T* X = reinterpret_cast<T*>(w.dX);
+    T* Y = reinterpret_cast<T*>(w.dY);
+    T* A = reinterpret_cast<T*>(w.dA);
+    const unsigned eb = (unsigned)std::min<size_t>((nn + 255) / 256, 1024);
+    direct_init_kernel<T><<<dim3(eb, (unsigned)B), 256, 0, st>>>(j.H_dev, w.params, w.params + B, md.abcd[3], X, A,
+                                                                 n, w.flags);
+    CK(cudaGetLastError());
+    const int nt = (n + 31) / 32;
+    const unsigned tiles = (unsigned)(nt * (nt + 1) / 2);
+    const T one = (T)1, zero = (T)0;
+    for (int l = 0; l < md.n_layers; ++l) {
+        cublasStatus_t cs;
+        if constexpr (std::is_same<T, double>::value)
+            cs = g_cublas.dgemm(hd, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, X, n, (long long)nn, X, n, (long long)nn,
+                                &zero, Y, n, (long long)nn, B);
+        else
+            cs = g_cublas.sgemm(hd, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, X, n, (long long)nn, X, n, (long long)nn,
+                                &zero, Y, n, (long long)nn, B);
+        if (cs != CUBLAS_STATUS_SUCCESS) return set_err(FFG_ERR_CUDA, "cuBLAS gemm failed (%d)", (int)cs);
+        DirectLayer<T> dl;
+        dl.Y = Y;
+        dl.X = X;
+        dl.A = A;
+        dl.a = md.abcd[4 * l + 0];
+        dl.b = md.abcd[4 * l + 1];
+        dl.c = md.abcd[4 * l + 2];
+        dl.d_next = l + 1 < md.n_layers ? md.abcd[4 * (l + 1) + 3] : 0.0;
+        dl.n = n;
+        dl.flags = w.flags;
+        dl.layer = l;
+        direct_layer_kernel<T><<<dim3(tiles, (unsigned)B), 256, 0, st>>>(dl);
+        CK(cudaGetLastError());
+    }
+    RegionCheck region{w.bounds, j.scale ? w.params + 2 * B : nullptr, w.params + 3 * B, md.mu0};
+    direct_final_kernel<T><<<dim3((unsigned)((n + 7) / 8), (unsigned)B), 256, 0, st>>>(
+        X, A, j.D_dev, n, w.partials, region, md.n_layers, w.products);
+    CK(cudaGetLastError());
+    EnqueueCtx cx;
+    cx.Tpart = n;
+    cx.region = region;
+    return enqueue_k3(w, j, st, cx, j.n);
+}
+
 int enqueue(Workspace& w, const Job& j, cudaStream_t st) {
+    if (j.mode == kModeF64) return enqueue_direct<double>(w, j, st);
+    if (j.mode == kModeF32) return enqueue_direct<float>(w, j, st);
     EnqueueCtx cx;
     int rc;
     if ((rc = enqueue_k1(w, j, st, cx))) return rc;
@@ -1313,7 +1452,7 @@ int submit_host(Workspace& w, cudaStream_t st, int B, const double* const* H, in
     hsl.ticket = ++w.next_ticket;
     hsl.B = B;
     hsl.n = n;
-    hsl.PT = w.PT;
+    hsl.PT = (mode == kModeF64 || mode == kModeF32) ? 1 : w.PT;  // direct modes count squarings directly
     hsl.mode_api = mode_api;
     hsl.model = *md;
     hsl.mu.assign(mu ? mu : alpha, (mu ? mu : alpha) + B);
@@ -1876,6 +2015,7 @@ int ffg_density_matrices_dev(int32_t batch, const double* H_dev, int64_t n, cons
 int32_t ffg_k2_kernel(int64_t n, int32_t mode) {
     int m;
     if (n < 1 || mode_to_internal(mode, &m)) return -1;
+    if (m == kModeF64 || m == kModeF32) return 2;  // library GEMM + direct.cuh layer kernels
     const int64_t np = (n + kBM - 1) / kBM * kBM;
     return use_wide(m, (int)(np / kBM), false) ? 1 : 0;
 }
@@ -1950,6 +2090,8 @@ int ffg_rowblock_begin(const double* H_dev, int64_t n, double mu, double kT, con
     *handle = nullptr;
     if ((rc = validate_model(model))) return rc;
     if ((rc = mode_to_internal(mode_api, &mode))) return rc;
+    if (mode == kModeF64 || mode == kModeF32)
+        return set_err(FFG_ERR_UNSUPPORTED, "row-block sharding runs the tensor-core modes (MIXED_EMULATED, BF16, FP16)");
     if ((rc = validate_n(n))) return rc;
     if ((rc = check_mu_kT(1, &mu, &kT))) return rc;
     if (world < 1 || rank < 0 || rank >= world)

@@ -466,7 +466,7 @@ def k2_kernel_name(n: int, mode: PrecisionMode = PrecisionMode.MIXED_EMULATED) -
     k = int(lib().ffg_k2_kernel(int(n), int(mode)))
     if k < 0:
         raise ValidationError(f"no recursion kernel for n={n}, mode={mode}")
-    return ("mlsp2_pair_kernel", "mlsp2_wide_kernel")[k]
+    return ("mlsp2_pair_kernel", "mlsp2_wide_kernel", "cublas_gemm+direct_layer")[k]
 
 
 def profile_layers(enable: bool) -> None:

@@ -159,6 +159,10 @@ def main():
     for n in (4096, 8192):
         for mode in (F32E, BF16, FP16):
             rows.append(run_case("configs[2] N=%d single" % n, n, 1, mode, model, pk, 3, cusolver=mode == F32E))
+    # outside the north star's tensor-core modes: DOUBLE / SINGLE (library GEMM path)
+    for mode in (E.PrecisionMode.DOUBLE, E.PrecisionMode.SINGLE):
+        for n in (1024, 4096):
+            rows.append(run_case("PrecisionMode %s N=%d single" % (mode.name, n), n, 1, mode, model, pk, 3))
     if not args.quick:
         mu, kT = batch_params(512)
         for mode in (F32E, BF16):

@@ -74,16 +74,15 @@ def test_validation_mirrors_reference():
 
 
 def test_modes():
+    """Every PrecisionMode of SPEC.md:308-311 is accepted (DOUBLE / SINGLE run the library-GEMM path);
+    an unknown mode id is a validation error before any device work."""
     m = E.load_model("M1500")
-    if E.device_available():
-        pytest.skip("device present")
-    for mode in (E.PrecisionMode.DOUBLE, E.PrecisionMode.SINGLE):
-        with pytest.raises(E.UnsupportedModeError):
-            E.lib()  # noqa
-            m_c = m._c()
-            rc = E.lib().ffg_density_matrix(E._dp(np.eye(4)), 4, 0.0, 0.01, ctypes.byref(m_c), int(mode),
-                                            None, None, None)
-            E._check(rc)
+    m_c = m._c()
+    assert E.k2_kernel_name(1024, E.PrecisionMode.DOUBLE) == "cublas_gemm+direct_layer"
+    assert E.k2_kernel_name(1024, E.PrecisionMode.SINGLE) == "cublas_gemm+direct_layer"
+    rc = E.lib().ffg_density_matrix(E._dp(np.eye(4)), 4, 0.0, 0.01, ctypes.byref(m_c), 7, None, None, None)
+    with pytest.raises(E.ValidationError, match="PrecisionMode"):
+        E._check(rc)
 
 
 def test_no_cpu_fallback_without_device():

@@ -7,6 +7,8 @@ Tolerances, vs the fp64 recursion on ide
 Integer-exact cases (exact-half inputs of mixed_square, Gershgorin bounds of the
 tight-binding family) are bit-exact.
 """
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -277,8 +279,9 @@ def test_validation_errors(model):
     H = tight_binding(64)
     with pytest.raises(E.ValidationError):
         E.compute_density_matrix(H, 0.0, -1.0, model)
-    with pytest.raises(E.UnsupportedModeError):
-        E.compute_density_matrix(H, 0.0, 0.01, model, E.PrecisionMode.DOUBLE)
+    with pytest.raises(E.ValidationError, match="PrecisionMode"):
+        E._check(E.lib().ffg_density_matrix(E._dp(H), H.shape[0], 0.0, 0.01, ctypes.byref(model._c()), 9,
+                                            None, None, None))
     bad = E.Mlsp2Model(model.abcd, model.beta0, 1.5)
     with pytest.raises(E.ValidationError, match="mu0"):
         E.compute_density_matrix(H, 0.0, 0.01, bad)
