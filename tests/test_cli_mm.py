@@ -86,3 +86,27 @@ def test_cli_apply_and_solve_mu(tmp_path):
     r = subprocess.run([sys.executable, "-m", "paper_2605_08523_b200", "solve-mu", "--hamiltonian", str(two),
                         "--beta", "10", "--nocc", "2"], capture_output=True, text=True, cwd=ROOT, timeout=300)
     assert r.returncode == 64
+
+
+@pytest.mark.gpu
+def test_cli_double_precision(tmp_path):
+    """SPEC.md:630 / :660: `apply --precision double` writes the DOUBLE-mode D (bitwise the engine's)
+    with n squarings in the provenance; `bench --precision double` reports matmul count = layers."""
+    from paper_2605_08523_b200 import engine as E
+    H = tight_binding(128, seed=77)
+    hp, dp = tmp_path / "H.mtx", tmp_path / "D.mtx"
+    write_matrix_market(H, str(hp))
+    r = subprocess.run([sys.executable, "-m", "paper_2605_08523_b200", "apply", "--model", "M1500",
+                        "--hamiltonian", str(hp), "--kT", "0.01", "--mu", "0", "--precision", "double",
+                        "--out", str(dp)], capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert r.returncode == 0, r.stderr
+    prov = json.loads(r.stdout.splitlines()[-1])
+    assert prov["precision"] == "double" and prov["half_products"] == 30
+    D, _, _ = E.compute_density_matrix(read_matrix_market(str(hp)), 0.0, 0.01, E.load_model("M1500"),
+                                       E.PrecisionMode.DOUBLE)
+    assert np.array_equal(read_matrix_market(str(dp)), D)
+    r = subprocess.run([sys.executable, "-m", "paper_2605_08523_b200", "bench", "--sizes", "128,256",
+                        "--precision", "double"], capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rows = [l.split() for l in r.stdout.splitlines() if l.strip() and l.split()[0] in ("128", "256")]
+    assert len(rows) == 2 and all(row[1] == "double" and int(row[4]) == 30 for row in rows), r.stdout
