@@ -137,3 +137,17 @@ def test_double_rowblock_unsupported(model):
     H = torch.from_numpy(tight_binding(512, seed=1)).cuda()
     with pytest.raises(E.UnsupportedModeError, match="row-block"):
         RB.RowBlockRank(H, 0.0, 0.01, model, rank=0, world=2, mode=DOUBLE)
+
+
+def test_double_workflow_callers():
+    """The workflow callers run in DOUBLE mode too: the SPEC two-level mu-solve and the
+    entropy trace against the fp64 recursion of the same entropy model (tighter than MIXED_EMULATED)."""
+    from paper_2605_08523_b200 import workflow as W
+    D, st, rep = W.solve_chemical_potential(np.diag([0.0, 1.0]), 10.0, 1.0, 0.4, tol=1e-9, mode=DOUBLE)
+    # the electron count is met to the Newton tolerance; mu = 0.5 up to the model's own error
+    assert rep.converged and abs(st.trace - 1.0) <= 1e-9 and abs(rep.mu_final - 0.5) <= 2e-5
+    em = W.load_entropy_model("E1500")
+    H = tight_binding(256, seed=9)
+    ts = W.entropy_trace(H, 0.1, 0.01, em, mode=DOUBLE)
+    ref = O.entropy_trace_f64(H, 0.1, 0.01, em.inner.abcd, em.alpha, em.beta0, em.mu0)
+    assert abs(ts - ref) <= 1e-9 * max(1.0, abs(ref)), (ts, ref)
