@@ -2021,11 +2021,13 @@ int32_t ffg_k2_kernel(int64_t n, int32_t mode) {
 }
 
 int64_t ffg_kernel_launches(int32_t batch, int64_t n, const ffg_model* model, int32_t mode) {
-    (void)batch;
-    (void)n;
-    (void)mode;
-    if (!model) return 0;
-    return 4;  // reset + K1 + K2 (all layers, one persistent launch) + K3
+    int m;
+    if (!model || batch < 1 || n < 1 || mode_to_internal(mode, &m)) return 0;
+    if (m == kModeF64 || m == kModeF32)  // upload, reset, bounds, init, L layer updates, final, K3
+        return 6 + model->n_layers;      // (+ L library GEMMs, not counted: not our kernels)
+    // two parameter uploads (launch-carried, upload_small), reset, K1, K2 (all layers; one persistent
+    // launch per kValidBits matrices), K3
+    return 5 + (batch + kValidBits - 1) / kValidBits;
 }
 
 int ffg_profile_layers(int enable) {

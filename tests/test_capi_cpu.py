@@ -97,7 +97,10 @@ def test_no_cpu_fallback_without_device():
 
 def test_kernel_launch_accounting():
     m = E.load_model("M1500")
-    assert E.kernel_launches(1, 1024, m) == 4  # reset, K1, K2 (all 30 layers), K3
+    # two launch-carried parameter uploads, reset, K1, K2 (all 30 layers), K3
+    assert E.kernel_launches(1, 1024, m) == 6 and E.kernel_launches(16, 1024, m) == 6
+    assert E.kernel_launches(8193, 512, m) == 7  # K2 once per 8192 matrices (validity bitmap)
+    assert E.kernel_launches(4, 1024, m, E.PrecisionMode.DOUBLE) == 6 + 30
     assert E.algorithmic_flops(4096, 30, E.PrecisionMode.MIXED_EMULATED) == pytest.approx(6.19e12, rel=1e-3)
     assert E.algorithmic_flops(1024, 30, E.PrecisionMode.BF16) == pytest.approx(3.22e10, rel=1e-2)
 
