@@ -1,6 +1,6 @@
 """Workload for compute-sanitizer (memcheck / racecheck / synccheck): K1 -> K2 -> K3 at N=256 in
 FP32-emulated and BF16 mode, a 3-matrix batch (8-warp and 16-worker epilogues), one row-block rank,
-and the wide kernel (forced, FFG_WIDE=1) on a 2-matrix N=512 batch in both modes.
+the wide kernel (forced, FFG_WIDE=1) on a 2-matrix N=512 batch in both modes, and DOUBLE / SINGLE at N=256.
 
     compute-sanitizer --tool racecheck python scripts/sanitize_small.py
 """
@@ -38,3 +38,7 @@ for mode in (E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16):
     s, status, _ = E.compute_density_matrices_device(Hw, mu[:2], kT[:2], m, mode, D_dev=Dw)
     torch.cuda.synchronize()
     print("wide", mode.name, status.tolist(), s[:, 0].tolist(), flush=True)
+os.environ.pop("FFG_WIDE")
+for mode in (E.PrecisionMode.DOUBLE, E.PrecisionMode.SINGLE):
+    D, st, pv = E.compute_density_matrix(H, 0.0, 0.01, m, mode)
+    print(mode.name, "trace", st.trace, "status", pv.status, flush=True)
