@@ -147,3 +147,16 @@ def test_wide_provenance_products(model, monkeypatch):
     assert pv.half_products == 10 * 4 + (model.layer_count - 10) * 3
     _, _, pv = E.compute_density_matrix(H, 0.0, 0.01, model, E.PrecisionMode.BF16)
     assert pv.half_products == model.layer_count
+
+
+@pytest.mark.parametrize("mode", [E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16])
+def test_wide_default_padded_size(torch, model, mode):
+    """The default selection at a padded size (n = 2300 -> np = 2304, 9 super-rows, 44 padded rows and
+    columns): wide kernel, within the gates, exactly symmetric; n = 2176 (odd block count) stays on the
+    pair kernel."""
+    assert E.k2_kernel_name(2300) == "mlsp2_wide_kernel" and E.k2_kernel_name(2176) == "mlsp2_pair_kernel"
+    H = torch.from_numpy(tight_binding(2300, seed=23)).cuda().unsqueeze(0)
+    D, stats, status = run(torch, H, [0.05], [0.011], model, mode)
+    assert status.tolist() == [0] and torch.equal(D, D.transpose(1, 2))
+    R = DR.density_matrices_f64(H, [0.05], [0.011], model.abcd, model.beta0, model.mu0)
+    gate(mode, D, R, "wide default N=2300")
