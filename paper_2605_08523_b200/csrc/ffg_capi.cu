@@ -1110,7 +1110,8 @@ int enqueue_k2(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx
         if (cx.wide) {
             if ((rc = wide_capacity_mode(j.mode, &cap))) return rc;
             lp.G = wide_group_size(Bl, cx.np, w.PT, cap);
-            lp.blockdeps = 0;
+            const char* bdw = getenv("FFG_BLOCKDEPS");
+            lp.blockdeps = bdw ? atoi(bdw) : (lp.G == 1 && l1 - l0 > 1);
             const int64_t items = (int64_t)(l1 - l0) * Bl * w.PT;
             if ((rc = launch_wide_mode(j.mode, w.pmaps, lp, items, k2s))) return rc;
             continue;

@@ -257,13 +257,17 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
         const size_t xrow = ((size_t)m * np + gi) * np + (size_t)Q * kBN + 64 * (cg & 1);
         const uint16_t* xh = p.ophi[l & 1] + xrow;
         const uint16_t* xl = p.oplo[l & 1] + xrow;
-        // X_l of this block is complete once super-row S is (the producer's dependency wait,
-        // re-acquired here for this warp's own generic loads); its loads go out before the wait for Y
-        if (!redundant && l > p.l0) {
+        // X_l of this block is complete once super-row S is, and every layer-l reader of the parity
+        // this item overwrites is done once super-rows S and T are (the producer's dependency wait, or
+        // -- block-granular mode -- not yet: re-acquired here for this warp's own loads and stores);
+        // the X loads go out before the wait for Y
+        if (l > p.l0) {
             if (lane == 0) {
                 const uint32_t need = (uint32_t)(kWideCount * nsb * (l - p.l0));
                 const long long t0 = FFG_ROLE_PROF ? clock64() : 0;
                 while (ld_acquire_gpu(p.counters + (size_t)m * nsb + S) < need) {
+                }
+                while (ld_acquire_gpu(p.counters + (size_t)m * nsb + T) < need) {
                 }
                 if (FFG_ROLE_PROF) w_dep += (unsigned long long)(clock64() - t0);
             }
@@ -434,6 +438,7 @@ __device__ __forceinline__ void wide_workers(const PairParams& p, const MatrixMa
             if (wk == 0 && lane == 0) {
                 __threadfence();
                 uint32_t* cm = p.counters + (size_t)m * nsb;
+                if (p.blockdeps) red_relaxed_gpu_add(p.bflags + ((size_t)m * nsb + S) * nsb + T, 1u);
                 red_relaxed_gpu_add(cm + S, 1u);
                 if (T != S) red_relaxed_gpu_add(cm + T, 1u);
             }
@@ -534,22 +539,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWideThreads, 1)
                 pair_decode(p, mm, item, m, l, pi);
                 const uint32_t pr = __ldg(p.pairs + pi);
                 const int S = pr & 1023, T = (pr >> 10) & 1023;
+                const uint32_t* cm = p.counters + (size_t)m * nsb;
+                const uint32_t need = (uint32_t)(kWideCount * nsb * (l - p.l0));
+                // block-granular dependencies (single-matrix groups, p.blockdeps): while super-row S or
+                // T is incomplete, each super-column U of the K loop waits for the two super-blocks
+                // its operand tiles come from, so the item's first K-blocks overlap the previous
+                // layer's tail (the pair kernel's scheme, k2_pair.cuh)
+                bool blockwise = false;
                 if (l > p.l0) {
-                    const uint32_t need = (uint32_t)(kWideCount * nsb * (l - p.l0));
-                    const uint32_t* cm = p.counters + (size_t)m * nsb;
                     const long long t0 = clock64();
-                    while (ld_acquire_gpu(cm + S) < need)
-                        watchdog_check(t0, 13, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + S), need);
-                    while (ld_acquire_gpu(cm + T) < need)
-                        watchdog_check(t0, 14, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + T), need);
+                    if (p.blockdeps) {
+                        blockwise = ld_acquire_gpu(cm + S) < need || ld_acquire_gpu(cm + T) < need;
+                    } else {
+                        while (ld_acquire_gpu(cm + S) < need)
+                            watchdog_check(t0, 13, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + S), need);
+                        while (ld_acquire_gpu(cm + T) < need)
+                            watchdog_check(t0, 14, ((unsigned long long)item << 32) | (uint32_t)(m * 1024 + T), need);
+                    }
                     if (FFG_ROLE_PROF) w_dep += (unsigned long long)(clock64() - t0);
-                    fence_proxy_async_global();
+                    if (!blockwise) fence_proxy_async_global();
                 }
                 const int par = l & 1;
                 const int mrow = m * p.np;
                 const int PA = 2 * S + (int)rank, PB = 2 * T + (int)rank;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % S_;
+                    if (blockwise && (kb & 3) == 0) {
+                        const int U = kb >> 2;  // super-column of the next four K-blocks
+                        const uint32_t needb = (uint32_t)(kWideCount * (l - p.l0));
+                        const uint32_t* bf = p.bflags + (size_t)m * nsb * nsb;
+                        const uint32_t* fa = bf + min(S, U) * nsb + max(S, U);
+                        const uint32_t* fb = bf + min(T, U) * nsb + max(T, U);
+                        const long long t0 = clock64();
+                        uint32_t va = ld_acquire_gpu(fa), vb = ld_acquire_gpu(fb);
+                        if (ld_acquire_gpu(cm + S) >= need && ld_acquire_gpu(cm + T) >= need) blockwise = false;
+                        while (va < needb) {
+                            watchdog_check(t0, 15, ((unsigned long long)item << 32) | (uint32_t)(S * 1024 + U), needb);
+                            va = ld_acquire_gpu(fa);
+                        }
+                        while (vb < needb) {
+                            watchdog_check(t0, 16, ((unsigned long long)item << 32) | (uint32_t)(T * 1024 + U), needb);
+                            vb = ld_acquire_gpu(fb);
+                        }
+                        if (FFG_ROLE_PROF) w_dep += (unsigned long long)(clock64() - t0);
+                        fence_proxy_async_global();
+                    }
                     FFG_TIMED(w_empty, mbar_wait_at(empty_a + 8 * s, ((it / S_) & 1) ^ 1));
                     const uint32_t fbar = full_l0 + 8 * s;
                     if (p.dbg & 16) {  // measurement: no operand traffic (MMAs on stale smem)

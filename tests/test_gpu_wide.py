@@ -120,6 +120,21 @@ def test_wide_schedule_invariance(torch, model, monkeypatch):
     assert torch.equal(D3[0], D0[3]) and np.array_equal(s3[0], s0[3])
 
 
+@pytest.mark.parametrize("mode", ["MIXED_EMULATED", "BF16"])
+def test_wide_block_dependencies_bit_identical(torch, model, mode, monkeypatch):
+    """Block-granular layer dependencies (single-matrix launches, FFG_BLOCKDEPS) only let an item's
+    first K-blocks start before its whole super-rows are done: D and the statistics are bit-identical
+    to the super-row-granular schedule."""
+    H = torch.from_numpy(tight_binding(2048, seed=77)[None]).cuda()
+    mu, kT = batch_params(1)
+    out = {}
+    for bd in ("0", "1"):
+        monkeypatch.setenv("FFG_BLOCKDEPS", bd)
+        out[bd] = run(torch, H, mu, kT, model, E.PrecisionMode[mode])
+    monkeypatch.delenv("FFG_BLOCKDEPS")
+    assert torch.equal(out["0"][0], out["1"][0]) and np.array_equal(out["0"][1], out["1"][1])
+
+
 def test_wide_out_of_region_member(torch, model, monkeypatch):
     """An out-of-region member of a wide batch issues no products and gets D = NaN; the other members
     are bit-identical to the batch without it."""
