@@ -2,7 +2,7 @@
 // (tcgen05.mma.cta_group::2, M = 256, N = 256) and each hi/lo block stored ONCE.
 //
 // Why: the pair kernel (k2_pair.cuh, 256 x 128 tiles) moves ~6200 B/cycle through L2 at the bench
-// configuration -- the LTS throughput cap -- and 58% of it is the operand stream (profiles/r2_*).
+// configuration, 58% of it the operand stream (profiles/r2_*).
 // A 256 x 256 tile loads 256 + 256 operand rows per 256 x 256 outputs instead of 256 + 128 per
 // 256 x 128: two thirds of the operand bytes per flop.
 //
