@@ -1088,9 +1088,14 @@ int enqueue_k2(Workspace& w, const Job& j, cudaStream_t st, const EnqueueCtx& cx
     }
     pp.dbg = debug_flags();
     if (pp.dbg & 8) {
+        // [0, 16 * 1024): per-CTA role wait cycles; then (dbg & 4096) [items][12] event times
         static unsigned long long* prof = nullptr;
-        if (!prof) CK(cudaMallocManaged(&prof, sizeof(unsigned long long) * 16 * 2 * 512));
+        if (!prof) {
+            CK(cudaMallocManaged(&prof, sizeof(unsigned long long) * (16 * 1024 + 12 * 131072)));
+            CK(cudaMemset(prof, 0, sizeof(unsigned long long) * (16 * 1024 + 12 * 131072)));
+        }
         pp.prof = prof;
+        if (pp.dbg & 4096) pp.tl = prof + 16 * 1024;  // every launch overwrites its items' entries
         g_prof_buf = prof;
     }
     DevState* d;

@@ -45,6 +45,24 @@
 
 namespace ffg {
 
+#ifndef FFG_ROLE_PROF
+#define FFG_ROLE_PROF 0
+#endif
+// measurement builds: per-item event times (PairParams::tl)
+#define FFG_TL(item_, ev_)                                                                      \
+    do {                                                                                        \
+        if (FFG_ROLE_PROF && (p.dbg & 4096) && p.tl) {                                          \
+            unsigned long long t_;                                                              \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+            p.tl[(size_t)(item_) * 12 + (ev_)] = t_;                                             \
+        }                                                                                       \
+    } while (0)
+#define FFG_TLV(item_, ev_, v_)                                                                 \
+    do {                                                                                        \
+        if (FFG_ROLE_PROF && (p.dbg & 4096) && p.tl) p.tl[(size_t)(item_) * 12 + (ev_)] = (v_); \
+    } while (0)
+
+
 constexpr int kPairThreads = 640;
 // setmaxnreg budgets per warpgroup (control / drain / epilogue); they only redistribute the
 // launch allocation of 640 x 96 registers
@@ -180,6 +198,10 @@ struct PairParams {
                               // 16 skip operand loads, 32 skip hi/lo stores, 64 skip X/A
                               // stores (A: reductions), 128 skip X loads (all measurement only: results are wrong)
     unsigned long long* prof; // [gridDim][16] (dbg & 8)
+    unsigned long long* tl;   // [items][12] globaltimer per item (dbg & 4096, FFG_ROLE_PROF builds): producer
+                              // start, first operand load issued, last chunk drained, published, first
+                              // operands landed (MMA), last MMA issued, epilogue math done (S16), stores issued;
+                              // cumulative wait cycles: MMA full at the item's end and after its first stage, producer deps, empty
     int m0;                   // first matrix of this launch
     uint32_t zero;            // always 0: an opaque operand for scheduling dependencies (drain)
     uint32_t* products;       // [B] tensor-core product passes issued per matrix (instrumented count)
@@ -278,6 +300,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                 yacc[e + 1] = acc.y;
             }
         }
+        if (wk == 0 && lane == 0 && rank == 0) FFG_TL(item, 2);
         // ------------------------------------------------------------- epilogue of the item
         const uint32_t pr = __ldg(p.pairs + pi);
         const int R = rank ? (pr >> 10) & 1023 : pr & 1023;
@@ -323,6 +346,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                                                      gi, C * kBN, p.dbg & 64);
                     if (sub == 0) xq = xn;
                 }
+                if (wk == 0 && lane == 0 && rank == 0) FFG_TL(item, 6);
                 if (!(p.dbg & 32)) {
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -393,9 +417,11 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                     T1 += red[2 * w + 1];
                 }
                 p.partials[(size_t)m * 2 * p.PT + 2 * pi + rank] = make_double2(T0, T1);
+                if (rank == 0) FFG_TL(item, 3);
             }
         } else if (!dummy && l + 1 < p.l1) {
             // publish the block: hi/lo stores landed, X/A writes ordered -> block / panel counters
+            if (wk == 0 && lane == 0 && rank == 0) FFG_TL(item, 7);
             if (lane == 0) {
                 tma_store_wait_all();
                 fence_proxy_async_global();
@@ -409,6 +435,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
                     red_relaxed_gpu_add(p.bflags + (size_t)m * nb * nb + (R < C ? R * nb + C : C * nb + R), 1u);
                 red_relaxed_gpu_add(cm + R, 1u);
                 if (C != R) red_relaxed_gpu_add(cm + C, 1u);
+                if (rank == 0) FFG_TL(item, 3);
             }
         }
     }
@@ -417,9 +444,7 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
 
 // dbg & 8: accumulate the cycles a role spends in a wait into a register counter (measurement
 // builds only, -DFFG_ROLE_PROF=1: the counters cost registers in roles at the edge of their budget)
-#ifndef FFG_ROLE_PROF
-#define FFG_ROLE_PROF 0
-#endif
+
 #define FFG_TIMED(acc, stmt)                                     \
     do {                                                         \
         if (FFG_ROLE_PROF && (p.dbg & 8)) {                                         \
@@ -527,6 +552,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             for (int item = pair_id; item < total; item += n_pairs) {
                 int m, l, pi;
                 pair_decode(p, mm, item, m, l, pi);
+                if (rank == 0) FFG_TL(item, 0);
                 const uint32_t pr = __ldg(p.pairs + pi);
                 const int a0 = pr & 1023, a1 = (pr >> 10) & 1023, sp = (pr >> 20) & 1023;
                 const int ap = rank ? a1 : a0;
@@ -613,6 +639,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     } else {
                         tma_load_2d_pair(st + kPairOpA, &tm.b_hi[par], fbar, kb * kBK, rowB);
                     }
+                    if (kb == 0 && rank == 0) FFG_TL(item, 1);
+                }
+                if (rank == 0) {
+                    FFG_TLV(item, 10, w_dep);
+                    FFG_TLV(item, 11, w_empty);
                 }
             }
             if (FFG_ROLE_PROF && (p.dbg & 8)) {
@@ -681,6 +712,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 for (int kb = 0; kb < ((p.dbg & 2) ? 0 : nk); ++kb, ++it) {
                     const int s = it % S;
                     FFG_TIMED(w_full, mbar_wait_at(full_a + 8 * s, (it / S) & 1));
+                    if (kb == 0 && lane == 0) {
+                        FFG_TL(item, 4);
+                        FFG_TLV(item, 9, w_full);
+                    }
                     tc_fence_after();
                     const uint64_t sb = desc0 + (uint64_t)((s * Cfg::kStageBytes) >> 4);
                     if (kFixed) {
@@ -753,6 +788,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                     }
                     if (elect_one_sync()) umma_commit_pair(&empty[s]);
                     __syncwarp();
+                }
+                if (lane == 0) {
+                    FFG_TL(item, 5);
+                    FFG_TLV(item, 8, w_full);
                 }
                 if (kFixed) {
                     if (elect_one_sync()) {
