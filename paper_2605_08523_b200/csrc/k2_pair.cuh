@@ -196,7 +196,9 @@ struct PairParams {
     int dbg;                  // measurement only: 1 skip epilogue math, 2 skip loads/MMAs,
                               // 4 skip dependency waits, 8 per-role wait cycles -> prof,
                               // 16 skip operand loads, 32 skip hi/lo stores, 64 skip X/A
-                              // stores (A: reductions), 128 skip X loads (all measurement only: results are wrong)
+                              // stores (A: reductions), 128 skip X loads (all measurement only: results are wrong);
+                              // FFG_ROLE_PROF builds: 4096 per-item event times -> tl, 8192 16-worker drains
+                              // without TMEM reads
     unsigned long long* prof; // [gridDim][16] (dbg & 8)
     unsigned long long* tl;   // [items][12] globaltimer per item (dbg & 4096, FFG_ROLE_PROF builds): producer
                               // start, first operand load issued, last chunk drained, published, first
@@ -286,9 +288,14 @@ __device__ __forceinline__ void stream16_workers(const PairMaps& tm, const PairP
             mbar_wait_at(slot_full_a + 8 * sl, (g >> 2) & 1);
             tc_fence_after();
             uint32_t v[32];
-            tmem_ld_32x32b_x16(tl + sl * 128, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
-            tmem_ld_32x32b_x16(tl + sl * 128 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
-            tmem_ld_wait();
+            if (FFG_ROLE_PROF && (p.dbg & 8192)) {  // measurement: no TMEM reads (results wrong)
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] = 0u;
+            } else {
+                tmem_ld_32x32b_x16(tl + sl * 128, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                tmem_ld_32x32b_x16(tl + sl * 128 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                tmem_ld_wait();
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(slot_empty_l0 + 8 * sl);

@@ -10,27 +10,46 @@
 //       every two K-blocks
 //   P7  P6 + the K-block's operands rotating over three 48 KB stages
 //   P8  P7 + the issuer waits on a (completed) full barrier and fences per K-block, like the kernel
+// and P1 / P3 / P8 again with pseudo-random operand values (hi in [-1, 1], lo ~2^-11 of it) instead of zeros;
+// P8 with 16 more warps per CTA waiting on an mbarrier (spinning / suspend-hint try_wait), like the kernel's workers.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2605_08523_b200/csrc mma_acc_bench.cu
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include "ptx.cuh"
 using namespace ffg;
 
 constexpr uint32_t kAhi = 0, kAlo = 16384, kBhi = 32768, kBlo = 40960;
 
-template <int P>
-__global__ void __launch_bounds__(128, 1) acc_bench(int iters, unsigned long long* out) {
+template <int P, int FILL = 0, int SPIN = 0>
+__global__ void __launch_bounds__(640, 1) acc_bench(int iters, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar, ebar[3], sbar[4], fbar[3];
+    __shared__ uint64_t bar, ebar[3], sbar[4], fbar[3], never;
     __shared__ uint32_t slot;
+    __shared__ volatile int stop;
     const int warp = threadIdx.x >> 5;
     const uint32_t rank = cluster_ctarank();
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         for (int i = 0; i < 3; ++i) { mbar_init(&ebar[i], 1); mbar_init(&fbar[i], 1); }
         for (int i = 0; i < 4; ++i) mbar_init(&sbar[i], 1);
+        mbar_init(&never, 1);
+        stop = 0;
         fence_barrier_init();
+    }
+    if (FILL) {  // operands: pseudo-random binary16 values in [-1, 1] (hi) and ~2^-11 of that (lo)
+        uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+        for (int i = threadIdx.x; i < 3 * 49152 / 4; i += blockDim.x) {
+            uint32_t h = (uint32_t)i * 2654435761u + 12345u * (blockIdx.x + 1);
+            h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+            const float a = ((h & 0xffff) / 32768.0f) - 1.0f, b = ((h >> 16) / 32768.0f) - 1.0f;
+            const bool lo = ((i * 4) % 49152) >= 16384 && ((i * 4) % 49152) < 32768;
+            const __half2 v = __floats2half2_rn(lo ? a * 4.8828125e-4f : a, lo ? b * 4.8828125e-4f : b);
+            w[i] = *reinterpret_cast<const uint32_t*>(&v);
+        }
+        __syncthreads();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 1) tmem_alloc_pair(&slot, 512);
     tc_fence_before();
@@ -101,9 +120,21 @@ __global__ void __launch_bounds__(128, 1) acc_bench(int iters, unsigned long lon
         if (elect_one_sync()) umma_commit_pair(&bar);
         __syncwarp();
         mbar_wait(&bar, 0);
-        if (threadIdx.x == 0) out[blockIdx.x] = (unsigned long long)(clock64() - c0);
+        if (threadIdx.x == 0) {
+            out[blockIdx.x] = (unsigned long long)(clock64() - c0);
+            stop = 1;
+        }
     } else if (rank == 1 && warp == 0) {
         mbar_wait(&bar, 0);
+        if (threadIdx.x == 0) stop = 1;
+    } else if (warp >= 4) {
+        // the kernel's 16 worker warps waiting on a barrier (spin or suspend-hint try_wait) meanwhile
+        const uint32_t a = smem_u32(&never);
+        if (SPIN == 1) {
+            while (!stop) mbar_try_wait(a, 0);
+        } else if (SPIN == 2) {
+            while (!stop) mbar_try_wait_sleep(a, 0);
+        }
     }
     tc_fence_before();
     cluster_sync_all();
@@ -113,9 +144,9 @@ __global__ void __launch_bounds__(128, 1) acc_bench(int iters, unsigned long lon
     }
 }
 
-template <int P>
+template <int P, int FILL = 0, int SPIN = 0>
 void run(const char* name, int grid) {
-    auto k = acc_bench<P>;
+    auto k = acc_bench<P, FILL, SPIN>;
     const int smem = 160 * 1024;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     unsigned long long* out;
@@ -123,7 +154,7 @@ void run(const char* name, int grid) {
     const int iters = 2048;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(SPIN ? 640 : 128);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -163,6 +194,11 @@ int main() {
         run<6>("P6 P1 + per-K-block multicast commit + slot commit", grid);
         run<7>("P7 P6 + three rotating 48 KB stages", grid);
         run<8>("P8 P7 + full-barrier wait + fence per K-block", grid);
+        run<1, 1>("P1 with random operand data", grid);
+        run<3, 1>("P3 with random operand data", grid);
+        run<8, 1>("P8 with random operand data", grid);
+        run<8, 1, 1>("P8 + 16 warps spinning on try_wait", grid);
+        run<8, 1, 2>("P8 + 16 warps on suspend-hint try_wait", grid);
     }
     return 0;
 }
