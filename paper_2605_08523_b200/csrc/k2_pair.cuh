@@ -20,7 +20,7 @@
 // Single-matrix groups also track per-block completion (bflags) and a producer whose panels are
 // not complete yet waits per 128-column block just before loading it.
 //
-// Per CTA (640 threads, warp-specialised, setmaxnreg 48/104/112):
+// Per CTA (640 threads, warp-specialised, setmaxnreg 48/104/112; 16-worker variant 64/104):
 //   warp 0        TMA producer: A_hi, A_lo (128 x 64) of panel A_c and this CTA's half
 //                 (64 x 64) of B_hi, B_lo of panel S; complete_tx on the LEADER's full barrier
 //   warp 1        TMEM allocator (both CTAs) / UMMA issuer (leader only)
@@ -79,7 +79,13 @@ constexpr int kPRegsCtl = 48, kPRegsDrain = 96, kPRegsEpi = 120;
 static_assert(128 * kPRegsCtl + 256 * kPRegsDrain + 256 * kPRegsEpi <= 640 * 96, "setmaxnreg budget");
 // 16-worker variant: 16 worker warps (drain + epilogue) own 32 columns each of the CTA's block
 constexpr int kResWorkers = 16;
-constexpr int kRRegsCtl = 40, kRRegsWork = 104;
+#ifndef FFG_R_CTL
+// control warps' registers in the 16-worker variant: 64 (the whole 640 x 96 budget) keeps the producer's and
+// the MMA issuer's K-loop state out of local memory (measured against 40: N=1024 single -7%, 16 x N=1024
+// BF16 -2%)
+#define FFG_R_CTL 64
+#endif
+constexpr int kRRegsCtl = FFG_R_CTL, kRRegsWork = 104;
 static_assert(128 * kRRegsCtl + 512 * kRRegsWork <= 640 * 96, "setmaxnreg budget (16 workers)");
 constexpr int kPairHalf = kBN / 2;                  // B rows supplied by each CTA
 constexpr int kPairOpA = kBM * kBK * 2;             // 16 KB
