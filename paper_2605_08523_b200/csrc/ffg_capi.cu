@@ -484,7 +484,10 @@ bool use_wide(int mode, int nb, bool rowblock) {
     const char* e = getenv("FFG_WIDE");
     const bool ok = nb % 2 == 0 && !rowblock && (mode != kModeF32E || FFG_FIXED_SPLIT);
     if (e) return ok && atoi(e) != 0;
-    return ok && nb >= 16;
+    // N >= 4096: below it the 16-worker pair kernel is faster on every shape measured (N=2048 single
+    // FP32E 0.84 vs 1.55 ms, N=3072 2.26 vs 2.67 ms, 16 x N=2048 BF16 6.11 vs 6.44 ms); from N=4096 the wide
+    // kernel's operand economy wins (N=4096 FP32E 4.93 vs 5.02 ms, BF16 2.42 vs 2.64 ms)
+    return ok && nb >= 32;
 }
 
 // --------------------------------------------------------------------- small kernels
@@ -823,9 +826,12 @@ int launch_pair_mode(int mode, const PairMaps& maps, const PairParams& pp, int64
 bool use_s16(int mode, int64_t np, int64_t items_per_layer, int pairs) {
     const char* e = getenv("FFG_S16");
     if (e) return atoi(e) != 0;
-    // a layer with no more items than resident pairs is latency-bound: more epilogue parallelism
-    // pays; with two or more items per pair the MMA must keep running through the epilogues
-    return np <= 512 || (np <= 1024 && mode != kModeF32E) || items_per_layer <= pairs;
+    // the 16-worker epilogue (one 32-column piece per warp, sixteen in flight, 64-register control
+    // warps) wins wherever measured up to N=2048, batched or not (16 x N=1024 FP32E 1.88 vs 2.12 ms,
+    // 64 x N=1024 -9%, N=2048 single -15%; 16 x N=2048 FP32E +2%); beyond that only latency-bound
+    // layers (no more items than resident pairs) use it
+    (void)mode;
+    return np <= 2048 || items_per_layer <= pairs;
 }
 
 

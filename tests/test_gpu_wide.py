@@ -1,7 +1,7 @@
 """The wide K2 kernel (csrc/k2_wide.cuh: 256 x 256 super-block items, hi/lo blocks stored once and
 read MN-major for the mirrored orientation) against the fp64 recursion (-m gpu).
 
-The default for nb even and N >= 2048 (ffg_capi.cu use_wide); FFG_WIDE=1 forces it below that,
+The default for nb even and N >= 4096 (ffg_capi.cu use_wide); FFG_WIDE=1 forces it below that,
 FFG_WIDE=0 selects the pair kernel.  Gates are SURVEY.md 8(c), unchanged:
 
   MIXED_EMULATED: max|dD| <= 5e-6, ||dD||_F/||D||_F <= 1e-5, |dTr|/Tr <= 1e-6
@@ -59,7 +59,7 @@ def gate(mode, D, R, what):
 @pytest.mark.parametrize("mode", list(GATE))
 def test_wide_vs_fp64_recursion(torch, model, n, B, mode, monkeypatch):
     """Forced at N >= 1000 (nb even; 1000 pads to 1024, 1280 has an odd number of super-rows; the
-    default from N=2048): every member within the gates, D exactly symmetric, statistics consistent."""
+    default from N=4096): every member within the gates, D exactly symmetric, statistics consistent."""
     monkeypatch.setenv("FFG_WIDE", "1")
     mu, kT = batch_params(B)
     H = torch.from_numpy(np.stack([tight_binding(n, seed=300 + k) for k in range(B)])).cuda()
@@ -89,9 +89,9 @@ def test_wide_forced_small(torch, model, n, monkeypatch):
 
 def test_wide_and_pair_kernels_agree(torch, model, monkeypatch):
     """Both kernels evaluate the same recursion: at N=2048 their D differ only by rounding (both are
-    within the gates of the fp64 recursion) and the wide kernel is the default there."""
-    assert E.k2_kernel_name(2048) == "mlsp2_wide_kernel" and E.k2_kernel_name(1024) == "mlsp2_pair_kernel"
-    assert E.k2_kernel_name(2176) == "mlsp2_pair_kernel"  # nb = 17: no super-block tiling
+    within the gates of the fp64 recursion); the pair kernel is the default below N=4096."""
+    assert E.k2_kernel_name(4096) == "mlsp2_wide_kernel" and E.k2_kernel_name(2048) == "mlsp2_pair_kernel"
+    assert E.k2_kernel_name(4224) == "mlsp2_pair_kernel"  # nb = 33: no super-block tiling
     mu, kT = batch_params(2)
     H = torch.from_numpy(np.stack([tight_binding(2048, seed=70 + k) for k in range(2)])).cuda()
     Dd, _, _ = run(torch, H, mu, kT, model, E.PrecisionMode.MIXED_EMULATED)
@@ -99,7 +99,7 @@ def test_wide_and_pair_kernels_agree(torch, model, monkeypatch):
     Dw, _, _ = run(torch, H, mu, kT, model, E.PrecisionMode.MIXED_EMULATED)
     monkeypatch.setenv("FFG_WIDE", "0")
     Dp, _, _ = run(torch, H, mu, kT, model, E.PrecisionMode.MIXED_EMULATED)
-    assert torch.equal(Dd, Dw)              # the default at N=2048 is the wide kernel
+    assert torch.equal(Dd, Dp)              # the default at N=2048 is the pair kernel
     assert (Dw - Dp).abs().max().item() < 5e-6
     assert not torch.equal(Dw, Dp)          # (different accumulation schedules: not the same bits)
 
@@ -125,6 +125,7 @@ def test_wide_block_dependencies_bit_identical(torch, model, mode, monkeypatch):
     """Block-granular layer dependencies (single-matrix launches, FFG_BLOCKDEPS) only let an item's
     first K-blocks start before its whole super-rows are done: D and the statistics are bit-identical
     to the super-row-granular schedule."""
+    monkeypatch.setenv("FFG_WIDE", "1")
     H = torch.from_numpy(tight_binding(2048, seed=77)[None]).cuda()
     mu, kT = batch_params(1)
     out = {}
@@ -166,12 +167,13 @@ def test_wide_provenance_products(model, monkeypatch):
 
 @pytest.mark.parametrize("mode", [E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16])
 def test_wide_default_padded_size(torch, model, mode):
-    """The default selection at a padded size (n = 2300 -> np = 2304, 9 super-rows, 44 padded rows and
-    columns): wide kernel, within the gates, exactly symmetric; n = 2176 (odd block count) stays on the
-    pair kernel."""
-    assert E.k2_kernel_name(2300) == "mlsp2_wide_kernel" and E.k2_kernel_name(2176) == "mlsp2_pair_kernel"
-    H = torch.from_numpy(tight_binding(2300, seed=23)).cuda().unsqueeze(0)
+    """The default selection at a padded size (n = 4300 -> np = 4352, 17 super-rows, 52 padded rows and
+    columns): wide kernel, within the gates, exactly symmetric; n = 4200 (odd block count) and n = 2300
+    stay on the pair kernel."""
+    assert E.k2_kernel_name(4300) == "mlsp2_wide_kernel" and E.k2_kernel_name(4200) == "mlsp2_pair_kernel"
+    assert E.k2_kernel_name(2300) == "mlsp2_pair_kernel"
+    H = torch.from_numpy(tight_binding(4300, seed=23)).cuda().unsqueeze(0)
     D, stats, status = run(torch, H, [0.05], [0.011], model, mode)
     assert status.tolist() == [0] and torch.equal(D, D.transpose(1, 2))
     R = DR.density_matrices_f64(H, [0.05], [0.011], model.abcd, model.beta0, model.mu0)
-    gate(mode, D, R, "wide default N=2300")
+    gate(mode, D, R, "wide default N=4300")
