@@ -11,7 +11,8 @@
 //   P7  P6 + the K-block's operands rotating over three 48 KB stages
 //   P8  P7 + the issuer waits on a (completed) full barrier and fences per K-block, like the kernel
 // and P1 / P3 / P8 again with pseudo-random operand values (hi in [-1, 1], lo ~2^-11 of it) instead of zeros;
-// P8 with 16 more warps per CTA waiting on an mbarrier (spinning / suspend-hint try_wait), like the kernel's workers.
+// P8 with 16 more warps per CTA waiting on an mbarrier (spinning / suspend-hint try_wait), like the kernel's workers;
+// P10 / P11: the normal layers' chunks (a fresh accumulator every two K-blocks, rotating over four slots / one slot).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2605_08523_b200/csrc mma_acc_bench.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -97,6 +98,21 @@ __global__ void __launch_bounds__(640, 1) acc_bench(int iters, unsigned long lon
                         umma_f16_pair(t0a, D(kAlo, kk), D(kBhi, kk), idesc, 1u);
                         umma_f16_pair(t0a, D(kAhi, kk), D(kBhi, kk), idesc, 1u);
                     }
+                } else if (P == 10 || P == 11) {
+                    // chunked: a new accumulator slot (of four) every two K-blocks, overwritten by its
+                    // first MMA, committed to a slot barrier at the chunk's end (P11: one slot, same commits)
+                    const uint32_t st = (uint32_t)(i % 3) * 49152u;
+                    const uint32_t ta = P == 10 ? slot + ((i >> 1) & 3) * 128 : t0a;
+                    const bool first = (i & 1) == 0;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        umma_f16_pair(ta, D(st + kAhi, kk), D(st + kBlo, kk), idesc, (first && kk == 0) ? 0u : 1u);
+                        umma_f16_pair(ta, D(st + kAlo, kk), D(st + kBhi, kk), idesc, 1u);
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) umma_f16_pair(ta, D(st + kAhi, kk), D(st + kBhi, kk), idesc, 1u);
+                    if (i & 1) umma_commit_pair(&sbar[(i >> 1) & 3]);
+                    umma_commit_pair(&ebar[i % 3]);
                 } else if (P >= 6) {
                     const uint32_t st = P >= 7 ? (uint32_t)(i % 3) * 49152u : 0u;
 #pragma unroll
@@ -199,6 +215,8 @@ int main() {
         run<8, 1>("P8 with random operand data", grid);
         run<8, 1, 1>("P8 + 16 warps spinning on try_wait", grid);
         run<8, 1, 2>("P8 + 16 warps on suspend-hint try_wait", grid);
+        run<10, 1>("P10 chunks: new accumulator slot every 2 K-blocks", grid);
+        run<11, 1>("P11 chunks: one slot, overwrite every 2 K-blocks", grid);
     }
     return 0;
 }
