@@ -73,6 +73,22 @@ def test_validation_mirrors_reference():
         E.compute_density_matrices([np.eye(4), np.eye(5)], 0.0, 0.01, m)
 
 
+def test_kernel_selection(monkeypatch):
+    """The recursion kernel depends only on n and the mode (ffg_k2_kernel, host logic): the pair kernel
+    below N=4096 and for odd block counts, the wide kernel from N=4096 with an even block count;
+    FFG_WIDE overrides where the wide tiling applies."""
+    monkeypatch.delenv("FFG_WIDE", raising=False)
+    for mode in (E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16, E.PrecisionMode.FP16):
+        for n in (1, 256, 1000, 1024, 2048, 3072, 3968, 4200):
+            assert E.k2_kernel_name(n, mode) == "mlsp2_pair_kernel", (n, mode)
+        for n in (4000, 4096, 4300, 8192, 16384):  # 4000 pads to 4096
+            assert E.k2_kernel_name(n, mode) == "mlsp2_wide_kernel", (n, mode)
+    monkeypatch.setenv("FFG_WIDE", "1")
+    assert E.k2_kernel_name(1024) == "mlsp2_wide_kernel" and E.k2_kernel_name(4200) == "mlsp2_pair_kernel"
+    monkeypatch.setenv("FFG_WIDE", "0")
+    assert E.k2_kernel_name(8192) == "mlsp2_pair_kernel"
+
+
 def test_modes():
     """Every PrecisionMode of SPEC.md:308-311 is accepted (DOUBLE / SINGLE run the library-GEMM path);
     an unknown mode id is a validation error before any device work."""
