@@ -87,6 +87,21 @@ def test_config3_single_matrix_all_modes_vs_fp64_recursion(torch, model, n):
         del D
 
 
+@pytest.mark.parametrize("n,B", [(3000, 1), (2500, 2)])
+def test_pair_kernel_between_2048_and_4096_vs_fp64_recursion(torch, model, n, B):
+    """The selection band between the 16-worker pair kernel (np <= 2048) and the wide kernel (N >= 4096):
+    ragged sizes on the 8+8-warp pair kernel (np = 3072 / 2560, more items per layer than CTA pairs),
+    FP32-emulated, every element of D against the fp64 recursion; D exactly symmetric."""
+    assert E.k2_kernel_name(n) == "mlsp2_pair_kernel"
+    mu, kT = batch_params(B)
+    H = torch.from_numpy(np.stack([tight_binding(n, seed=2500 + k) for k in range(B)])).cuda()
+    R = DR.density_matrices_f64(H, mu, kT, model.abcd, model.beta0, model.mu0)
+    D, stats, status = run_device(torch, H, mu, kT, model, E.PrecisionMode.MIXED_EMULATED)
+    assert status.tolist() == [0] * B and torch.equal(D, D.transpose(1, 2))
+    mx, fro, tr = DR.errors(D, R)
+    gate(E.PrecisionMode.MIXED_EMULATED, mx, fro, tr, f"{B} x N={n}")
+
+
 @pytest.mark.parametrize("mode", [E.PrecisionMode.MIXED_EMULATED, E.PrecisionMode.BF16])
 def test_config4_all_512_members_vs_fp64_recursion(torch, model, mode):
     """configs[3]: the batch of 512 N=512 Hamiltonians (seeds 10000+k, mu_k ~ U(-0.5, 0.25),
